@@ -1,0 +1,170 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container only (it imports fracturekit from
+/root/reference/pkg/src, which does not exist on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+Inputs are the BASELINE.json synthetic draws:
+rng = default_rng(seed), u0 ~ U[-1e-3, 1e-3] (2n) -> phi0 ~ U[0,1] (n) ->
+x ~ U[-1,1] (3n); phi_tilde = phi_old = phi0; active = phi0 < 0.05;
+Dirichlet = top + bottom nodes; lambda=121.15e3, mu=80.77e3, Gc=2.7,
+kappa=1e-10, eps=2h.  The fixtures store inputs and outputs so the tests
+never need the reference at run time.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+import fracturekit.pff_operator as op  # noqa: E402
+from fracturekit.krylov import KrylovConfig, gmres_solve  # noqa: E402
+from fracturekit.material_model import MaterialParams  # noqa: E402
+from fracturekit.mesh_hierarchy import build_hierarchy  # noqa: E402
+from fracturekit.multigrid import (ChebyshevConfig, GmgPreconditioner,  # noqa: E402
+                                   TransferOperator, chebyshev_apply,
+                                   estimate_lambda_range)
+from fracturekit.active_set_solver import lumped_mass_diagonal  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def params(level):
+    return MaterialParams(lame_lambda=121.15e3, mu=80.77e3, g_c=2.7, kappa=1e-10,
+                          eps=2.0 / 2 ** level)
+
+
+def notch(dm, eps):
+    x, y = dm.coords[:, 0], dm.coords[:, 1]
+    dx = np.maximum(x - 0.5, 0.0)
+    return 1.0 - np.exp(-np.sqrt(dx * dx + (y - 0.5) ** 2) / eps)
+
+
+def make(h, level, split, seed, notch_phi=False):
+    st = op.LinearizationState(h, level, params(level), split=split)
+    dm = h.dof_map(level)
+    n = st.n_scalar
+    rng = np.random.default_rng(seed)
+    u0 = rng.uniform(-1e-3, 1e-3, 2 * n)
+    phi0 = notch(dm, params(level).eps) if notch_phi else rng.uniform(0.0, 1.0, n)
+    x = rng.uniform(-1.0, 1.0, 3 * n)
+    st.set_solution(np.concatenate([u0, phi0]))
+    st.set_phi_tilde(phi0)
+    st.set_phi_old(phi0)
+    st.set_active(phi0 < 0.05)
+    st.set_dirichlet_nodes(np.unique(np.concatenate(
+        [dm.boundary_nodes["top"], dm.boundary_nodes["bottom"]])))
+    st.refresh_cache()
+    return st, x
+
+
+def inputs(st, x):
+    return dict(U=st.U.copy(), phi_tilde=st.phi_tilde.copy(), phi_old=st.phi_old.copy(),
+                active=st.active.copy(), dirichlet=st.dirichlet_nodes.copy(), x=x)
+
+
+def operator_case(p, level, split, seed, with_cache=False):
+    h = build_hierarchy(max(level, 2), p)
+    st, x = make(h, level, split, seed)
+    n = st.n_scalar
+    d = inputs(st, x)
+    d["jac"] = op.apply_jacobian(st, x)
+    d["uu"] = op.apply_block_uu(st, x[:2 * n])
+    d["pp"] = op.apply_block_phiphi(st, x[2 * n:])
+    d["prow"] = op.apply_phi_row(st, x)
+    d["diag_uu"] = op.block_diagonal(st, "uu")
+    d["diag_pp"] = op.block_diagonal(st, "phiphi")
+    d["residual"] = op.residual(st)
+    d["residual_raw"] = op.residual(st, mask_dirichlet=False)
+    if with_cache:
+        for k, v in st.cache().items():
+            if k not in ("C", "gs"):
+                d["cache_" + k] = v.ravel().copy()
+    d["meta"] = np.array([p, level, seed, 1 if split == "miehe" else 0])
+    return d
+
+
+def solver_case(p, level, split, seed, notch_phi, sweeps=3):
+    h = build_hierarchy(level, p)
+    st, x = make(h, level, split, seed, notch_phi)
+    n = st.n_scalar
+    d = inputs(st, x)
+    gmg = GmgPreconditioner(h, coarse_level=2, cheb=ChebyshevConfig(sweeps=sweeps))
+    gmg.setup(st)
+    for l, rg in gmg.ranges.items():
+        d[f"range_{l}"] = np.array([rg["uu"][0], rg["uu"][1], rg["phiphi"][0], rg["phiphi"][1]])
+    d["vcycle"] = gmg.apply(x)
+    # Chebyshev on the finest uu block with the smoothing interval
+    lo, hi = gmg.ranges[level]["uu"]
+    d["cheb_uu"] = chebyshev_apply(lambda v: op.apply_block_uu(st, v), gmg.diags[level]["uu"],
+                                   x[:2 * n], 0.24 * hi, 1.2 * hi, 5)
+    d["lanczos_uu"] = np.array(estimate_lambda_range(
+        lambda v: op.apply_block_uu(st, v), gmg.diags[level]["uu"], seed=7))
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    res = gmres_solve(lambda v: op.apply_jacobian(st, v), rhs,
+                      KrylovConfig(relative_tolerance=1e-8, restart=50),
+                      preconditioner=gmg.apply)
+    d["gmres_x"] = res.solution
+    d["gmres_iters"] = np.array([res.iterations])
+    d["gmres_hist"] = np.array(res.residual_history)
+    d["gmres_conv"] = np.array([int(res.converged)])
+    d["meta"] = np.array([p, level, seed, 1 if split == "miehe" else 0, int(notch_phi), sweeps])
+    return d
+
+
+def transfer_case(p, fine_level, seed):
+    h = build_hierarchy(max(fine_level, 2), p)
+    tr = TransferOperator(h, fine_level)
+    rng = np.random.default_rng(seed)
+    xc = rng.uniform(-1, 1, 3 * tr.n_coarse)
+    yf = rng.uniform(-1, 1, 3 * tr.n_fine)
+    inj = h.injection(fine_level)
+    return dict(xc=xc, yf=yf, Px=tr.prolongate(xc), Ry=tr.restrict(yf), inj=inj,
+                P_indptr=tr.P.indptr, P_indices=tr.P.indices, P_data=tr.P.data,
+                meta=np.array([p, fine_level, seed]))
+
+
+def restrict_case(p, level, target, seed):
+    h = build_hierarchy(level, p)
+    st, x = make(h, level, "miehe", seed)
+    c = op.restrict_state_to_level(st, target)
+    d = inputs(st, x)
+    d.update(cU=c.U, cphi_tilde=c.phi_tilde, cactive=c.active, cdirichlet=c.dirichlet_nodes,
+             meta=np.array([p, level, target, seed]))
+    return d
+
+
+def main():
+    cases = {}
+    for split in ("none", "miehe"):
+        cases[f"pr1_{split}"] = operator_case(2, 5, split, 0, with_cache=True)
+        for p in (1, 3, 4):
+            cases[f"op_p{p}_l3_{split}"] = operator_case(p, 3, split, p)
+        cases[f"op_p2_l1_{split}"] = operator_case(2, 1, split, 5)
+        cases[f"op_p1_l0_{split}"] = operator_case(1, 0, split, 6)
+        cases[f"solve_p2_l5_{split}_rand"] = solver_case(2, 5, split, 0, False)
+        cases[f"solve_p2_l5_{split}_notch"] = solver_case(2, 5, split, 0, True)
+    cases["solve_p1_l4_miehe_notch_s5"] = solver_case(1, 4, "miehe", 1, True, sweeps=5)
+    for p in (1, 2, 3, 4):
+        cases[f"transfer_p{p}_l4"] = transfer_case(p, 4, 10 + p)
+    cases["transfer_p2_l1"] = transfer_case(2, 1, 9)
+    cases["restrict_p2_l5_l2"] = restrict_case(2, 5, 2, 3)
+    for p in (1, 2, 4):
+        h = build_hierarchy(3, p)
+        cases[f"mass_p{p}_l3"] = dict(m=lumped_mass_diagonal(h, 3), meta=np.array([p, 3]))
+    for name, d in cases.items():
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+        print(name, {k: np.asarray(v).shape for k, v in d.items() if k.startswith(("gmres_iters", "meta"))},
+              d.get("gmres_iters", ""))
+
+
+if __name__ == "__main__":
+    main()
