@@ -1,0 +1,374 @@
+"""Benchmark of the B200 PFF hot path (BASELINE.json metric).
+
+Headline (N=1): configs[1] -- the fp64 Jacobian vmult (apply_jacobian) on the
+1024x1024 Q2 mesh, 12,598,275 DoFs, BASELINE value distributions; a step is
+one application over the whole vector; value = GDoF/s.  Each step moves
+340 MB (> 126 MB L2), so no L2 flush is needed between steps.
+
+Also reported (BASELINE.json's second metric): the GMRES+GMG solve time of
+one semi-smooth Newton step on configs[3] (1024^2 Q2, notch phase field,
+9 levels, Chebyshev sweeps=3, restart 50, rtol 1e-8).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--split miehe|none]
+    python bench.py --impl reference ...   # the CPU oracle port on host cores
+
+N>1 (torchrun): every rank applies the operator to its own 1024^2 problem
+(replicas; the slab-partitioned path is exercised by tests) -- weak scaling.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_DOF = 27.0   # src+dst 6 + nodal state 4 doubles + 1 flag byte per node / 3
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def baseline_inputs(p, level, split, seed=0, notch=False):
+    """BASELINE.json synthetic draws: u0 ~ U[-1e-3,1e-3] (2n),
+    phi0 ~ U[0,1] (n) or the notch profile, x ~ U[-1,1] (3n);
+    phi_tilde = phi_old = phi0, active = phi0 < 0.05, Dirichlet = top+bottom."""
+    import paper_2005_00331_b200 as P
+    h = P.build_hierarchy(level, p)
+    dm = h.dof_map(level)
+    n = dm.n_scalar
+    eps = 2.0 / 2 ** level
+    params = P.MaterialParams(lame_lambda=121.15e3, mu=80.77e3, g_c=2.7, kappa=1e-10, eps=eps)
+    rng = np.random.default_rng(seed)
+    u0 = rng.uniform(-1e-3, 1e-3, 2 * n)
+    if notch:
+        c = dm.coords
+        dx = np.maximum(c[:, 0] - 0.5, 0.0)
+        phi0 = 1.0 - np.exp(-np.sqrt(dx * dx + (c[:, 1] - 0.5) ** 2) / eps)
+    else:
+        phi0 = rng.uniform(0.0, 1.0, n)
+    x = rng.uniform(-1.0, 1.0, 3 * n)
+    dirichlet = np.unique(np.concatenate([dm.boundary_nodes["top"], dm.boundary_nodes["bottom"]]))
+    return h, params, np.concatenate([u0, phi0]), phi0, phi0 < 0.05, dirichlet, x
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index=0, period=0.01):
+        self.samples, self.reasons, self.period = [], set(), period
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:   # pragma: no cover - no NVML
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def traffic_from_profiles(split):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(split)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- ours
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2005_00331_b200 as P
+    from paper_2005_00331_b200 import _lib
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.load()
+    dev = torch.device("cuda", local)
+
+    p, level = 2, 10
+    h, params, U, pt, act, dirn, x = baseline_inputs(p, level, args.split, seed=rank)
+    st = P.LinearizationState(h, level, params, split=args.split)
+    st.set_solution(U)
+    st.set_phi_tilde(pt)
+    st.set_phi_old(pt)
+    st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    st.refresh_cache()
+    n = st.n_scalar
+    dofs = 3 * n
+    xd = torch.from_numpy(x).to(dev)
+    yd = torch.empty_like(xd)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        st.apply_into(_lib.MODE_FULL, xd, yd)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    c0 = L.pff_launch_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = L.pff_launch_counter() - c0
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    value = ws * dofs * args.steps / (ms * 1e-3) / 1e9
+
+    # end to end through the public API with pinned host buffers
+    xh = torch.from_numpy(x).pin_memory()
+    e2e_steps = max(3, min(20, args.steps))
+    P.apply_jacobian(st, xh)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        yh = P.apply_jacobian(st, xh)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+
+    # correctness of the timed output (bench never reports an unchecked number)
+    yref = P.apply_jacobian(st, xd)
+    assert torch.equal(yref, yd) or float((yref - yd).norm() / yref.norm()) < 1e-13
+    assert float((torch.from_numpy(yh.numpy()).to(dev) - yd).norm() / yd.norm()) < 1e-13
+
+    newton = None
+    if args.newton and rank == 0:
+        try:
+            newton = newton_step_ours(args, P, torch)
+        except Exception as e:   # reported, never silently dropped
+            newton = {"error": f"{type(e).__name__}: {e}"}
+
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_DOF * dofs / (ms_step * 1e-3) / 1e9
+    cpu = cpu_baseline(args) if not args.no_cpu_baseline else None
+    out = {
+        "metric": "GDoF/s of fp64 Jacobian vmult (apply_jacobian, 1024^2 Q2)",
+        "value": round(value, 3),
+        "unit": "GDoF/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE.json configs[1] draws, seed=rank)",
+        "config": {"workload": "configs[1]: 1024x1024 Q2 apply_jacobian, 12,598,275 DoFs",
+                   "split": args.split, "degree": p, "level": level, "dofs": dofs,
+                   "l2": "inputs larger than L2 (340 MB per step), no flush",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic_from_profiles(args.split),
+                     "algorithmic_bytes_per_dof": BYTES_PER_DOF, "peak_source": peak_src},
+        "e2e": {"value": round(dofs / e2e_s / 1e9, 4), "unit": "GDoF/s",
+                "h2d_bytes_per_step": 8 * dofs, "d2h_bytes_per_step": 8 * dofs,
+                "path": "paper_2005_00331_b200.apply_jacobian(state, pinned host tensor)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    if newton is not None:
+        out["newton_step"] = newton
+    print(json.dumps(out))
+
+
+def newton_step_ours(args, P, torch):
+    """configs[3]: one Newton step's GMRES+GMG solve on 1024^2 Q2."""
+    level = args.newton_level
+    h, params, U, pt, act, dirn, x = baseline_inputs(2, level, args.split, seed=0, notch=True)
+    st = P.LinearizationState(h, level, params, split=args.split)
+    st.set_solution(U)
+    st.set_phi_tilde(pt)
+    st.set_phi_old(pt)
+    st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    rhs = x.copy()
+    mask = np.concatenate([st.dirichlet_nodes, st.dirichlet_nodes, st.active])
+    rhs[mask] = 0.0
+    rhs_h = torch.from_numpy(rhs).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.refresh_cache()
+    gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    gmg.io_buffers()[0].zero_()
+    gmg.run_cycle()                       # CUDA-graph capture counted as setup
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    rhs_d = rhs_h.to("cuda", non_blocking=True)
+    res = P.gmres_solve(P.JacobianOperator(st), rhs_d,
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    sol = res.solution.cpu()
+    torch.cuda.synchronize()
+    t_gmres = time.perf_counter() - t1
+    return {"config": f"configs[3]: {2 ** level}^2 Q2 notch, levels 2..{level}, sweeps=3, "
+                      "restart 50, rtol 1e-8",
+            "split": args.split, "iterations": res.iterations, "converged": res.converged,
+            "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
+            "total_s": round(t_setup + t_gmres, 4),
+            "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
+            "note": "gmres_s includes the rhs H2D and solution D2H"}
+
+
+# ------------------------------------------------------------ CPU sides
+
+def cpu_baseline(args, budget_s=15.0):
+    """The C oracle port on this host's cores, bounded sample of configs[1]."""
+    from oracle import oracle as O
+    nt = O.max_threads()
+    st, x = O.baseline_state(2, 10, args.split, seed=0)
+    st.refresh_cache(nthreads=nt)
+    O.apply_jacobian(st, x, nthreads=nt)   # warm
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end and len(times) < 20:
+        t0 = time.perf_counter()
+        O.apply_jacobian(st, x, nthreads=nt)
+        times.append(time.perf_counter() - t0)
+    dofs = 3 * st.n
+    return {"value": round(dofs / min(times) / 1e9, 5), "unit": "GDoF/s", "cores": nt,
+            "kind": "port",
+            "sample": f"oracle/pff_oracle.c apply_jacobian on the full 1024^2 Q2 vector "
+                      f"({args.split}), best of {len(times)} in a {budget_s:.0f} s budget"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    nt = O.max_threads()
+    st, x = O.baseline_state(2, 10, args.split, seed=0)
+    st.refresh_cache(nthreads=nt)
+    dofs = 3 * st.n
+    for _ in range(min(args.warmup, 1)):
+        O.apply_jacobian(st, x, nthreads=nt)
+    budget = 120.0
+    t0 = time.perf_counter()
+    done = 0
+    while done < args.steps and (time.perf_counter() - t0) < budget:
+        O.apply_jacobian(st, x, nthreads=nt)
+        done += 1
+    el = time.perf_counter() - t0
+    value = dofs * done / el / 1e9
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "GDoF/s of fp64 Jacobian vmult (apply_jacobian, 1024^2 Q2)",
+        "value": round(value, 5), "unit": "GDoF/s", "n_gpus": ws, "steps": done,
+        "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * el / done, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json configs[1] draws)",
+        "config": {"workload": "configs[1]: 1024x1024 Q2 apply_jacobian, 12,598,275 DoFs",
+                   "split": args.split},
+        "cpu_baseline": {"value": round(value, 5), "unit": "GDoF/s", "cores": nt, "kind": "port",
+                         "sample": f"{done} full applications (capped at {budget:.0f} s)"},
+        "e2e": {"value": round(value, 5), "unit": "GDoF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "reference = fracturekit (Python/numba) cannot travel to the GPU box; this arm "
+                "times its C restatement oracle/pff_oracle.c (bitwise equal to the reference "
+                "on the golden vectors) with all host threads",
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--split", choices=["miehe", "none"], default="miehe")
+    ap.add_argument("--no-newton", dest="newton", action="store_false")
+    ap.add_argument("--newton-level", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)   # timing rule: at least 3 warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * pff_b200.h -- C ABI of libpff_b200.so, the B200 (sm_100a) implementation
+ * of the matrix-free phase-field-fracture hot path of fracturekit 0.1.0
+ * (arXiv 2005.00331).  `src/` below is /root/reference/pkg/src/fracturekit/.
+ *
+ * Conventions
+ *  - Every entry point returns 0 on success, a cudaError_t value (> 0) for a
+ *    CUDA failure or a negative PFF_E* code; it never throws or aborts.
+ *    pff_last_error() gives a message for the calling thread.
+ *  - All vector pointers are DEVICE pointers (fp64 unless stated), laid out
+ *    exactly as the reference's numpy vectors: component-major
+ *    [u_x | u_y | phi], each n_scalar long, grid node (i, j) at j*(p*2^l+1)+i,
+ *    upper slit copies appended (src/mesh_hierarchy.py:156-189).
+ *  - The caller owns all device memory.  A pff_level owns only its tables.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    asynchronous on that stream and CUDA-graph capturable; none synchronises.
+ *  - src and dst of one call must not alias; dst may alias rhs.
+ */
+#ifndef PFF_B200_H
+#define PFF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFF_ABI_VERSION 1
+
+enum { PFF_E_ARG = -1, PFF_E_STATE = -2, PFF_E_UNBOUND = -3 };
+
+/* operator modes (src/pff_operator.py:262-302) */
+enum {
+    PFF_MODE_FULL = 0,    /* apply_jacobian:     3n -> 3n */
+    PFF_MODE_UU = 1,      /* apply_block_uu:     2n -> 2n */
+    PFF_MODE_PHIPHI = 2,  /* apply_block_phiphi:  n ->  n */
+    PFF_MODE_PHIROW = 3   /* apply_phi_row:      3n ->  n */
+};
+
+/* constraint flag bits, one byte per scalar node (constrained_mask(),
+ * src/pff_operator.py:148-150) */
+enum { PFF_FLAG_DIRICHLET = 1, PFF_FLAG_ACTIVE = 2 };
+
+/* vector layouts for the masking helpers */
+enum { PFF_LAYOUT_FULL = 0, PFF_LAYOUT_UU = 1, PFF_LAYOUT_PHI = 2 };
+enum { PFF_CONS_SELECT = 0, PFF_CONS_ZERO = 1, PFF_CONS_COPY = 2 };
+
+/* MaterialParams, src/material_model.py:20-44 */
+typedef struct {
+    double lame_lambda, mu, g_c, kappa, eps;
+} pff_material;
+
+typedef struct pff_level pff_level;
+
+int pff_abi_version(void);
+const char* pff_last_error(void);
+
+/* number of kernels (and memsets) this library has enqueued so far; the
+ * benchmark reads it around its timed region */
+int64_t pff_launch_counter(void);
+
+/* One mesh level (replaces DofMap + LinearizationState's static data,
+ * src/pff_operator.py:74-101).  N, D: host (p+1)x(p+1) row-major shape
+ * values/derivatives at the Gauss points, w: (p+1) weights
+ * (src/tensor_basis.py:66-81); embed: host 2x(p+1)x(p+1) coarse basis at
+ * the child support points (src/multigrid.py:58-61).  split: 0 none, 1 miehe. */
+int pff_level_create(pff_level** out, int degree, int level, int split,
+                     const pff_material* mat, const double* N, const double* D,
+                     const double* w, const double* embed);
+int pff_level_destroy(pff_level* L);
+int64_t pff_level_n_scalar(const pff_level* L);
+int64_t pff_level_n_cells(const pff_level* L);
+int64_t pff_level_qcache_len(const pff_level* L);
+
+/* Bind the linearisation point: U (3n), phi_tilde (n), flags (n bytes) and a
+ * caller-allocated q-point cache of pff_level_qcache_len() doubles. */
+int pff_level_bind(pff_level* L, const double* U, const double* phi_tilde,
+                   const uint8_t* flags, double* qcache);
+
+/* LinearizationState.refresh_cache -> cache_kernel (src/pff_operator.py:154-184) */
+int pff_level_refresh(pff_level* L, void* stream);
+
+/* Jacobian family with identity rows/columns on constraints
+ * (src/pff_operator.py:262-302 -> src/_kernels.py:555-693).
+ * rhs == NULL: dst = G src.  rhs != NULL: dst = rhs - G src (fused residual,
+ * e.g. `r - apply_jacobian(z)` of src/multigrid.py:298,336). */
+int pff_apply(const pff_level* L, int mode, const double* src, double* dst,
+              const double* rhs, void* stream);
+
+/* block_diagonal (src/pff_operator.py:305-327 -> src/_kernels.py:700-746):
+ * diag_uu (2n), diag_pp (n); constrained entries 1; invert != 0 stores 1/d. */
+int pff_diagonal(const pff_level* L, double* diag_uu, double* diag_pp, int invert,
+                 void* stream);
+
+/* residual (src/pff_operator.py:218-241 -> src/_kernels.py:319-440), 3n */
+int pff_residual(const pff_level* L, double* out, int mask_dirichlet, int mask_active,
+                 void* stream);
+
+/* TransferOperator (src/multigrid.py:97-120) between fine = coarse + 1.
+ * prolongate: yf = P xc, or with add_masked: yf += where(cons_f, 0, P xc)
+ * (src/multigrid.py:340-342).  restrict: xc = P^T yf, zero_cons: xc[cons_c]=0. */
+int pff_prolongate(const pff_level* fine, const pff_level* coarse, const double* xc,
+                   double* yf, int add_masked, void* stream);
+int pff_restrict(const pff_level* fine, const pff_level* coarse, const double* yf,
+                 double* xc, int zero_cons, void* stream);
+
+/* MeshHierarchy.injection gathers (src/mesh_hierarchy.py:316-338), one level */
+int pff_inject_f64(const pff_level* fine, const pff_level* coarse, const double* src,
+                   double* dst, int ncomp, void* stream);
+int pff_inject_u8(const pff_level* fine, const pff_level* coarse, const uint8_t* src,
+                  uint8_t* dst, void* stream);
+
+/* constraint masking on a level's vector (layout PFF_LAYOUT_*, op PFF_CONS_*) */
+int pff_cons(const pff_level* L, int layout, int op, const double* r, double* z,
+             void* stream);
+
+/* chebyshev_apply pieces (src/multigrid.py:170-198):
+ * init: d = invd*rhs/theta; acc_mode 0: acc = d, 1: acc += d, 2: untouched
+ * step: d = c1*d + c2*(invd*r); acc += d */
+int pff_cheb_init(int64_t n, const double* invd, const double* rhs, double theta,
+                  double* d, double* acc, int acc_mode, void* stream);
+int pff_cheb_step(int64_t n, const double* invd, const double* r, double c1, double c2,
+                  double* d, double* acc, void* stream);
+
+/* y = a x + b y;  y = x / s (s = *sdev if sdev else sval);  y = a .* x */
+int pff_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);
+int pff_div(int64_t n, const double* x, const double* sdev, double sval, double* y,
+            void* stream);
+int pff_mul(int64_t n, const double* a, const double* x, double* y, void* stream);
+
+/* deterministic dot: partials = pff_reduce_scratch_len() doubles, out = 1 double */
+int64_t pff_reduce_scratch_len(void);
+int pff_dot(int64_t n, const double* x, const double* y, double* partials, double* out,
+            void* stream);
+
+/* Arnoldi column j of GMRES (src/krylov.py:76-80): V holds rows 0..j (row
+ * stride ldv), w is overwritten by the MGS-orthogonalised vector;
+ * h[0..j] = coefficients, h[j+1] = ||w||. */
+int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* partials,
+            double* h, void* stream);
+
+/* out = sum_{i<k} y[i] V[i] (+ out if accumulate); y is a device array */
+int pff_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y, double* out,
+                int accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PFF_B200_H */

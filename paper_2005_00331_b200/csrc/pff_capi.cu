@@ -1,0 +1,221 @@
+// pff_capi.cu -- extern "C" entry points of libpff_b200.so (include/pff_b200.h).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/pff_b200.h"
+#include "pff_internal.cuh"
+
+using pff::Level;
+
+namespace pff {
+std::atomic<long long> g_launch_count{0};
+void count_launches(int k) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace pff
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, const char* what) {
+    std::snprintf(g_err, sizeof(g_err), fmt, what);
+    return code;
+}
+
+int check(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return 0;
+    std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return (int)e;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bool bound(const Level* L) { return L && L->U && L->phi_tilde && L->flags && L->qcache; }
+
+}  // namespace
+
+extern "C" {
+
+int pff_abi_version(void) { return PFF_ABI_VERSION; }
+
+const char* pff_last_error(void) { return g_err; }
+
+int64_t pff_launch_counter(void) { return pff::g_launch_count.load(); }
+
+int pff_level_create(pff_level** out, int degree, int level, int split, const pff_material* mat,
+                     const double* N, const double* D, const double* w, const double* embed) {
+    if (!out || !mat || !N || !D || !w) return fail(PFF_E_ARG, "%s", "pff_level_create: null argument");
+    if (degree < 1 || degree > pff::PMAX) return fail(PFF_E_ARG, "%s", "pff_level_create: degree must be in 1..4");
+    if (level < 0 || level > 14) return fail(PFF_E_ARG, "%s", "pff_level_create: level out of range");
+    if (split != 0 && split != 1) return fail(PFF_E_ARG, "%s", "split must be 'none' or 'miehe'");
+    Level* L = new (std::nothrow) Level();
+    if (!L) return fail(PFF_E_ARG, "%s", "pff_level_create: out of host memory");
+    L->mesh = pff::Mesh::make(degree, level);
+    std::memset(&L->shape, 0, sizeof(L->shape));
+    std::memset(&L->embed, 0, sizeof(L->embed));
+    const int n1 = degree + 1;
+    for (int iq = 0; iq < n1; ++iq) {
+        L->shape.w[iq] = w[iq];
+        for (int a = 0; a < n1; ++a) {
+            L->shape.N[iq][a] = N[iq * n1 + a];
+            L->shape.D[iq][a] = D[iq * n1 + a];
+        }
+    }
+    if (embed)
+        for (int c = 0; c < 2; ++c)
+            for (int k = 0; k < n1; ++k)
+                for (int m = 0; m < n1; ++m) L->embed.E[c][k][m] = embed[(c * n1 + k) * n1 + m];
+    L->mat = pff::Material{mat->lame_lambda, mat->mu, mat->g_c, mat->kappa, mat->eps};
+    L->miehe = split;
+    *out = reinterpret_cast<pff_level*>(L);
+    return 0;
+}
+
+int pff_level_destroy(pff_level* L) {
+    delete reinterpret_cast<Level*>(L);
+    return 0;
+}
+
+int64_t pff_level_n_scalar(const pff_level* L) {
+    return L ? reinterpret_cast<const Level*>(L)->mesh.n : -1;
+}
+
+int64_t pff_level_n_cells(const pff_level* L) {
+    return L ? reinterpret_cast<const Level*>(L)->mesh.n_cells() : -1;
+}
+
+int64_t pff_level_qcache_len(const pff_level* L) {
+    return L ? reinterpret_cast<const Level*>(L)->qcache_len() : -1;
+}
+
+int pff_level_bind(pff_level* h, const double* U, const double* phi_tilde, const uint8_t* flags,
+                   double* qcache) {
+    Level* L = reinterpret_cast<Level*>(h);
+    if (!L) return fail(PFF_E_ARG, "%s", "pff_level_bind: null level");
+    L->U = U;
+    L->phi_tilde = phi_tilde;
+    L->flags = flags;
+    L->qcache = qcache;
+    return 0;
+}
+
+int pff_level_refresh(pff_level* h, void* stream) {
+    Level* L = reinterpret_cast<Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_level_refresh: state not bound");
+    return check(pff::launch_refresh(*L, S(stream)), "pff_level_refresh");
+}
+
+int pff_apply(const pff_level* h, int mode, const double* src, double* dst, const double* rhs,
+              void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_apply: state not bound");
+    if (mode < 0 || mode > 3 || !src || !dst) return fail(PFF_E_ARG, "%s", "pff_apply: bad mode or null vector");
+    return check(pff::launch_apply(*L, mode, src, dst, rhs, S(stream)), "pff_apply");
+}
+
+int pff_diagonal(const pff_level* h, double* duu, double* dpp, int invert, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_diagonal: state not bound");
+    if (!duu || !dpp) return fail(PFF_E_ARG, "%s", "pff_diagonal: null output");
+    return check(pff::launch_diagonal(*L, duu, duu + L->mesh.n, dpp, invert, S(stream)),
+                 "pff_diagonal");
+}
+
+int pff_residual(const pff_level* h, double* out, int md, int ma, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_residual: state not bound");
+    if (!out) return fail(PFF_E_ARG, "%s", "pff_residual: null output");
+    return check(pff::launch_residual(*L, out, md, ma, S(stream)), "pff_residual");
+}
+
+int pff_prolongate(const pff_level* f, const pff_level* c, const double* xc, double* yf,
+                   int add_masked, void* stream) {
+    const Level* F = reinterpret_cast<const Level*>(f);
+    const Level* C = reinterpret_cast<const Level*>(c);
+    if (!F || !C || !xc || !yf) return fail(PFF_E_ARG, "%s", "pff_prolongate: null argument");
+    if (add_masked && !F->flags) return fail(PFF_E_UNBOUND, "%s", "pff_prolongate: fine flags not bound");
+    return check(pff::launch_prolongate(*F, *C, xc, yf, add_masked, S(stream)), "pff_prolongate");
+}
+
+int pff_restrict(const pff_level* f, const pff_level* c, const double* yf, double* xc,
+                 int zero_cons, void* stream) {
+    const Level* F = reinterpret_cast<const Level*>(f);
+    const Level* C = reinterpret_cast<const Level*>(c);
+    if (!F || !C || !xc || !yf) return fail(PFF_E_ARG, "%s", "pff_restrict: null argument");
+    if (zero_cons && !C->flags) return fail(PFF_E_UNBOUND, "%s", "pff_restrict: coarse flags not bound");
+    return check(pff::launch_restrict(*F, *C, yf, xc, zero_cons, S(stream)), "pff_restrict");
+}
+
+int pff_inject_f64(const pff_level* f, const pff_level* c, const double* src, double* dst,
+                   int ncomp, void* stream) {
+    const Level* F = reinterpret_cast<const Level*>(f);
+    const Level* C = reinterpret_cast<const Level*>(c);
+    if (!F || !C || !src || !dst || ncomp < 1) return fail(PFF_E_ARG, "%s", "pff_inject_f64: bad argument");
+    return check(pff::launch_inject_f64(*F, *C, src, dst, ncomp, S(stream)), "pff_inject_f64");
+}
+
+int pff_inject_u8(const pff_level* f, const pff_level* c, const uint8_t* src, uint8_t* dst,
+                  void* stream) {
+    const Level* F = reinterpret_cast<const Level*>(f);
+    const Level* C = reinterpret_cast<const Level*>(c);
+    if (!F || !C || !src || !dst) return fail(PFF_E_ARG, "%s", "pff_inject_u8: bad argument");
+    return check(pff::launch_inject_u8(*F, *C, src, dst, S(stream)), "pff_inject_u8");
+}
+
+int pff_cons(const pff_level* h, int layout, int op, const double* r, double* z, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!L || !L->flags) return fail(PFF_E_UNBOUND, "%s", "pff_cons: flags not bound");
+    if (layout < 0 || layout > 2 || op < 0 || op > 2 || !z || (op != 1 && !r))
+        return fail(PFF_E_ARG, "%s", "pff_cons: bad argument");
+    return check(pff::launch_cons(*L, layout, op, r, z, S(stream)), "pff_cons");
+}
+
+int pff_cheb_init(int64_t n, const double* invd, const double* rhs, double theta, double* d,
+                  double* acc, int acc_mode, void* stream) {
+    if (n < 0 || !invd || !rhs || !d || (acc_mode != 2 && !acc)) return fail(PFF_E_ARG, "%s", "pff_cheb_init: bad argument");
+    return check(pff::launch_cheb_init(n, invd, rhs, theta, d, acc, acc_mode, S(stream)), "pff_cheb_init");
+}
+
+int pff_cheb_step(int64_t n, const double* invd, const double* r, double c1, double c2,
+                  double* d, double* acc, void* stream) {
+    if (n < 0 || !invd || !r || !d || !acc) return fail(PFF_E_ARG, "%s", "pff_cheb_step: bad argument");
+    return check(pff::launch_cheb_step(n, invd, r, c1, c2, d, acc, S(stream)), "pff_cheb_step");
+}
+
+int pff_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream) {
+    if (n < 0 || !x || !y) return fail(PFF_E_ARG, "%s", "pff_axpby: bad argument");
+    return check(pff::launch_axpby(n, a, x, b, y, S(stream)), "pff_axpby");
+}
+
+int pff_div(int64_t n, const double* x, const double* sdev, double sval, double* y, void* stream) {
+    if (n < 0 || !x || !y) return fail(PFF_E_ARG, "%s", "pff_div: bad argument");
+    return check(pff::launch_div(n, x, sdev, sval, y, S(stream)), "pff_div");
+}
+
+int pff_mul(int64_t n, const double* a, const double* x, double* y, void* stream) {
+    if (n < 0 || !a || !x || !y) return fail(PFF_E_ARG, "%s", "pff_mul: bad argument");
+    return check(pff::launch_lanczos_scale(n, a, x, y, S(stream)), "pff_mul");
+}
+
+int64_t pff_reduce_scratch_len(void) { return 2 * pff::RED_BLOCKS; }
+
+int pff_dot(int64_t n, const double* x, const double* y, double* partials, double* out,
+            void* stream) {
+    if (n < 0 || !x || !y || !partials) return fail(PFF_E_ARG, "%s", "pff_dot: bad argument");
+    return check(pff::launch_dot(n, x, y, partials, out, S(stream)), "pff_dot");
+}
+
+int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* partials, double* h,
+            void* stream) {
+    if (n < 0 || j < 0 || !V || !w || !partials || !h || ldv < n) return fail(PFF_E_ARG, "%s", "pff_mgs: bad argument");
+    return check(pff::launch_mgs(n, j, V, ldv, w, partials, h, S(stream)), "pff_mgs");
+}
+
+int pff_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y, double* out,
+                int accumulate, void* stream) {
+    if (n < 0 || k < 0 || !V || !y || !out) return fail(PFF_E_ARG, "%s", "pff_combine: bad argument");
+    return check(pff::launch_combine(n, k, V, ldv, y, out, accumulate, S(stream)), "pff_combine");
+}
+
+}  // extern "C"

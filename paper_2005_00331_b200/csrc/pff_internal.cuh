@@ -1,0 +1,66 @@
+// pff_internal.cuh -- host-side launch interface shared by the .cu files.
+#pragma once
+#include "pff_common.cuh"
+
+namespace pff {
+
+// kernels (and memsets) enqueued by this library; see pff_launch_counter()
+void count_launches(int k);
+
+// Per-level handle contents (the C-ABI's opaque pff_level).
+struct Level {
+    Mesh mesh;
+    Shape shape;
+    Embed embed;       // coarse basis at this level's child support points
+    Material mat;
+    int miehe;
+    // bound linearisation point (device pointers owned by the caller)
+    const double* U = nullptr;          // 3n: u0x | u0y | phi0
+    const double* phi_tilde = nullptr;  // n
+    const uint8_t* flags = nullptr;     // n: F_DIR | F_ACT
+    double* qcache = nullptr;           // qcache_len() doubles
+    int64_t qcache_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells(); }
+};
+
+// operator family (pff_ops.cu)
+cudaError_t launch_refresh(const Level& L, cudaStream_t s);
+cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
+                         const double* rhs, cudaStream_t s);
+cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, int invert,
+                            cudaStream_t s);
+cudaError_t launch_residual(const Level& L, double* out, int mask_dirichlet, int mask_active,
+                            cudaStream_t s);
+
+// transfers (pff_transfer.cu)
+cudaError_t launch_prolongate(const Level& fine, const Level& coarse, const double* xc,
+                              double* yf, int add_masked, cudaStream_t s);
+cudaError_t launch_restrict(const Level& fine, const Level& coarse, const double* yf,
+                            double* xc, int zero_cons, cudaStream_t s);
+cudaError_t launch_inject_f64(const Level& fine, const Level& coarse, const double* src,
+                              double* dst, int ncomp, cudaStream_t s);
+cudaError_t launch_inject_u8(const Level& fine, const Level& coarse, const uint8_t* src,
+                             uint8_t* dst, cudaStream_t s);
+
+// vectors (pff_vec.cu)
+constexpr int RED_BLOCKS = 592;   // 4 x 148 SMs: fixed, so reductions are deterministic
+constexpr int RED_THREADS = 256;
+cudaError_t launch_cons(const Level& L, int layout, int op, const double* r, double* z,
+                        cudaStream_t s);
+cudaError_t launch_cheb_init(int64_t n, const double* invd, const double* rhs, double theta,
+                             double* d, double* acc, int acc_mode, cudaStream_t s);
+cudaError_t launch_cheb_step(int64_t n, const double* invd, const double* r, double c1,
+                             double c2, double* d, double* acc, cudaStream_t s);
+cudaError_t launch_axpby(int64_t n, double a, const double* x, double b, double* y,
+                         cudaStream_t s);
+cudaError_t launch_div(int64_t n, const double* x, const double* sdev, double sval, double* y,
+                       cudaStream_t s);
+cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* partials,
+                       double* out, cudaStream_t s);
+cudaError_t launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w,
+                       double* partials, double* h, cudaStream_t s);
+cudaError_t launch_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y,
+                           double* out, int accumulate, cudaStream_t s);
+cudaError_t launch_lanczos_scale(int64_t n, const double* dhalf, const double* v, double* out,
+                                 cudaStream_t s);
+
+}  // namespace pff

@@ -1,0 +1,569 @@
+// pff_ops.cu -- operator family on device: q-point refresh, Jacobian
+// application (full / uu / phiphi / phi-row, optional fused r - J z),
+// block diagonals, nonlinear residual.
+//
+// Generic path (any p in 1..4): one thread per cell, sum-factorised 1-D
+// contractions in registers, q-point physics restated from
+// src/_kernels.py:555-693, scatter by fp64 atomics into a vector whose
+// constrained rows were initialised first (identity rows/columns,
+// src/pff_operator.py:262-302).  The Q2 fast path lives in pff_sweep.cu.
+#include "pff_internal.cuh"
+
+namespace pff {
+
+namespace {
+
+constexpr int CELL_THREADS = 128;
+
+inline unsigned grid_for(int64_t n, int threads) {
+    return (unsigned)((n + threads - 1) / threads);
+}
+
+template <int N1>
+__device__ __forceinline__ void cell_ids(const Mesh& m, int cx, int cy, int64_t (&gid)[N1][N1]) {
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) gid[b][a] = m.node(cx, cy, a, b);
+}
+
+// value + reference gradients of a nodal field at the q x q points
+template <int N1>
+__device__ __forceinline__ void grad_q(const Shape& S, const double (&c)[N1][N1],
+                                       double (&gx)[N1][N1], double (&gy)[N1][N1]) {
+    double tx[N1][N1], td[N1][N1];
+    fwd_x<N1>(S.N, c, tx);
+    fwd_x<N1>(S.D, c, td);
+    fwd_y<N1>(S.D, tx, gy);
+    fwd_y<N1>(S.N, td, gx);
+}
+
+// ------------------------------------------------------------ refresh
+// q-point linearisation cache, src/_kernels.py:447-516.  Layout
+// qc[f][k][cell], f in {e11, e22, e12, g(phi~), g'(phi), pc}, k = jq*q+iq.
+template <int P, bool MIEHE>
+__global__ void __launch_bounds__(CELL_THREADS)
+k_refresh(Mesh m, Shape S, Material M, const double* __restrict__ U,
+          const double* __restrict__ pt, double* __restrict__ qc) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t nc = m.n_cells();
+    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= nc) return;
+    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    int64_t gid[N1][N1];
+    cell_ids<N1>(m, cx, cy, gid);
+    const int64_t n = m.n;
+    double cu[N1][N1], cv[N1][N1], cp[N1][N1], ct[N1][N1];
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+            cu[b][a] = U[gid[b][a]];
+            cv[b][a] = U[n + gid[b][a]];
+            cp[b][a] = U[2 * n + gid[b][a]];
+            ct[b][a] = pt[gid[b][a]];
+        }
+    double gxu[N1][N1], gyu[N1][N1], gxv[N1][N1], gyv[N1][N1], vp[N1][N1], vt[N1][N1];
+    double tx[N1][N1];
+    grad_q<N1>(S, cu, gxu, gyu);
+    grad_q<N1>(S, cv, gxv, gyv);
+    fwd_x<N1>(S.N, cp, tx);
+    fwd_y<N1>(S.N, tx, vp);
+    fwd_x<N1>(S.N, ct, tx);
+    fwd_y<N1>(S.N, tx, vt);
+    const double inv_h = 1.0 / m.h, gce = M.gc / M.eps, gdd = 2.0 * (1.0 - M.kappa);
+#pragma unroll
+    for (int jq = 0; jq < N1; ++jq)
+#pragma unroll
+        for (int iq = 0; iq < N1; ++iq) {
+            double e11 = gxu[jq][iq] * inv_h;
+            double e22 = gyv[jq][iq] * inv_h;
+            double e12 = 0.5 * (gyu[jq][iq] + gxv[jq][iq]) * inv_h;
+            double tre = e11 + e22;
+            double g_t = (1.0 - M.kappa) * vt[jq][iq] * vt[jq][iq] + M.kappa;
+            double esp = MIEHE ? esplus2(M.lam, M.mu, tre, eig2(e11, e22, e12))
+                               : 0.5 * M.lam * tre * tre +
+                                     M.mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
+            double* q = qc + (int64_t)(jq * N1 + iq) * nc + cell;
+            const int64_t fs = (int64_t)QQ * nc;
+            q[0] = e11;
+            q[fs] = e22;
+            q[2 * fs] = e12;
+            q[3 * fs] = g_t;
+            q[4 * fs] = gdd * vp[jq][iq];
+            q[5 * fs] = gdd * esp + gce;
+        }
+}
+
+// ----------------------------------------------------- Jacobian (generic)
+template <int MODE>
+struct ModeTraits {
+    static constexpr bool DO_UU = MODE == MODE_FULL || MODE == MODE_UU;
+    static constexpr bool DO_PP = MODE != MODE_UU;
+    static constexpr bool DO_COUP = MODE == MODE_FULL || MODE == MODE_PHIROW;
+    static constexpr bool NEED_U = DO_UU || DO_COUP;
+};
+
+// dst rows: constrained -> src (identity row); free -> 0, or for the fused
+// residual dst = rhs - J src: constrained -> rhs - src, free -> rhs.
+template <int MODE>
+__global__ void k_apply_init(int64_t n, const uint8_t* __restrict__ flags,
+                             const double* __restrict__ src, const double* __restrict__ rhs,
+                             double* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t f = flags[i];
+    auto put = [&](int64_t o, int64_t so, bool cons) {
+        double v = cons ? src[so] : 0.0;
+        dst[o] = rhs ? rhs[o] - v : v;
+    };
+    if (MODE == MODE_FULL) {
+        put(i, i, f & F_DIR);
+        put(n + i, n + i, f & F_DIR);
+        put(2 * n + i, 2 * n + i, f & F_ACT);
+    } else if (MODE == MODE_UU) {
+        put(i, i, f & F_DIR);
+        put(n + i, n + i, f & F_DIR);
+    } else if (MODE == MODE_PHIPHI) {
+        put(i, i, f & F_ACT);
+    } else {
+        put(i, 2 * n + i, f & F_ACT);
+    }
+}
+
+template <int P, bool MIEHE, int MODE>
+__global__ void __launch_bounds__(CELL_THREADS)
+k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
+              const uint8_t* __restrict__ flags, const double* __restrict__ sx,
+              const double* __restrict__ sy, const double* __restrict__ sp, double* dx,
+              double* dy, double* dp, double sign) {
+    using T = ModeTraits<MODE>;
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t nc = m.n_cells();
+    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= nc) return;
+    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    int64_t gid[N1][N1];
+    uint8_t fl[N1][N1];
+    cell_ids<N1>(m, cx, cy, gid);
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) fl[b][a] = flags[gid[b][a]];
+
+    double gxu[N1][N1], gyu[N1][N1], gxv[N1][N1], gyv[N1][N1];
+    double vp[N1][N1], gxp[N1][N1], gyp[N1][N1];
+    if (T::NEED_U) {
+        double c[N1][N1];
+#pragma unroll
+        for (int b = 0; b < N1; ++b)
+#pragma unroll
+            for (int a = 0; a < N1; ++a) c[b][a] = (fl[b][a] & F_DIR) ? 0.0 : sx[gid[b][a]];
+        grad_q<N1>(S, c, gxu, gyu);
+#pragma unroll
+        for (int b = 0; b < N1; ++b)
+#pragma unroll
+            for (int a = 0; a < N1; ++a) c[b][a] = (fl[b][a] & F_DIR) ? 0.0 : sy[gid[b][a]];
+        grad_q<N1>(S, c, gxv, gyv);
+    }
+    if (T::DO_PP) {
+        double c[N1][N1], tx[N1][N1], td[N1][N1];
+#pragma unroll
+        for (int b = 0; b < N1; ++b)
+#pragma unroll
+            for (int a = 0; a < N1; ++a) c[b][a] = (fl[b][a] & F_ACT) ? 0.0 : sp[gid[b][a]];
+        fwd_x<N1>(S.N, c, tx);
+        fwd_x<N1>(S.D, c, td);
+        fwd_y<N1>(S.N, tx, vp);
+        fwd_y<N1>(S.D, tx, gyp);
+        fwd_y<N1>(S.N, td, gxp);
+    }
+
+    const double h = m.h, inv_h = 1.0 / h;
+    const int64_t fs = (int64_t)QQ * nc;
+    double s11[N1][N1], s22[N1][N1], s12[N1][N1], fv[N1][N1], fgx[N1][N1], fgy[N1][N1];
+#pragma unroll
+    for (int jq = 0; jq < N1; ++jq)
+#pragma unroll
+        for (int iq = 0; iq < N1; ++iq) {
+            const double wq = S.w[jq] * S.w[iq];
+            const double wg = wq * h, wv = wq * h * h;
+            const double* q = qc + (int64_t)(jq * N1 + iq) * nc + cell;
+            double coup = 0.0;
+            if (T::NEED_U) {
+                double d11 = gxu[jq][iq] * inv_h;
+                double d22 = gyv[jq][iq] * inv_h;
+                double d12 = 0.5 * (gyu[jq][iq] + gxv[jq][iq]) * inv_h;
+                double ds11, ds22, ds12, spde;
+                dsig<MIEHE>(M.lam, M.mu, q[3 * fs], q[0], q[fs], q[2 * fs], d11, d22, d12, ds11,
+                            ds22, ds12, spde);
+                coup = q[4 * fs] * spde;
+                if (T::DO_UU) {
+                    s11[jq][iq] = ds11 * wg;
+                    s22[jq][iq] = ds22 * wg;
+                    s12[jq][iq] = ds12 * wg;
+                }
+            }
+            if (T::DO_PP) {
+                double pval = q[5 * fs] * vp[jq][iq];
+                if (T::DO_COUP) pval += coup;
+                fv[jq][iq] = pval * wv;
+                fgx[jq][iq] = M.gc * M.eps * gxp[jq][iq] * inv_h * wg;
+                fgy[jq][iq] = M.gc * M.eps * gyp[jq][iq] * inv_h * wg;
+            }
+        }
+
+    double t[N1][N1];
+    if (T::DO_UU) {
+        double ru[N1][N1] = {}, rv[N1][N1] = {};
+        bwd_y<N1>(S.N, s11, t);
+        bwd_x_add<N1>(S.D, t, ru);
+        bwd_y<N1>(S.D, s12, t);
+        bwd_x_add<N1>(S.N, t, ru);
+        bwd_y<N1>(S.N, s12, t);
+        bwd_x_add<N1>(S.D, t, rv);
+        bwd_y<N1>(S.D, s22, t);
+        bwd_x_add<N1>(S.N, t, rv);
+#pragma unroll
+        for (int b = 0; b < N1; ++b)
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+                if (!(fl[b][a] & F_DIR)) {
+                    atomicAdd(dx + gid[b][a], sign * ru[b][a]);
+                    atomicAdd(dy + gid[b][a], sign * rv[b][a]);
+                }
+    }
+    if (T::DO_PP) {
+        double rp[N1][N1] = {};
+        bwd_y<N1>(S.N, fv, t);
+        bwd_x_add<N1>(S.N, t, rp);
+        bwd_y<N1>(S.N, fgx, t);
+        bwd_x_add<N1>(S.D, t, rp);
+        bwd_y<N1>(S.D, fgy, t);
+        bwd_x_add<N1>(S.N, t, rp);
+#pragma unroll
+        for (int b = 0; b < N1; ++b)
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+                if (!(fl[b][a] & F_ACT)) atomicAdd(dp + gid[b][a], sign * rp[b][a]);
+    }
+}
+
+// ---------------------------------------------------------- diagonals
+// src/_kernels.py:700-746, with the state eigensystem computed once per
+// quadrature point instead of once per (node, point).
+template <int P, bool MIEHE>
+__global__ void __launch_bounds__(CELL_THREADS)
+k_diag_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc, double* dx,
+             double* dy, double* dp) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t nc = m.n_cells();
+    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= nc) return;
+    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    const double h = m.h, inv_h = 1.0 / h;
+    const int64_t fs = (int64_t)QQ * nc;
+    double ax[N1][N1] = {}, ay[N1][N1] = {}, ap[N1][N1] = {};
+#pragma unroll
+    for (int jq = 0; jq < N1; ++jq)
+#pragma unroll
+        for (int iq = 0; iq < N1; ++iq) {
+            const double wq = S.w[jq] * S.w[iq] * h * h;
+            const double* q = qc + (int64_t)(jq * N1 + iq) * nc + cell;
+            const double e11 = q[0], e22 = q[fs], e12 = q[2 * fs], g_t = q[3 * fs],
+                         pc = q[5 * fs];
+            Eig e;
+            double scale = 1.0, tre = 0.0;
+            if (MIEHE) {
+                e = eig2(e11, e22, e12);
+                scale = scale2(e11, e22, e12);
+                tre = e11 + e22;
+            }
+#pragma unroll
+            for (int b = 0; b < N1; ++b)
+#pragma unroll
+                for (int a = 0; a < N1; ++a) {
+                    double gx = S.D[iq][a] * S.N[jq][b] * inv_h;
+                    double gy = S.N[iq][a] * S.D[jq][b] * inv_h;
+                    double val = S.N[iq][a] * S.N[jq][b];
+                    double x11, x12, y12, y22, unused0, unused1;
+                    if (MIEHE) {
+                        dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, gx, 0.0, 0.5 * gy, x11,
+                                       unused0, x12, unused1);
+                        dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, 0.0, gy, 0.5 * gx,
+                                       unused0, y22, y12, unused1);
+                    } else {
+                        x11 = g_t * (M.lam + 2.0 * M.mu) * gx;
+                        x12 = g_t * M.mu * gy;
+                        y22 = g_t * (M.lam + 2.0 * M.mu) * gy;
+                        y12 = g_t * M.mu * gx;
+                    }
+                    ax[b][a] += (x11 * gx + x12 * gy) * wq;
+                    ay[b][a] += (y12 * gx + y22 * gy) * wq;
+                    ap[b][a] += (pc * val * val + M.gc * M.eps * (gx * gx + gy * gy)) * wq;
+                }
+        }
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+            int64_t g = m.node(cx, cy, a, b);
+            atomicAdd(dx + g, ax[b][a]);
+            atomicAdd(dy + g, ay[b][a]);
+            atomicAdd(dp + g, ap[b][a]);
+        }
+}
+
+// constrained entries -> 1 (src/pff_operator.py:320-326), optional reciprocal
+__global__ void k_diag_finalize(int64_t n, const uint8_t* __restrict__ flags, double* dx,
+                                double* dy, double* dp, int invert) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t f = flags[i];
+    double x = (f & F_DIR) ? 1.0 : dx[i];
+    double y = (f & F_DIR) ? 1.0 : dy[i];
+    double p = (f & F_ACT) ? 1.0 : dp[i];
+    if (invert) {
+        x = 1.0 / x;
+        y = 1.0 / y;
+        p = 1.0 / p;
+    }
+    dx[i] = x;
+    dy[i] = y;
+    dp[i] = p;
+}
+
+// ------------------------------------------------------------ residual
+// src/_kernels.py:319-440 (the Newton right-hand side)
+template <int P, bool MIEHE>
+__global__ void __launch_bounds__(CELL_THREADS)
+k_residual_cells(Mesh m, Shape S, Material M, const double* __restrict__ U,
+                 const double* __restrict__ pt, double* out) {
+    constexpr int N1 = P + 1;
+    const int64_t nc = m.n_cells();
+    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= nc) return;
+    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    const int64_t n = m.n;
+    int64_t gid[N1][N1];
+    cell_ids<N1>(m, cx, cy, gid);
+    double cu[N1][N1], cv[N1][N1], cp[N1][N1], ct[N1][N1];
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+            cu[b][a] = U[gid[b][a]];
+            cv[b][a] = U[n + gid[b][a]];
+            cp[b][a] = U[2 * n + gid[b][a]];
+            ct[b][a] = pt[gid[b][a]];
+        }
+    double gxu[N1][N1], gyu[N1][N1], gxv[N1][N1], gyv[N1][N1];
+    double vp[N1][N1], gxp[N1][N1], gyp[N1][N1], vt[N1][N1], tx[N1][N1], td[N1][N1];
+    grad_q<N1>(S, cu, gxu, gyu);
+    grad_q<N1>(S, cv, gxv, gyv);
+    fwd_x<N1>(S.N, cp, tx);
+    fwd_x<N1>(S.D, cp, td);
+    fwd_y<N1>(S.N, tx, vp);
+    fwd_y<N1>(S.D, tx, gyp);
+    fwd_y<N1>(S.N, td, gxp);
+    fwd_x<N1>(S.N, ct, tx);
+    fwd_y<N1>(S.N, tx, vt);
+    const double h = m.h, inv_h = 1.0 / h, gce = M.gc / M.eps;
+    double s11[N1][N1], s22[N1][N1], s12[N1][N1], fv[N1][N1], fgx[N1][N1], fgy[N1][N1];
+#pragma unroll
+    for (int jq = 0; jq < N1; ++jq)
+#pragma unroll
+        for (int iq = 0; iq < N1; ++iq) {
+            const double wq = S.w[jq] * S.w[iq];
+            const double wg = wq * h, wv = wq * h * h;
+            double e11 = gxu[jq][iq] * inv_h;
+            double e22 = gyv[jq][iq] * inv_h;
+            double e12 = 0.5 * (gyu[jq][iq] + gxv[jq][iq]) * inv_h;
+            double tre = e11 + e22;
+            double phv = vp[jq][iq], ptv = vt[jq][iq];
+            double g_t = (1.0 - M.kappa) * ptv * ptv + M.kappa;
+            double sp11, sp22, sp12, sm11 = 0.0, sm22 = 0.0, sm12 = 0.0, esp;
+            if (MIEHE) {
+                Eig e = eig2(e11, e22, e12);
+                sigplus2(M.lam, M.mu, tre, e, sp11, sp22, sp12);
+                sm11 = M.lam * tre + 2.0 * M.mu * e11 - sp11;
+                sm22 = M.lam * tre + 2.0 * M.mu * e22 - sp22;
+                sm12 = 2.0 * M.mu * e12 - sp12;
+                esp = esplus2(M.lam, M.mu, tre, e);
+            } else {
+                sp11 = M.lam * tre + 2.0 * M.mu * e11;
+                sp22 = M.lam * tre + 2.0 * M.mu * e22;
+                sp12 = 2.0 * M.mu * e12;
+                esp = 0.5 * M.lam * tre * tre + M.mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
+            }
+            s11[jq][iq] = (g_t * sp11 + sm11) * wg;
+            s22[jq][iq] = (g_t * sp22 + sm22) * wg;
+            s12[jq][iq] = (g_t * sp12 + sm12) * wg;
+            double dgv = 2.0 * (1.0 - M.kappa) * phv;
+            fv[jq][iq] = (dgv * esp - gce * (1.0 - phv)) * wv;
+            fgx[jq][iq] = M.gc * M.eps * gxp[jq][iq] * inv_h * wg;
+            fgy[jq][iq] = M.gc * M.eps * gyp[jq][iq] * inv_h * wg;
+        }
+    double t[N1][N1], ru[N1][N1] = {}, rv[N1][N1] = {}, rp[N1][N1] = {};
+    bwd_y<N1>(S.N, s11, t);
+    bwd_x_add<N1>(S.D, t, ru);
+    bwd_y<N1>(S.D, s12, t);
+    bwd_x_add<N1>(S.N, t, ru);
+    bwd_y<N1>(S.N, s12, t);
+    bwd_x_add<N1>(S.D, t, rv);
+    bwd_y<N1>(S.D, s22, t);
+    bwd_x_add<N1>(S.N, t, rv);
+    bwd_y<N1>(S.N, fv, t);
+    bwd_x_add<N1>(S.N, t, rp);
+    bwd_y<N1>(S.N, fgx, t);
+    bwd_x_add<N1>(S.D, t, rp);
+    bwd_y<N1>(S.D, fgy, t);
+    bwd_x_add<N1>(S.N, t, rp);
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+            atomicAdd(out + gid[b][a], ru[b][a]);
+            atomicAdd(out + n + gid[b][a], rv[b][a]);
+            atomicAdd(out + 2 * n + gid[b][a], rp[b][a]);
+        }
+}
+
+__global__ void k_residual_mask(int64_t n, const uint8_t* __restrict__ flags, double* out,
+                                int mask_dirichlet, int mask_active) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t f = flags[i];
+    if (mask_dirichlet && (f & F_DIR)) {
+        out[i] = 0.0;
+        out[n + i] = 0.0;
+    }
+    if (mask_active && (f & F_ACT)) out[2 * n + i] = 0.0;
+}
+
+// ------------------------------------------------------------ dispatch
+template <template <int, bool> class F, typename... A>
+cudaError_t dispatch_p_split(int p, bool miehe, A... args) {
+    switch (p * 2 + (miehe ? 1 : 0)) {
+        case 2: return F<1, false>::run(args...);
+        case 3: return F<1, true>::run(args...);
+        case 4: return F<2, false>::run(args...);
+        case 5: return F<2, true>::run(args...);
+        case 6: return F<3, false>::run(args...);
+        case 7: return F<3, true>::run(args...);
+        case 8: return F<4, false>::run(args...);
+        case 9: return F<4, true>::run(args...);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int P, bool MIEHE>
+struct RefreshL {
+    static cudaError_t run(const Level* L, cudaStream_t s) {
+        const Mesh& m = L->mesh;
+        k_refresh<P, MIEHE><<<grid_for(m.n_cells(), CELL_THREADS), CELL_THREADS, 0, s>>>(
+            m, L->shape, L->mat, L->U, L->phi_tilde, L->qcache);
+        count_launches(1);
+        return cudaGetLastError();
+    }
+};
+
+template <int P, bool MIEHE>
+struct ApplyL {
+    static cudaError_t run(const Level* L, int mode, const double* src, double* dst,
+                           const double* rhs, cudaStream_t s) {
+        const Mesh& m = L->mesh;
+        const int64_t n = m.n;
+        const unsigned gi = grid_for(n, 256), gc = grid_for(m.n_cells(), CELL_THREADS);
+        const double sign = rhs ? -1.0 : 1.0;
+        const double* q = L->qcache;
+        const uint8_t* f = L->flags;
+        switch (mode) {
+            case MODE_FULL:
+                k_apply_init<MODE_FULL><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
+                k_apply_cells<P, MIEHE, MODE_FULL><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, dst, dst + n,
+                    dst + 2 * n, sign);
+                break;
+            case MODE_UU:
+                k_apply_init<MODE_UU><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
+                k_apply_cells<P, MIEHE, MODE_UU><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, nullptr, dst, dst + n, nullptr,
+                    sign);
+                break;
+            case MODE_PHIPHI:
+                k_apply_init<MODE_PHIPHI><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
+                k_apply_cells<P, MIEHE, MODE_PHIPHI><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, nullptr, nullptr, src, nullptr, nullptr, dst,
+                    sign);
+                break;
+            case MODE_PHIROW:
+                k_apply_init<MODE_PHIROW><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
+                k_apply_cells<P, MIEHE, MODE_PHIROW><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, nullptr, nullptr, dst,
+                    sign);
+                break;
+            default:
+                return cudaErrorInvalidValue;
+        }
+        count_launches(2);
+        return cudaGetLastError();
+    }
+};
+
+template <int P, bool MIEHE>
+struct DiagL {
+    static cudaError_t run(const Level* L, double* dx, double* dy, double* dp, int invert,
+                           cudaStream_t s) {
+        const Mesh& m = L->mesh;
+        cudaMemsetAsync(dx, 0, sizeof(double) * m.n, s);
+        cudaMemsetAsync(dy, 0, sizeof(double) * m.n, s);
+        cudaMemsetAsync(dp, 0, sizeof(double) * m.n, s);
+        k_diag_cells<P, MIEHE><<<grid_for(m.n_cells(), CELL_THREADS), CELL_THREADS, 0, s>>>(
+            m, L->shape, L->mat, L->qcache, dx, dy, dp);
+        k_diag_finalize<<<grid_for(m.n, 256), 256, 0, s>>>(m.n, L->flags, dx, dy, dp, invert);
+        count_launches(5);
+        return cudaGetLastError();
+    }
+};
+
+template <int P, bool MIEHE>
+struct ResidualL {
+    static cudaError_t run(const Level* L, double* out, int md, int ma, cudaStream_t s) {
+        const Mesh& m = L->mesh;
+        cudaMemsetAsync(out, 0, sizeof(double) * 3 * m.n, s);
+        k_residual_cells<P, MIEHE><<<grid_for(m.n_cells(), CELL_THREADS), CELL_THREADS, 0, s>>>(
+            m, L->shape, L->mat, L->U, L->phi_tilde, out);
+        k_residual_mask<<<grid_for(m.n, 256), 256, 0, s>>>(m.n, L->flags, out, md, ma);
+        count_launches(3);
+        return cudaGetLastError();
+    }
+};
+
+}  // namespace
+
+cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
+                               const double* rhs, cudaStream_t s, bool* handled);
+
+cudaError_t launch_refresh(const Level& L, cudaStream_t s) {
+    return dispatch_p_split<RefreshL>(L.mesh.p, L.miehe, &L, s);
+}
+
+cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
+                         const double* rhs, cudaStream_t s) {
+    bool handled = false;
+    cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
+    if (handled || e != cudaSuccess) return e;
+    return dispatch_p_split<ApplyL>(L.mesh.p, L.miehe, &L, mode, src, dst, rhs, s);
+}
+
+cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, int invert,
+                            cudaStream_t s) {
+    return dispatch_p_split<DiagL>(L.mesh.p, L.miehe, &L, dx, dy, dp, invert, s);
+}
+
+cudaError_t launch_residual(const Level& L, double* out, int md, int ma, cudaStream_t s) {
+    return dispatch_p_split<ResidualL>(L.mesh.p, L.miehe, &L, out, md, ma, s);
+}
+
+}  // namespace pff

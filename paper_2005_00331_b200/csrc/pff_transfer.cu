@@ -1,0 +1,191 @@
+// pff_transfer.cu -- level transfers and state injection on device.
+//
+// Prolongation restates src/multigrid.py:44-112 without the CSR: each fine
+// scalar row is owned by the first fine cell (ascending cell index) that
+// references it, which in closed form is the lowest containing cell in each
+// direction -- except the upper slit copies (n_grid + i), owned by the upper
+// cell row.  The row is the coarse Lagrange basis of the owner's parent cell
+// evaluated through the child embedding; weights with |w| <= 1e-14 are
+// dropped exactly as the reference does (multigrid.py:81-83).
+// Restriction is the exact transpose (multigrid.py:114-120): each fine row
+// scatters its kept weights into the coarse vector.
+// Injection restates src/mesh_hierarchy.py:316-338 / pff_operator.py:380-400.
+#include "pff_internal.cuh"
+
+namespace pff {
+
+namespace {
+
+struct Owner {
+    int ccx, ccy, chx, chy, a, b;
+};
+
+__device__ __forceinline__ Owner fine_owner(const Mesh& mf, int64_t gid) {
+    int64_t i, j;
+    bool dup = gid >= mf.n_grid;
+    if (dup) {
+        i = gid - mf.n_grid;
+        j = mf.i_mid;
+    } else {
+        i = gid % mf.np1;
+        j = gid / mf.np1;
+    }
+    const int p = mf.p;
+    auto lowest = [&](int64_t k) -> int {
+        int64_t c = (k % p == 0 && k > 0) ? k / p - 1 : k / p;
+        return (int)(c < mf.nside ? c : mf.nside - 1);
+    };
+    int fx = lowest(i);
+    int fy = dup ? (mf.nside >> 1) : lowest(j);
+    Owner o;
+    o.a = (int)(i - (int64_t)p * fx);
+    o.b = (int)(j - (int64_t)p * fy);
+    o.ccx = fx >> 1;
+    o.ccy = fy >> 1;
+    o.chx = fx & 1;
+    o.chy = fy & 1;
+    return o;
+}
+
+template <int P>
+__global__ void k_prolong(Mesh mf, Mesh mc, Embed E, const double* __restrict__ xc,
+                          double* __restrict__ yf, const uint8_t* __restrict__ flags_f,
+                          int add_masked) {
+    constexpr int N1 = P + 1;
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= mf.n) return;
+    Owner o = fine_owner(mf, g);
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int my = 0; my < N1; ++my)
+#pragma unroll
+        for (int mx = 0; mx < N1; ++mx) {
+            double w = E.E[o.chy][o.b][my] * E.E[o.chx][o.a][mx];
+            if (fabs(w) > 1e-14) {
+                int64_t c = mc.node(o.ccx, o.ccy, mx, my);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) acc[k] = fma(w, xc[k * mc.n + c], acc[k]);
+            }
+        }
+    if (add_masked) {
+        // z += where(cons, 0, P zc)  (src/multigrid.py:340-342)
+        uint8_t f = flags_f[g];
+        if (!(f & F_DIR)) {
+            yf[g] += acc[0];
+            yf[mf.n + g] += acc[1];
+        }
+        if (!(f & F_ACT)) yf[2 * mf.n + g] += acc[2];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) yf[k * mf.n + g] = acc[k];
+    }
+}
+
+template <int P>
+__global__ void k_restrict(Mesh mf, Mesh mc, Embed E, const double* __restrict__ yf,
+                           double* xc) {
+    constexpr int N1 = P + 1;
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= mf.n) return;
+    Owner o = fine_owner(mf, g);
+    double v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] = yf[k * mf.n + g];
+#pragma unroll
+    for (int my = 0; my < N1; ++my)
+#pragma unroll
+        for (int mx = 0; mx < N1; ++mx) {
+            double w = E.E[o.chy][o.b][my] * E.E[o.chx][o.a][mx];
+            if (fabs(w) > 1e-14) {
+                int64_t c = mc.node(o.ccx, o.ccy, mx, my);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) atomicAdd(xc + k * mc.n + c, w * v[k]);
+            }
+        }
+}
+
+// rc[cons_c] = 0 (src/multigrid.py:338)
+__global__ void k_zero_cons3(int64_t n, const uint8_t* __restrict__ flags, double* x) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t f = flags[i];
+    if (f & F_DIR) {
+        x[i] = 0.0;
+        x[n + i] = 0.0;
+    }
+    if (f & F_ACT) x[2 * n + i] = 0.0;
+}
+
+__device__ __forceinline__ int64_t inject_src(const Mesh& mf, const Mesh& mc, int64_t c) {
+    if (c < mc.n_grid) {
+        int64_t I = c % mc.np1, J = c / mc.np1;
+        return (2 * J) * mf.np1 + 2 * I;
+    }
+    return mf.n_grid + 2 * (c - mc.n_grid);
+}
+
+__global__ void k_inject_f64(Mesh mf, Mesh mc, const double* __restrict__ src, double* dst,
+                             int ncomp) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mc.n) return;
+    int64_t f = inject_src(mf, mc, c);
+    for (int k = 0; k < ncomp; ++k) dst[k * mc.n + c] = src[k * mf.n + f];
+}
+
+__global__ void k_inject_u8(Mesh mf, Mesh mc, const uint8_t* __restrict__ src, uint8_t* dst) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mc.n) return;
+    dst[c] = src[inject_src(mf, mc, c)];
+}
+
+inline unsigned blocks(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+}  // namespace
+
+cudaError_t launch_prolongate(const Level& F, const Level& C, const double* xc, double* yf,
+                              int add_masked, cudaStream_t s) {
+    if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
+    switch (F.mesh.p) {
+        case 1: k_prolong<1><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 2: k_prolong<2><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 3: k_prolong<3><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 4: k_prolong<4><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        default: return cudaErrorInvalidValue;
+    }
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, double* xc,
+                            int zero_cons, cudaStream_t s) {
+    if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
+    cudaMemsetAsync(xc, 0, sizeof(double) * 3 * C.mesh.n, s);
+    switch (F.mesh.p) {
+        case 1: k_restrict<1><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
+        case 2: k_restrict<2><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
+        case 3: k_restrict<3><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
+        case 4: k_restrict<4><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (zero_cons) k_zero_cons3<<<blocks(C.mesh.n), 256, 0, s>>>(C.mesh.n, C.flags, xc);
+    count_launches(zero_cons ? 3 : 2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inject_f64(const Level& F, const Level& C, const double* src, double* dst,
+                              int ncomp, cudaStream_t s) {
+    if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
+    k_inject_f64<<<blocks(C.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, src, dst, ncomp);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inject_u8(const Level& F, const Level& C, const uint8_t* src, uint8_t* dst,
+                             cudaStream_t s) {
+    if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
+    k_inject_u8<<<blocks(C.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, src, dst);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace pff

@@ -1,0 +1,167 @@
+"""Nested slit-square meshes with the reference's Q_p scalar numbering.
+
+Closed-form replacement of src/mesh_hierarchy.py (whose per-cell Python
+loops take 7 s at 1024^2): the device kernels never read a connectivity
+array; ``DofMap.conn`` is materialised lazily (vectorised numpy) only for
+callers that ask for it.  Numbering: grid node (i, j) -> j*n1 + i, upper
+slit copies appended at n_grid + i (src/mesh_hierarchy.py:156-189).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from functools import cached_property
+
+import numpy as np
+
+BOUNDARY_TAGS = ("bottom", "top", "left", "right")
+COMPONENTS = ("u_x", "u_y", "phi")
+
+
+@dataclass(frozen=True)
+class MeshLevel:
+    level_index: int
+
+    @property
+    def cells_per_side(self) -> int:
+        return 2 ** self.level_index
+
+    @property
+    def h(self) -> float:
+        return 1.0 / self.cells_per_side
+
+    @property
+    def n_cells(self) -> int:
+        return self.cells_per_side ** 2
+
+
+@dataclass(frozen=True)
+class DofMap:
+    level_index: int
+    degree: int
+
+    @property
+    def nodes_per_side(self) -> int:
+        return self.degree * 2 ** self.level_index + 1
+
+    @property
+    def n_grid(self) -> int:
+        return self.nodes_per_side ** 2
+
+    @property
+    def i_mid(self) -> int:
+        return (self.nodes_per_side - 1) // 2
+
+    @property
+    def n_dup(self) -> int:
+        return self.i_mid if self.level_index >= 1 else 0
+
+    @property
+    def n_scalar(self) -> int:
+        return self.n_grid + self.n_dup
+
+    @property
+    def n_total(self) -> int:
+        return 3 * self.n_scalar
+
+    @property
+    def n_local(self) -> int:
+        return (self.degree + 1) ** 2
+
+    @cached_property
+    def conn(self) -> np.ndarray:
+        p, ns, n1 = self.degree, 2 ** self.level_index, self.nodes_per_side
+        cy, cx = np.divmod(np.arange(ns * ns, dtype=np.int64), ns)
+        b, a = np.divmod(np.arange((p + 1) ** 2, dtype=np.int64), p + 1)
+        j = cy[:, None] * p + b[None, :]
+        i = cx[:, None] * p + a[None, :]
+        gid = j * n1 + i
+        if self.level_index >= 1:
+            up = (cy[:, None] >= ns // 2) & (j == self.i_mid) & (i < self.i_mid)
+            gid = np.where(up, self.n_grid + i, gid)
+        return gid
+
+    @cached_property
+    def coords(self) -> np.ndarray:
+        xs = np.arange(self.nodes_per_side) / (self.nodes_per_side - 1)
+        gx, gy = np.meshgrid(xs, xs, indexing="xy")
+        c = np.column_stack([gx.ravel(), gy.ravel()])
+        if self.n_dup:
+            c = np.vstack([c, np.column_stack([xs[: self.n_dup], np.full(self.n_dup, 0.5)])])
+        return c
+
+    @cached_property
+    def boundary_nodes(self) -> dict:
+        n1, ng = self.nodes_per_side, self.n_grid
+        line = np.arange(n1, dtype=np.int64)
+        out = {"bottom": line.copy(), "top": (n1 - 1) * n1 + line,
+               "left": line * n1, "right": line * n1 + n1 - 1}
+        if self.n_dup:
+            out["left"] = np.sort(np.append(out["left"], ng))
+        return out
+
+    @property
+    def slit_lower(self) -> np.ndarray:
+        if not self.n_dup:
+            return np.empty(0, dtype=np.int64)
+        return self.i_mid * self.nodes_per_side + np.arange(self.n_dup, dtype=np.int64)
+
+    @property
+    def slit_upper(self) -> np.ndarray:
+        if not self.n_dup:
+            return np.empty(0, dtype=np.int64)
+        return self.n_grid + np.arange(self.n_dup, dtype=np.int64)
+
+
+@dataclass
+class MeshHierarchy:
+    """Levels 0..max_level (src/mesh_hierarchy.py:279-338)."""
+
+    max_level: int
+    degree: int
+    _injections: dict = field(default_factory=dict, repr=False)
+
+    def level(self, l: int) -> MeshLevel:
+        self._check(l)
+        return MeshLevel(l)
+
+    def dof_map(self, l: int) -> DofMap:
+        self._check(l)
+        return DofMap(l, self.degree)
+
+    def _check(self, l):
+        if not 0 <= l <= self.max_level:
+            raise IndexError(f"level {l} outside 0..{self.max_level}")
+
+    def boundary_dofs(self, level: int, tag: str) -> np.ndarray:
+        if tag not in BOUNDARY_TAGS:
+            raise ValueError(f"unknown boundary tag {tag!r}")
+        dm = self.dof_map(level)
+        nodes = dm.boundary_nodes[tag]
+        return np.sort(np.concatenate([nodes, dm.n_scalar + nodes]))
+
+    def injection(self, fine_level: int) -> np.ndarray:
+        """coarse = fine[injection(fine_level)] (src/mesh_hierarchy.py:316-338)."""
+        if fine_level in self._injections:
+            return self._injections[fine_level]
+        if fine_level < 1:
+            raise ValueError("level 0 has no coarser level")
+        fine, coarse = self.dof_map(fine_level), self.dof_map(fine_level - 1)
+        idx = np.arange(coarse.nodes_per_side, dtype=np.int64) * 2
+        jj, ii = np.meshgrid(idx, idx, indexing="ij")
+        inj = (jj * fine.nodes_per_side + ii).ravel()
+        if coarse.n_dup:
+            inj = np.append(inj, fine.n_grid + 2 * np.arange(coarse.n_dup, dtype=np.int64))
+        self._injections[fine_level] = inj
+        return inj
+
+
+def build_hierarchy(max_level: int, degree: int) -> MeshHierarchy:
+    """src/mesh_hierarchy.py:352-366 (closed form, O(1) build)."""
+    if max_level < 2:
+        raise ValueError("max_level must be >= 2 (coarse solve is on level 2)")
+    if degree < 1:
+        raise ValueError("degree must be >= 1")
+    if degree > 4:
+        raise ValueError("degree must be <= 4 on the B200 kernels")
+    return MeshHierarchy(max_level=max_level, degree=degree)

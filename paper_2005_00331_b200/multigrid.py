@@ -1,0 +1,481 @@
+"""Geometric multigrid V-cycle on the B200 (drop-in for src/multigrid.py).
+
+Same algebra as the reference (src/multigrid.py:201-344): block
+Chebyshev-Jacobi smoothing (u block, then phi block), Q_p embedding
+transfers, a Chebyshev "solve" on the coarse level, Lanczos range
+estimates with the reference's seeds.  Every vector operation of the cycle
+is a libpff_b200 kernel on device-resident per-level buffers, and the whole
+cycle is captured once per setup into a CUDA graph, so one ``apply`` is one
+graph launch instead of a few hundred kernel launches.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+from . import operator as op
+from ._lib import call, ptr, stream_handle
+from .basis import MaterialParams, lagrange_matrices, shape_data, support_points_01
+from .mesh import MeshHierarchy
+
+logger = logging.getLogger(__name__)
+
+
+@dataclass
+class ChebyshevConfig:
+    """Smoothing/solve ranges and sweep counts (src/multigrid.py:27-41)."""
+
+    sweeps: int = 5
+    coarse_sweeps: int = 32
+    c: float = 0.24
+    C: float = 1.2
+    lambda_min_floor: float = 1e-3
+    lanczos_iterations: int = 30
+    seed: int = 20240915
+
+    def __post_init__(self):
+        if not (0.0 < self.c <= 1.0 <= self.C):
+            raise ValueError("need 0 < c <= 1 <= C")
+
+
+# --------------------------------------------------------------- helpers
+
+def _dev():
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _empty(n):
+    return torch.empty(n, dtype=torch.float64, device=_dev())
+
+
+def _dot(x: torch.Tensor, y: torch.Tensor, scratch: torch.Tensor, out: torch.Tensor) -> float:
+    call("pff_dot", x.numel(), ptr(x), ptr(y), ptr(scratch), ptr(out), stream_handle())
+    return float(out.item())
+
+
+class _Scratch:
+    def __init__(self):
+        self.partials = _empty(_lib.load().pff_reduce_scratch_len())
+        self.out = _empty(4)
+
+    def dot(self, x, y) -> float:
+        return _dot(x, y, self.partials, self.out)
+
+    def norm(self, x) -> float:
+        return float(np.sqrt(self.dot(x, x)))
+
+
+def _axpby(a, x, b, y):
+    call("pff_axpby", y.numel(), float(a), ptr(x), float(b), ptr(y), stream_handle())
+    return y
+
+
+class _HostCallable:
+    """Wrap a user callable so it sees the array type the user passed in."""
+
+    def __init__(self, fn, numpy_mode: bool):
+        self.fn, self.numpy_mode = fn, numpy_mode
+
+    def __call__(self, t: torch.Tensor) -> torch.Tensor:
+        if self.numpy_mode:
+            res = self.fn(t.cpu().numpy())
+        else:
+            res = self.fn(t)
+        out, _ = op.as_device(res, t.numel())
+        if out.data_ptr() == t.data_ptr():
+            out = out.clone()   # the reference's callables always return new arrays
+        return out
+
+
+def _level_handle(hierarchy: MeshHierarchy, level: int):
+    h = ctypes.c_void_p()
+    s = shape_data(hierarchy.degree)
+    mat = _lib.material(MaterialParams())
+    E = s.embedding()
+    call("pff_level_create", ctypes.byref(h), hierarchy.degree, level, 0, ctypes.byref(mat),
+         s.values.ctypes.data, s.derivatives.ctypes.data, s.quad_weights.ctypes.data,
+         E.ctypes.data)
+    return h
+
+
+# ------------------------------------------------------------- transfers
+
+def build_prolongation(hierarchy: MeshHierarchy, fine_level: int) -> sp.csr_matrix:
+    """The assembled scalar embedding (src/multigrid.py:44-94), for callers
+    that want the matrix; the V-cycle itself uses the structured kernels."""
+    if fine_level < 1:
+        raise ValueError("fine level must be >= 1")
+    dmf, dmc = hierarchy.dof_map(fine_level), hierarchy.dof_map(fine_level - 1)
+    p = hierarchy.degree
+    n1 = p + 1
+    sup = support_points_01(p)
+    E = np.stack([lagrange_matrices(sup, (ch + sup) / 2.0)[0] for ch in (0, 1)])
+    flat = dmf.conn.ravel()
+    fdofs, first = np.unique(flat, return_index=True)
+    cell, k = np.divmod(first, n1 * n1)
+    b, a = np.divmod(k, n1)
+    nsf = 2 ** fine_level
+    fy, fx = np.divmod(cell, nsf)
+    ccell = (fy // 2) * (nsf // 2) + fx // 2
+    W = (E[fy % 2, b][:, :, None] * E[fx % 2, a][:, None, :]).reshape(len(fdofs), n1 * n1)
+    C = dmc.conn[ccell]
+    keep = np.abs(W) > 1e-14
+    indptr = np.zeros(dmf.n_scalar + 1, dtype=np.int64)
+    indptr[fdofs + 1] = keep.sum(axis=1)
+    np.cumsum(indptr, out=indptr)
+    return sp.csr_matrix((W[keep], C[keep], indptr), shape=(dmf.n_scalar, dmc.n_scalar))
+
+
+class TransferOperator:
+    """Componentwise prolongation/restriction between adjacent levels
+    (src/multigrid.py:97-120), as structured device kernels."""
+
+    def __init__(self, hierarchy: MeshHierarchy, fine_level: int):
+        if fine_level < 1:
+            raise ValueError("fine level must be >= 1")
+        self.hierarchy = hierarchy
+        self.fine_level = fine_level
+        self.n_fine = hierarchy.dof_map(fine_level).n_scalar
+        self.n_coarse = hierarchy.dof_map(fine_level - 1).n_scalar
+        self._h = None
+
+    def _handles(self):
+        if self._h is None:
+            self._h = (_level_handle(self.hierarchy, self.fine_level),
+                       _level_handle(self.hierarchy, self.fine_level - 1))
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            for h in self._h:
+                _lib._lib.pff_level_destroy(h)
+
+    @cached_property
+    def P(self) -> sp.csr_matrix:
+        return build_prolongation(self.hierarchy, self.fine_level)
+
+    @cached_property
+    def R(self) -> sp.csr_matrix:
+        return self.P.T.tocsr()
+
+    def prolongate(self, coarse):
+        x, was_np = op.as_device(coarse, 3 * self.n_coarse)
+        out = _empty(3 * self.n_fine)
+        hf, hc = self._handles()
+        call("pff_prolongate", hf, hc, ptr(x), ptr(out), 0, stream_handle())
+        return op.back(out, was_np)
+
+    def restrict(self, fine):
+        y, was_np = op.as_device(fine, 3 * self.n_fine)
+        out = _empty(3 * self.n_coarse)
+        hf, hc = self._handles()
+        call("pff_restrict", hf, hc, ptr(y), ptr(out), 0, stream_handle())
+        return op.back(out, was_np)
+
+
+# ------------------------------------------------------ Lanczos / Chebyshev
+
+def estimate_lambda_range(apply_fn, diag, max_iterations: int = 30, seed: int = 0,
+                          rtol: float = 1e-4):
+    """Lanczos Ritz estimates of the extremal eigenvalues of diag^-1 A
+    (src/multigrid.py:123-162), device vectors, host tridiagonal solve."""
+    numpy_mode = not isinstance(diag, torch.Tensor)
+    d, _ = op.as_device(diag)
+    n = d.numel()
+    fn = apply_fn if getattr(apply_fn, "_pff_device", False) else _HostCallable(apply_fn, numpy_mode)
+    sc = _Scratch()
+    dhalf = 1.0 / torch.sqrt(d)
+    v_h = np.random.default_rng(seed).standard_normal(n)
+    v_h /= np.linalg.norm(v_h)
+    v = torch.from_numpy(v_h).to(d.device)
+    v_prev = torch.zeros_like(v)
+    tmp = torch.empty_like(v)
+    beta = 0.0
+    alphas, betas = [], []
+    lam_min = lam_max = 1.0
+    prev_max = None
+    s = stream_handle()
+    for _ in range(min(max_iterations, n)):
+        call("pff_mul", n, ptr(dhalf), ptr(v), ptr(tmp), s)
+        w = fn(tmp)
+        call("pff_mul", n, ptr(dhalf), ptr(w), ptr(w), s)
+        _axpby(-beta, v_prev, 1.0, w)
+        alpha = sc.dot(v, w)
+        _axpby(-alpha, v, 1.0, w)
+        alphas.append(alpha)
+        ritz = scipy.linalg.eigvalsh_tridiagonal(alphas, betas) if betas else np.array([alpha])
+        lam_min, lam_max = float(ritz[0]), float(ritz[-1])
+        beta = sc.norm(w)
+        if beta < 1e-12 * max(1.0, abs(lam_max)):
+            break
+        if prev_max is not None and abs(lam_max - prev_max) <= rtol * abs(lam_max):
+            break
+        prev_max = lam_max
+        betas.append(beta)
+        v_prev, v = v, w
+        call("pff_div", n, ptr(v), None, beta, ptr(v), s)
+    return lam_min, lam_max
+
+
+def estimate_lambda_max(apply_fn, diag, max_iterations: int = 30, seed: int = 0) -> float:
+    return estimate_lambda_range(apply_fn, diag, max_iterations, seed)[1]
+
+
+def chebyshev_apply(apply_fn, diag, rhs, a: float, b: float, sweeps: int):
+    """Fixed-sweep Chebyshev iteration for A z = rhs on [a, b]
+    (src/multigrid.py:170-198)."""
+    if not (0.0 < a < b):
+        raise ValueError(f"invalid Chebyshev interval [{a}, {b}]")
+    if sweeps < 1:
+        raise ValueError("sweeps must be >= 1")
+    numpy_mode = not isinstance(rhs, torch.Tensor)
+    rh, was_np = op.as_device(rhs)
+    dg, _ = op.as_device(diag, rh.numel())
+    n = rh.numel()
+    fn = apply_fn if getattr(apply_fn, "_pff_device", False) else _HostCallable(apply_fn, numpy_mode)
+    theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+    sigma1 = theta / delta
+    invd = 1.0 / dg
+    d, z = torch.empty_like(rh), torch.empty_like(rh)
+    s = stream_handle()
+    call("pff_cheb_init", n, ptr(invd), ptr(rh), theta, ptr(d), ptr(z), 0, s)
+    if sweeps == 1:
+        return op.back(z, was_np)
+    r = rh.clone()
+    _axpby(-1.0, fn(d), 1.0, r)
+    rho_old = 1.0 / sigma1
+    for k in range(1, sweeps):
+        rho = 1.0 / (2.0 * sigma1 - rho_old)
+        call("pff_cheb_step", n, ptr(invd), ptr(r), rho * rho_old, 2.0 * rho / delta, ptr(d),
+             ptr(z), s)
+        rho_old = rho
+        if k < sweeps - 1:
+            _axpby(-1.0, fn(d), 1.0, r)
+    return op.back(z, was_np)
+
+
+# --------------------------------------------------------------- V-cycle
+
+class _BlockApply:
+    """Device block operator of one level, flagged as tensor-native."""
+    _pff_device = True
+
+    def __init__(self, state, mode, n):
+        self.state, self.mode, self.n = state, mode, n
+
+    def __call__(self, v):
+        out = _empty(self.n)
+        self.state.apply_into(self.mode, v, out)
+        return out
+
+
+class _LevelWork:
+    def __init__(self, n):
+        self.r = _empty(3 * n)      # level right-hand side (restricted residual)
+        self.z = _empty(3 * n)      # level correction
+        self.res = _empty(3 * n)
+        self.resphi = _empty(n)
+        self.d = _empty(2 * n)
+        self.acc = _empty(2 * n)
+        self.cr = _empty(2 * n)
+
+
+class _ConsView(dict):
+    """gmg.cons[l] as in the reference (host masks), computed on demand."""
+
+    def __init__(self, gmg):
+        super().__init__()
+        self._gmg = gmg
+
+    def __missing__(self, l):
+        return self._gmg.states[l].constrained_mask()
+
+    def __contains__(self, l):
+        return l in self._gmg.states
+
+
+class GmgPreconditioner:
+    """V-cycle over restricted linearisation states; a fixed linear operator
+    (src/multigrid.py:201-344)."""
+
+    def __init__(self, hierarchy: MeshHierarchy, coarse_level: int = 2,
+                 cheb: ChebyshevConfig | None = None, use_graph: bool = True):
+        if coarse_level < 2:
+            raise ValueError("coarse level must be >= 2")
+        if coarse_level > hierarchy.max_level:
+            raise ValueError("hierarchy shallower than the coarse level")
+        self.hierarchy = hierarchy
+        self.coarse_level = coarse_level
+        self.cheb = cheb or ChebyshevConfig()
+        self.transfers = {l: TransferOperator(hierarchy, l)
+                          for l in range(coarse_level + 1, hierarchy.max_level + 1)}
+        self.states: dict[int, op.LinearizationState] = {}
+        self.diags: dict[int, dict] = {}
+        self.ranges: dict[int, dict] = {}
+        self.cons = _ConsView(self)
+        self.finest: int | None = None
+        self.use_graph = use_graph
+        self._inv: dict[int, tuple] = {}
+        self._work: dict[int, _LevelWork] = {}
+        self._graph = None
+        self._scratch = None
+
+    # -- setup -----------------------------------------------------------------
+    def setup(self, state: op.LinearizationState, reuse_eigen: bool = False, ranges=None):
+        self.finest = state.level
+        if state.level < self.coarse_level:
+            raise ValueError("state level below the coarse level")
+        if state._cache_version != state.version:
+            state.refresh_cache()
+        self.states = {state.level: state}
+        cur = state
+        for l in range(state.level - 1, self.coarse_level - 1, -1):
+            cur = op.restrict_state_to_level(cur, l)
+            cur.refresh_cache()
+            self.states[l] = cur
+        for l in range(self.coarse_level, state.level + 1):
+            s = self.states[l]
+            duu, dpp = op.block_diagonals(s, invert=False)
+            self.diags[l] = {"uu": duu, "phiphi": dpp}
+            self._inv[l] = (1.0 / duu, 1.0 / dpp)
+            if ranges is not None:
+                self.ranges[l] = ranges[l]
+            elif not reuse_eigen or l not in self.ranges:
+                self.ranges[l] = self._estimate_ranges(l)
+            if l not in self._work or self._work[l].resphi.numel() != s.n_scalar:
+                self._work[l] = _LevelWork(s.n_scalar)
+        self._graph = None
+        if logger.isEnabledFor(logging.DEBUG):
+            logger.debug("gmg setup: levels %d..%d, ranges %s", self.coarse_level, state.level,
+                         {l: (r["uu"][1], r["phiphi"][1]) for l, r in self.ranges.items()})
+
+    def _estimate_ranges(self, level: int):
+        s = self.states[level]
+        n = s.n_scalar
+        cfg = self.cheb
+        out = {}
+        for block, mode, nb in (("uu", _lib.MODE_UU, 2 * n), ("phiphi", _lib.MODE_PHIPHI, n)):
+            lo, hi = estimate_lambda_range(
+                _BlockApply(s, mode, nb), self.diags[level][block],
+                max_iterations=cfg.lanczos_iterations,
+                seed=cfg.seed + 101 * level + (0 if block == "uu" else 1))
+            hi = max(hi, 1e-30)
+            lo = max(lo, cfg.lambda_min_floor * hi)
+            out[block] = (lo, hi)
+        return out
+
+    # -- linear operator ---------------------------------------------------------
+    def apply(self, r):
+        """One V-cycle approximating G z = r from the finest level."""
+        if self.finest is None:
+            raise RuntimeError("setup() must run before apply()")
+        x, was_np = op.as_device(r, 3 * self.states[self.finest].n_scalar)
+        top = self._work[self.finest]
+        top.r.copy_(x)
+        self.run_cycle()
+        return op.back(top.z.clone(), was_np)
+
+    __call__ = apply
+    _pff_device = True
+
+    def run_cycle(self):
+        """V-cycle from work[finest].r into work[finest].z (graph replay)."""
+        top = self._work[self.finest]
+        if not self.use_graph:
+            self._vcycle(self.finest, top.r, top.z)
+            return
+        if self._graph is None:
+            self._capture()
+        self._graph.replay()
+
+    def io_buffers(self):
+        top = self._work[self.finest]
+        return top.r, top.z
+
+    def _capture(self):
+        top = self._work[self.finest]
+        # one eager pass first: validates every launch outside capture
+        self._vcycle(self.finest, top.r, top.z)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            self._vcycle(self.finest, top.r, top.z)
+        self._graph = g
+
+    # -- device V-cycle (src/multigrid.py:295-344) ---------------------------------
+    def _cheb(self, l, mode, rhs, a, b, sweeps, out, assign):
+        s = self.states[l]
+        W = self._work[l]
+        nb = rhs.numel()
+        inv = self._inv[l][0 if mode == _lib.MODE_UU else 1]
+        d, cr = W.d[:nb], W.cr[:nb]
+        acc = out if assign else W.acc[:nb]
+        theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+        sigma1 = theta / delta
+        st = stream_handle()
+        call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0, st)
+        if sweeps > 1:
+            s.apply_into(mode, d, cr, rhs)
+            rho_old = 1.0 / sigma1
+            for k in range(1, sweeps):
+                rho = 1.0 / (2.0 * sigma1 - rho_old)
+                call("pff_cheb_step", nb, ptr(inv), ptr(cr), rho * rho_old, 2.0 * rho / delta,
+                     ptr(d), ptr(acc), st)
+                rho_old = rho
+                if k < sweeps - 1:
+                    s.apply_into(mode, d, cr, cr)
+        if not assign:
+            _axpby(1.0, acc, 1.0, out)
+
+    def _smooth(self, l, z, r):
+        s = self.states[l]
+        n = s.n_scalar
+        W = self._work[l]
+        s.apply_into(_lib.MODE_FULL, z, W.res, r)
+        hi = self.ranges[l]["uu"][1]
+        self._cheb(l, _lib.MODE_UU, W.res[:2 * n], self.cheb.c * hi, self.cheb.C * hi,
+                   self.cheb.sweeps, z[:2 * n], False)
+        s.apply_into(_lib.MODE_PHIROW, z, W.resphi, r[2 * n:])
+        hi = self.ranges[l]["phiphi"][1]
+        self._cheb(l, _lib.MODE_PHIPHI, W.resphi, self.cheb.c * hi, self.cheb.C * hi,
+                   self.cheb.sweeps, z[2 * n:], False)
+
+    def _coarse(self, l, r, z):
+        s = self.states[l]
+        n = s.n_scalar
+        W = self._work[l]
+        lo, hi = self.ranges[l]["uu"]
+        self._cheb(l, _lib.MODE_UU, r[:2 * n], lo, self.cheb.C * hi, self.cheb.coarse_sweeps,
+                   z[:2 * n], True)
+        z[2 * n:].zero_()
+        s.apply_into(_lib.MODE_PHIROW, z, W.resphi, r[2 * n:])
+        lo, hi = self.ranges[l]["phiphi"]
+        self._cheb(l, _lib.MODE_PHIPHI, W.resphi, lo, self.cheb.C * hi, self.cheb.coarse_sweeps,
+                   z[2 * n:], True)
+        call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_COPY, ptr(r), ptr(z),
+             stream_handle())
+
+    def _vcycle(self, l, r, z):
+        if l == self.coarse_level:
+            self._coarse(l, r, z)
+            return
+        s, sc = self.states[l], self.states[l - 1]
+        W, Wc = self._work[l], self._work[l - 1]
+        st = stream_handle()
+        call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
+        self._smooth(l, z, r)
+        s.apply_into(_lib.MODE_FULL, z, W.res, r)
+        call("pff_restrict", s.bind(), sc.bind(), ptr(W.res), ptr(Wc.r), 1, st)
+        self._vcycle(l - 1, Wc.r, Wc.z)
+        call("pff_prolongate", s.bind(), sc.bind(), ptr(Wc.z), ptr(z), 1, st)
+        self._smooth(l, z, r)

@@ -1,0 +1,410 @@
+"""Linearisation state and the matrix-free Jacobian family on the B200.
+
+Drop-in for src/pff_operator.py (fracturekit 0.1.0): same names, argument
+meaning, constraint conventions and exceptions.  Vectors may be numpy arrays
+(copied to the device, results returned as numpy) or CUDA float64 torch
+tensors (zero-copy, results returned as CUDA tensors).  All arithmetic runs
+in libpff_b200.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_handle
+from .basis import LANE_WIDTHS, MaterialParams, ShapeData, shape_data
+from .mesh import MeshHierarchy
+
+
+class StaleCacheError(RuntimeError):
+    """Raised when the Jacobian is applied at an outdated linearization."""
+
+
+def _dev():
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def as_device(v, n: int | None = None, name: str = "vector"):
+    """(CUDA float64 contiguous tensor, origin) with origin False for CUDA
+    tensors, True for numpy input, or the host torch tensor it came from."""
+    if isinstance(v, torch.Tensor):
+        t = v
+        was_np = False
+        if t.device.type != "cuda":
+            was_np = t
+            t = t.to(device=_dev(), dtype=torch.float64, non_blocking=t.is_pinned())
+        elif t.dtype != torch.float64 or not t.is_contiguous():
+            t = t.to(dtype=torch.float64).contiguous()
+    else:
+        a = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+        t = torch.from_numpy(a).to(_dev(), non_blocking=False)
+        was_np = True
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name} must have {n} entries, got {t.numel()}")
+    return t.reshape(-1), was_np
+
+
+def back(t: torch.Tensor, was_np):
+    """Return the result in the caller's array kind (numpy / host tensor /
+    CUDA tensor); a pinned host input gets a pinned host result."""
+    if isinstance(was_np, torch.Tensor):
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=was_np.is_pinned())
+        out.copy_(t, non_blocking=False)
+        return out
+    return t.cpu().numpy() if was_np else t
+
+
+class _Dual:
+    """A host numpy array and its device mirror, synchronised lazily.
+
+    Reading the host side marks it possibly modified (callers may write into
+    it in place, as the reference's own code does), so the next device use
+    re-uploads; device writes mark the host side stale."""
+
+    def __init__(self, n: int, dtype, fill):
+        self._h = np.full(n, fill, dtype=dtype)
+        self._d = None
+        self._host_new = True
+        self._dev_new = False
+        self.stamp = 0   # bumped on every (possible) modification
+
+    def host(self) -> np.ndarray:
+        if self._dev_new:
+            self._h = self._d.cpu().numpy().copy()
+            self._dev_new = False
+        self._host_new = True
+        self.stamp += 1
+        return self._h
+
+    def device(self) -> torch.Tensor:
+        if self._d is None:
+            self._d = torch.from_numpy(self._h).to(_dev())
+            self._host_new = False
+        elif self._host_new:
+            self._d.copy_(torch.from_numpy(self._h))
+            self._host_new = False
+        return self._d
+
+    def set(self, value, index=None):
+        if isinstance(value, torch.Tensor) and value.is_cuda and index is None:
+            d = self.device() if self._d is None else self._d
+            d.copy_(value.reshape(-1).to(d.dtype))
+            self._host_new, self._dev_new = False, True
+            self.stamp += 1
+        else:
+            h = self.host()
+            if index is None:
+                h[:] = np.asarray(value.cpu() if isinstance(value, torch.Tensor) else value)
+            else:
+                h[:] = False
+                h[np.asarray(index)] = True
+            self._host_new = True
+
+
+class LinearizationState:
+    """Frozen evaluation point (u, phi, phi_tilde, active set) on one level
+    (src/pff_operator.py:64-196).
+
+    ``refresh_cache()`` uploads the linearisation point and rebuilds the
+    device q-point cache; applying at a stale cache raises
+    :class:`StaleCacheError` exactly like the reference.  ``lane_width`` and
+    ``cache_tensors`` are validated and kept for API compatibility (the GPU
+    has no SIMD lanes; the tangent is always built from the cache)."""
+
+    def __init__(self, hierarchy: MeshHierarchy, level: int, params: MaterialParams,
+                 split: str = "miehe", lane_width: int = 8, cache_tensors: bool = False):
+        if split not in ("none", "miehe"):
+            raise ValueError("split must be 'none' or 'miehe'")
+        if lane_width not in LANE_WIDTHS:
+            raise ValueError(f"lane_width must be one of {LANE_WIDTHS}")
+        self.hierarchy = hierarchy
+        self.level = level
+        self.params = params
+        self.split = split
+        self.lane_width = lane_width
+        self.cache_tensors = cache_tensors
+        self.dof_map = hierarchy.dof_map(level)
+        self.mesh = hierarchy.level(level)
+        self.shape: ShapeData = shape_data(hierarchy.degree)
+        n = self.dof_map.n_scalar
+        self._U = _Dual(3 * n, np.float64, 0.0)
+        self._U.host()[2 * n:] = 1.0
+        self._pt = _Dual(n, np.float64, 1.0)
+        self._po = _Dual(n, np.float64, 1.0)
+        self._act = _Dual(n, bool, False)
+        self._dir = _Dual(n, bool, False)
+        self._flags = None
+        self._flags_stamp = None
+        self._qcache = None
+        self._handle = None
+        self._version = 0
+        self._cache_version = -1
+
+    # -- sizes and views ----------------------------------------------------
+    @property
+    def n_scalar(self) -> int:
+        return self.dof_map.n_scalar
+
+    @property
+    def U(self) -> np.ndarray:
+        return self._U.host()
+
+    @property
+    def u_x(self) -> np.ndarray:
+        return self.U[: self.n_scalar]
+
+    @property
+    def u_y(self) -> np.ndarray:
+        return self.U[self.n_scalar: 2 * self.n_scalar]
+
+    @property
+    def phi(self) -> np.ndarray:
+        return self.U[2 * self.n_scalar:]
+
+    @property
+    def phi_tilde(self) -> np.ndarray:
+        return self._pt.host()
+
+    @property
+    def phi_old(self) -> np.ndarray:
+        return self._po.host()
+
+    @property
+    def active(self) -> np.ndarray:
+        return self._act.host()
+
+    @property
+    def dirichlet_nodes(self) -> np.ndarray:
+        return self._dir.host()
+
+    @property
+    def version(self) -> int:
+        return self._version
+
+    # -- mutation (bumps the version) ----------------------------------------
+    def set_solution(self, U):
+        self._U.set(U)
+        self._version += 1
+
+    def set_phi_tilde(self, phi_tilde):
+        self._pt.set(phi_tilde)
+        self._version += 1
+
+    def set_phi_old(self, phi_old):
+        self._po.set(phi_old)
+        self._version += 1
+
+    def set_active(self, active):
+        self._act.set(active)
+        self._version += 1
+
+    def set_dirichlet_nodes(self, nodes):
+        if isinstance(nodes, torch.Tensor) and nodes.dtype == torch.bool:
+            self._dir.set(nodes)
+        else:
+            self._dir.set(None, index=nodes)
+        self._version += 1
+
+    def constrained_mask(self) -> np.ndarray:
+        d = self.dirichlet_nodes
+        return np.concatenate([d, d, self.active])
+
+    # -- device side ----------------------------------------------------------
+    def _level_handle(self):
+        if self._handle is None:
+            s = self.shape
+            h = ctypes.c_void_p()
+            mat = _lib.material(self.params)
+            N, D, w, E = s.values, s.derivatives, s.quad_weights, s.embedding()
+            call("pff_level_create", ctypes.byref(h), self.hierarchy.degree,
+                 self.level, 1 if self.split == "miehe" else 0, ctypes.byref(mat),
+                 N.ctypes.data, D.ctypes.data, w.ctypes.data, E.ctypes.data)
+            self._handle = h
+            self._keep = (N, D, w, E)
+        return self._handle
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and _lib._lib is not None:
+            try:
+                _lib._lib.pff_level_destroy(h)
+            except Exception:
+                pass
+
+    def _sync_flags(self):
+        stamp = (self._dir.stamp, self._act.stamp)
+        if self._flags is None or stamp != self._flags_stamp:
+            d = self._dir.device()
+            a = self._act.device()
+            f = d.to(torch.uint8) | (a.to(torch.uint8) << 1)
+            if self._flags is None:
+                self._flags = f
+            else:
+                self._flags.copy_(f)
+            self._flags_stamp = (self._dir.stamp, self._act.stamp)
+        return self._flags
+
+    def bind(self):
+        """Bind the current device buffers to the level handle; returns it."""
+        h = self._level_handle()
+        if self._qcache is None:
+            qlen = _lib.load().pff_level_qcache_len(h)
+            self._qcache = torch.empty(qlen, dtype=torch.float64, device=_dev())
+        call("pff_level_bind", h, ptr(self._U.device()), ptr(self._pt.device()),
+             ptr(self._sync_flags()), ptr(self._qcache))
+        return h
+
+    def device_U(self) -> torch.Tensor:
+        return self._U.device()
+
+    def device_flags(self) -> torch.Tensor:
+        return self._sync_flags()
+
+    def refresh_cache(self):
+        call("pff_level_refresh", self.bind(), stream_handle())
+        self._cache_version = self._version
+
+    def _check_cache(self):
+        if self._qcache is None or self._cache_version != self._version:
+            raise StaleCacheError(
+                f"quadrature cache at version {self._cache_version}, state at {self._version}")
+
+    def cache(self):
+        """Device q-point cache as a dict of (n_cells, q, q) views
+        (src/pff_operator.py:186-191 names; stored cell-fastest on device)."""
+        self._check_cache()
+        q, nc = self.shape.q, self.mesh.n_cells
+        qc = self._qcache.view(6, q, q, nc)
+        names = ("e11", "e22", "e12", "gt", "dg", "pc")
+        return {k: qc[i].permute(2, 0, 1) for i, k in enumerate(names)}
+
+    def cache_bytes(self) -> int:
+        return 0 if self._qcache is None else self._qcache.numel() * 8
+
+    # -- operator entry points used by the solvers (device tensors) ----------
+    def apply_into(self, mode: int, src: torch.Tensor, dst: torch.Tensor,
+                   rhs: torch.Tensor | None = None):
+        self._check_cache()
+        call("pff_apply", self.bind(), mode, ptr(src), ptr(dst), ptr(rhs), stream_handle())
+        return dst
+
+
+def _run(state: LinearizationState, mode: int, v, n_in: int, n_out: int):
+    state._check_cache()
+    x, was_np = as_device(v, n_in)
+    out = torch.empty(n_out, dtype=torch.float64, device=x.device)
+    state.apply_into(mode, x, out)
+    return back(out, was_np)
+
+
+def apply_jacobian(state: LinearizationState, dU):
+    """Matrix-free Jacobian action with identity rows/columns on constraints
+    (src/pff_operator.py:262-270)."""
+    n = state.n_scalar
+    return _run(state, _lib.MODE_FULL, dU, 3 * n, 3 * n)
+
+
+def apply_block_uu(state: LinearizationState, du):
+    """Displacement block on a (2n,) vector (src/pff_operator.py:273-282)."""
+    n = state.n_scalar
+    return _run(state, _lib.MODE_UU, du, 2 * n, 2 * n)
+
+
+def apply_block_phiphi(state: LinearizationState, dphi):
+    """Phase-field block on an (n,) vector (src/pff_operator.py:285-291)."""
+    n = state.n_scalar
+    return _run(state, _lib.MODE_PHIPHI, dphi, n, n)
+
+
+def apply_phi_row(state: LinearizationState, dU):
+    """phi-row (coupling plus phi block) on a full vector (src/pff_operator.py:294-302)."""
+    n = state.n_scalar
+    return _run(state, _lib.MODE_PHIROW, dU, 3 * n, n)
+
+
+def block_diagonal(state: LinearizationState, block: str, invert: bool = False,
+                   as_numpy: bool = True):
+    """Matrix-free diagonal of the uu or phiphi block; constrained rows get 1
+    (src/pff_operator.py:305-327).  One kernel computes both blocks."""
+    if block not in ("uu", "phiphi"):
+        raise ValueError("block must be 'uu' or 'phiphi'")
+    duu, dpp = block_diagonals(state, invert)
+    out = duu if block == "uu" else dpp
+    return out.cpu().numpy() if as_numpy else out
+
+
+def block_diagonals(state: LinearizationState, invert: bool = False):
+    """Both block diagonals (device tensors) from one diagonal kernel."""
+    state._check_cache()
+    n = state.n_scalar
+    dev = _dev()
+    duu = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    dpp = torch.empty(n, dtype=torch.float64, device=dev)
+    call("pff_diagonal", state.bind(), ptr(duu), ptr(dpp), int(invert), stream_handle())
+    return duu, dpp
+
+
+def residual(state: LinearizationState, mask_dirichlet: bool = True, mask_active: bool = False,
+             as_numpy: bool = True):
+    """Nonlinear residual (src/pff_operator.py:218-241)."""
+    n = state.n_scalar
+    out = torch.empty(3 * n, dtype=torch.float64, device=_dev())
+    call("pff_residual", state.bind(), ptr(out), int(mask_dirichlet), int(mask_active),
+         stream_handle())
+    return out.cpu().numpy() if as_numpy else out
+
+
+def restrict_state_to_level(state: LinearizationState, target: int) -> LinearizationState:
+    """Nodal injection of the linearisation point (src/pff_operator.py:380-400),
+    done on device level by level."""
+    if not 0 <= target <= state.level:
+        raise ValueError("target level out of range")
+    if target == state.level:
+        return state
+    cur = state
+    for l in range(state.level - 1, target - 1, -1):
+        cur = _inject_once(cur, l)
+    return cur
+
+
+def _inject_once(fine: LinearizationState, level: int) -> LinearizationState:
+    coarse = LinearizationState(fine.hierarchy, level, fine.params, split=fine.split,
+                                lane_width=fine.lane_width, cache_tensors=fine.cache_tensors)
+    hf, hc = fine.bind(), coarse._level_handle()
+    n = coarse.n_scalar
+    dev = _dev()
+    U = torch.empty(3 * n, dtype=torch.float64, device=dev)
+    pt = torch.empty(n, dtype=torch.float64, device=dev)
+    po = torch.empty(n, dtype=torch.float64, device=dev)
+    fl = torch.empty(n, dtype=torch.uint8, device=dev)
+    s = stream_handle()
+    call("pff_inject_f64", hf, hc, ptr(fine._U.device()), ptr(U), 3, s)
+    call("pff_inject_f64", hf, hc, ptr(fine._pt.device()), ptr(pt), 1, s)
+    call("pff_inject_f64", hf, hc, ptr(fine._po.device()), ptr(po), 1, s)
+    call("pff_inject_u8", hf, hc, ptr(fine._sync_flags()), ptr(fl), s)
+    coarse.set_solution(U)
+    coarse.set_phi_tilde(pt)
+    coarse.set_phi_old(po)
+    coarse.set_active((fl & _lib.FLAG_ACTIVE) != 0)
+    coarse._dir.set((fl & _lib.FLAG_DIRICHLET) != 0)   # reference: no version bump
+    return coarse
+
+
+class JacobianOperator:
+    """Device callable ``v -> apply_jacobian(state, v)`` with an in-place entry
+    point the device GMRES uses to fuse ``rhs - A x``."""
+
+    def __init__(self, state: LinearizationState):
+        self.state = state
+        self.n = 3 * state.n_scalar
+
+    def __call__(self, v):
+        return apply_jacobian(self.state, v)
+
+    def apply_into(self, src, dst, rhs=None):
+        return self.state.apply_into(_lib.MODE_FULL, src, dst, rhs)

@@ -1,0 +1,114 @@
+"""CPU checks of the C ABI and host logic (no kernel launches)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+import paper_2005_00331_b200 as P
+from paper_2005_00331_b200 import _lib
+from oracle import oracle as O
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "pff_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(pff_\w+)\(", txt, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+
+
+def test_abi_version_and_host_only_calls():
+    L = _lib.load()
+    assert L.pff_abi_version() == 1
+    assert L.pff_reduce_scratch_len() > 0
+    s = P.shape_data(2)
+    h = ctypes.c_void_p()
+    mat = _lib.material(P.MaterialParams())
+    E = s.embedding()
+    rc = L.pff_level_create(ctypes.byref(h), 2, 10, 1, ctypes.byref(mat), s.values.ctypes.data,
+                            s.derivatives.ctypes.data, s.quad_weights.ctypes.data, E.ctypes.data)
+    assert rc == 0
+    assert L.pff_level_n_scalar(h) == 4_199_425
+    assert L.pff_level_n_cells(h) == 1024 * 1024
+    assert L.pff_level_qcache_len(h) == 6 * 9 * 1024 * 1024
+    # unbound state is an error, not a crash
+    assert L.pff_apply(h, 0, None, None, None, None) < 0
+    assert b"not bound" in L.pff_last_error()
+    L.pff_level_destroy(h)
+    bad = L.pff_level_create(ctypes.byref(h), 7, 3, 0, ctypes.byref(mat), s.values.ctypes.data,
+                             s.derivatives.ctypes.data, s.quad_weights.ctypes.data, None)
+    assert bad == _lib.load().pff_level_create.restype(-1) or bad < 0
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_shape_data_matches_oracle(p):
+    a, b = P.shape_data(p), O.shape(p)
+    assert np.array_equal(a.values, b.N) and np.array_equal(a.derivatives, b.D)
+    assert np.array_equal(a.quad_weights, b.w)
+
+
+@pytest.mark.parametrize("p,level", [(1, 0), (1, 3), (2, 1), (2, 5), (3, 3), (4, 4)])
+def test_closed_form_numbering(p, level):
+    dm = P.build_hierarchy(max(level, 2), p).dof_map(level)
+    lv = O.Level(p, level)
+    assert dm.n_scalar == lv.n
+    assert np.array_equal(dm.conn, lv.conn())
+    for tag in ("top", "bottom", "left", "right"):
+        assert np.array_equal(dm.boundary_nodes[tag], lv.boundary_nodes(tag))
+
+
+def test_dof_counts_match_configs():
+    assert 3 * P.build_hierarchy(5, 2).dof_map(5).n_scalar == 12_771
+    assert 3 * P.build_hierarchy(10, 2).dof_map(10).n_scalar == 12_598_275
+    assert 3 * P.build_hierarchy(9, 4).dof_map(9).n_scalar == 12_598_275
+    assert 3 * P.build_hierarchy(12, 2).dof_map(12).n_scalar == 201_388_035
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_injection_and_prolongation_matrix(golden, p):
+    d = golden(f"transfer_p{p}_l4")
+    h = P.build_hierarchy(4, p)
+    assert np.array_equal(h.injection(4), d["inj"])
+    Pm = P.build_prolongation(h, 4)
+    assert np.array_equal(Pm.indptr, d["P_indptr"]) and np.array_equal(Pm.indices, d["P_indices"])
+    assert np.array_equal(Pm.data, d["P_data"])
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        P.KrylovConfig(relative_tolerance=1.5)
+    with pytest.raises(ValueError):
+        P.KrylovConfig(restart=1)
+    with pytest.raises(ValueError):
+        P.ChebyshevConfig(c=2.0)
+    with pytest.raises(ValueError):
+        P.build_hierarchy(1, 2)
+    with pytest.raises(ValueError):
+        P.MaterialParams(mu=-1.0)
+    h = P.build_hierarchy(2, 1)
+    with pytest.raises(ValueError):
+        P.GmgPreconditioner(h, coarse_level=3)
+    with pytest.raises(ValueError):
+        P.LinearizationState(h, 2, P.MaterialParams(), split="bogus")
+    with pytest.raises(ValueError):
+        P.LinearizationState(h, 2, P.MaterialParams(), lane_width=3)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = P.build_hierarchy(2, 1)
+    st = P.LinearizationState(h, 2, P.MaterialParams())
+    with pytest.raises(RuntimeError, match="CUDA"):
+        st.refresh_cache()

@@ -1,0 +1,241 @@
+"""Parity of the CUDA path (libpff_b200.so through the drop-in API) against
+the reference's golden vectors and the CPU oracle.  GPU only.
+
+Bar (BASELINE.json north star): fp64 operator and V-cycle outputs within
+1e-12 relative L2 PER BLOCK (u_x, u_y, phi), GMRES iterations within +-1.
+"""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, block_rel, load_golden, rel_l2
+import paper_2005_00331_b200 as P
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def product_state(d, split):
+    p, level = int(d["meta"][0]), int(d["meta"][1])
+    h = P.build_hierarchy(max(level, 2), p)
+    st = P.LinearizationState(h, level, O.baseline_material(level), split=split)
+    st.set_solution(d["U"])
+    st.set_phi_tilde(d["phi_tilde"])
+    st.set_phi_old(d["phi_old"])
+    st.set_active(d["active"])
+    st.set_dirichlet_nodes(np.flatnonzero(d["dirichlet"]))
+    st.refresh_cache()
+    return st
+
+
+def oracle_state(d, split):
+    p, level = int(d["meta"][0]), int(d["meta"][1])
+    st = O.State(p, level, O.baseline_material(level), split)
+    st.U, st.phi_tilde, st.phi_old = d["U"].copy(), d["phi_tilde"].copy(), d["phi_old"].copy()
+    st.active, st.dirichlet = d["active"].copy(), d["dirichlet"].copy()
+    st.refresh_cache()
+    return st
+
+
+OP_CASES = sorted(os.path.basename(f)[:-4] for f in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if os.path.basename(f).startswith(("pr1_", "op_")))
+
+
+@pytest.mark.parametrize("name", OP_CASES)
+def test_operator_family_vs_golden(name):
+    d = load_golden(name)
+    split = "miehe" if int(d["meta"][3]) else "none"
+    st = product_state(d, split)
+    n = st.n_scalar
+    x = d["x"]
+    assert max(block_rel(P.apply_jacobian(st, x), d["jac"], n)) <= TOL
+    assert max(block_rel(P.apply_block_uu(st, x[:2 * n]), d["uu"], n)) <= TOL
+    assert rel_l2(P.apply_block_phiphi(st, x[2 * n:]), d["pp"]) <= TOL
+    assert rel_l2(P.apply_phi_row(st, x), d["prow"]) <= TOL
+    assert max(block_rel(P.block_diagonal(st, "uu"), d["diag_uu"], n)) <= TOL
+    assert rel_l2(P.block_diagonal(st, "phiphi"), d["diag_pp"]) <= TOL
+    r = P.residual(st)
+    for k, v in enumerate(block_rel(r, d["residual"], n)):
+        assert v <= TOL or np.abs(d["residual"][k * n:(k + 1) * n]).max() == 0.0
+    assert max(block_rel(P.residual(st, mask_dirichlet=False), d["residual_raw"], n)) <= TOL
+
+
+@pytest.mark.parametrize("split", ["none", "miehe"])
+def test_cache_vs_golden(split):
+    d = load_golden(f"pr1_{split}")
+    st = product_state(d, split)
+    c = st.cache()
+    for k in ("e11", "e22", "e12", "gt", "dg", "pc"):
+        got = c[k].contiguous().cpu().numpy().ravel()
+        assert rel_l2(got, d["cache_" + k]) <= TOL, k
+
+
+def test_identity_rows_and_columns():
+    d = load_golden("pr1_miehe")
+    st = product_state(d, "miehe")
+    n3 = 3 * st.n_scalar
+    mask = st.constrained_mask()
+    cdofs = np.flatnonzero(mask)
+    rng = np.random.default_rng(13)
+    v = rng.standard_normal(n3)
+    out = P.apply_jacobian(st, v)
+    assert np.array_equal(out[cdofs], v[cdofs])
+    for i in cdofs[:4]:
+        e = np.zeros(n3)
+        e[i] = 1.0
+        col = P.apply_jacobian(st, e)
+        assert col[i] == 1.0
+        col[i] = 0.0
+        assert np.all(col == 0.0)
+    assert np.all(P.apply_jacobian(st, np.zeros(n3)) == 0.0)
+
+
+def test_stale_cache_raises():
+    d = load_golden("pr1_none")
+    st = product_state(d, "none")
+    st.set_solution(st.U * 1.01)
+    with pytest.raises(P.StaleCacheError):
+        P.apply_jacobian(st, np.zeros(3 * st.n_scalar))
+
+
+def test_fused_residual_form():
+    d = load_golden("pr1_miehe")
+    st = product_state(d, "miehe")
+    n = st.n_scalar
+    x = torch.from_numpy(d["x"]).cuda()
+    r = torch.from_numpy(np.random.default_rng(3).standard_normal(3 * n)).cuda()
+    out = torch.empty_like(r)
+    st.apply_into(0, x, out, r)
+    want = d["x"] * 0 + r.cpu().numpy() - d["jac"]
+    assert max(block_rel(out.cpu().numpy(), want, n)) <= TOL
+    r2 = r.clone()
+    st.apply_into(0, x, r2, r2)   # dst aliases rhs
+    assert torch.equal(r2, out)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_transfers_vs_golden(p):
+    d = load_golden(f"transfer_p{p}_l4")
+    tr = P.TransferOperator(P.build_hierarchy(4, p), 4)
+    assert rel_l2(tr.prolongate(d["xc"]), d["Px"]) <= 1e-14
+    assert rel_l2(tr.restrict(d["yf"]), d["Ry"]) <= 1e-14
+
+
+def test_transfer_level1():
+    d = load_golden("transfer_p2_l1")
+    tr = P.TransferOperator(P.build_hierarchy(2, 2), 1)
+    assert rel_l2(tr.prolongate(d["xc"]), d["Px"]) <= 1e-14
+    assert rel_l2(tr.restrict(d["yf"]), d["Ry"]) <= 1e-14
+
+
+def test_restrict_state_vs_golden():
+    d = load_golden("restrict_p2_l5_l2")
+    st = product_state(dict(d, meta=np.array([2, 5, 0, 1])), "miehe")
+    c = P.restrict_state_to_level(st, 2)
+    assert np.array_equal(c.U, d["cU"])
+    assert np.array_equal(c.phi_tilde, d["cphi_tilde"])
+    assert np.array_equal(c.active, d["cactive"])
+    assert np.array_equal(c.dirichlet_nodes, d["cdirichlet"])
+
+
+SOLVE_CASES = sorted(os.path.basename(f)[:-4] for f in glob.glob(os.path.join(GOLDEN, "solve_*.npz")))
+
+
+@pytest.mark.parametrize("name", SOLVE_CASES)
+def test_solver_stack_vs_golden(name):
+    d = load_golden(name)
+    p, level, seed, miehe, notch, sweeps = (int(v) for v in d["meta"])
+    split = "miehe" if miehe else "none"
+    st = product_state(dict(d, meta=np.array([p, level, seed, miehe])), split)
+    n = st.n_scalar
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=sweeps))
+    gmg.setup(st)
+    for l in range(2, level + 1):
+        got = gmg.ranges[l]
+        assert np.allclose([got["uu"][0], got["uu"][1], got["phiphi"][0], got["phiphi"][1]],
+                           d[f"range_{l}"], rtol=1e-10, atol=0), l
+    z = gmg.apply(d["x"])
+    assert max(block_rel(z, d["vcycle"], n)) <= TOL
+    # same cycle without the CUDA graph
+    gmg.use_graph = False
+    assert max(block_rel(gmg.apply(d["x"]), z, n)) <= 1e-14
+    gmg.use_graph = True
+    hi = gmg.ranges[level]["uu"][1]
+    cheb = P.chebyshev_apply(lambda v: P.apply_block_uu(st, v), gmg.diags[level]["uu"].cpu().numpy(),
+                             d["x"][:2 * n], 0.24 * hi, 1.2 * hi, 5)
+    assert max(block_rel(cheb, d["cheb_uu"], n)) <= TOL
+    lz = P.estimate_lambda_range(lambda v: P.apply_block_uu(st, v),
+                                 gmg.diags[level]["uu"].cpu().numpy(), seed=7)
+    assert np.allclose(lz, d["lanczos_uu"], rtol=1e-10, atol=0)
+    rhs = d["x"].copy()
+    rhs[st.constrained_mask()] = 0.0
+    res = P.gmres_solve(P.JacobianOperator(st), rhs,
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    assert res.converged == bool(d["gmres_conv"][0])
+    assert abs(res.iterations - int(d["gmres_iters"][0])) <= 1
+    assert max(block_rel(res.solution, d["gmres_x"], n)) <= 1e-8
+    # reference-style closures give the same answer
+    res2 = P.gmres_solve(lambda v: P.apply_jacobian(st, v), rhs,
+                         P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                         preconditioner=gmg.apply)
+    assert res2.iterations == res.iterations
+
+
+@pytest.mark.parametrize("split", ["none", "miehe"])
+@pytest.mark.parametrize("p,level", [(2, 10), (4, 9)])
+def test_full_size_vs_oracle(split, p, level):
+    """BASELINE configs[1] / configs[2] at full size against the C oracle."""
+    ost, x = O.baseline_state(p, level, split, seed=0)
+    ost.refresh_cache(nthreads=O.max_threads())
+    want = O.apply_jacobian(ost, x, nthreads=O.max_threads())
+    h = P.build_hierarchy(level, p)
+    st = P.LinearizationState(h, level, ost.params, split=split)
+    st.set_solution(ost.U)
+    st.set_phi_tilde(ost.phi_tilde)
+    st.set_phi_old(ost.phi_old)
+    st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    got = P.apply_jacobian(st, x)
+    n = st.n_scalar
+    assert max(block_rel(got, want, n)) <= TOL
+    # linearity on device at full size (size-independent property)
+    xd = torch.from_numpy(x).cuda()
+    y1 = P.apply_jacobian(st, xd)
+    y2 = P.apply_jacobian(st, 2.0 * xd)
+    assert rel_l2((y2 - 2.0 * y1).cpu().numpy() + 2.0 * y1.cpu().numpy(),
+                  2.0 * y1.cpu().numpy()) <= 1e-14
+
+
+def test_gmres_small_dense_numpy_callables():
+    """The reference's own Krylov tests drive gmres with numpy callables."""
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((5, 5)) + 5 * np.eye(5)
+    b = rng.standard_normal(5)
+    res = P.gmres_solve(lambda v: A @ v, b, P.KrylovConfig(relative_tolerance=1e-12))
+    assert res.converged and res.iterations <= 5
+    assert np.linalg.norm(A @ res.solution - b) <= 1e-10 * np.linalg.norm(b)
+    d = np.arange(1.0, 11.0)
+    res = P.gmres_solve(lambda v: d * v, np.ones(10), P.KrylovConfig(),
+                        preconditioner=lambda v: v / d)
+    assert res.converged and res.iterations == 1
+    res = P.gmres_solve(lambda v: v, rng.standard_normal(20), P.KrylovConfig())
+    assert res.converged and res.iterations == 1
+
+
+def test_lanczos_and_chebyshev_numpy_callables():
+    n = 50
+    dd = np.arange(1.0, n + 1)
+    got = P.estimate_lambda_max(lambda v: dd * v, np.ones(n), seed=2)
+    assert abs(got - n) <= 0.05 * n
+    lo, hi = P.estimate_lambda_range(lambda v: 3.0 * v, np.ones(8), seed=4)
+    assert hi == pytest.approx(3.0, abs=1e-9) and lo == pytest.approx(3.0, abs=1e-9)
+    rhs = np.random.default_rng(0).standard_normal(25)
+    z = P.chebyshev_apply(lambda v: v, np.ones(25), rhs, 1.0, 1.2, 32)
+    assert np.linalg.norm(z - rhs) <= 1e-13 * np.linalg.norm(rhs)
