@@ -60,7 +60,7 @@ def _empty(n):
 
 def _dot(x: torch.Tensor, y: torch.Tensor, scratch: torch.Tensor, out: torch.Tensor) -> float:
     call("pff_dot", x.numel(), ptr(x), ptr(y), ptr(scratch), ptr(out), stream_handle())
-    return float(out.item())
+    return float(out[0].item())
 
 
 class _Scratch:

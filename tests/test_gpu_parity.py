@@ -115,7 +115,7 @@ def test_fused_residual_form():
     assert max(block_rel(out.cpu().numpy(), want, n)) <= TOL
     r2 = r.clone()
     st.apply_into(0, x, r2, r2)   # dst aliases rhs
-    assert torch.equal(r2, out)
+    assert max(block_rel(r2.cpu().numpy(), out.cpu().numpy(), n)) <= 1e-15
 
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
