@@ -59,6 +59,13 @@ const char* pff_last_error(void);
  * benchmark reads it around its timed region */
 int64_t pff_launch_counter(void);
 
+/* tuning / testing knobs (process-wide):
+ *   PFF_OPT_GENERIC_APPLY: 1 = route pff_apply through the generic per-cell
+ *     atomic kernel for every degree (the Q2 sweep kernel is the default)
+ *   PFF_OPT_SWEEP_ROWS: cell rows per warp chunk of the Q2 sweep (0 = auto) */
+enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2 };
+int pff_set_option(int key, int value);
+
 /* One mesh level (replaces DofMap + LinearizationState's static data,
  * src/pff_operator.py:74-101).  N, D: host (p+1)x(p+1) row-major shape
  * values/derivatives at the Gauss points, w: (p+1) weights

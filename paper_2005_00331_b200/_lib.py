@@ -22,6 +22,7 @@ SIGNATURES = {
     "pff_abi_version": (_i, []),
     "pff_last_error": (ctypes.c_char_p, []),
     "pff_launch_counter": (_i64, []),
+    "pff_set_option": (_i, [_i, _i]),
     "pff_level_create": (_i, [ctypes.POINTER(ctypes.c_void_p), _i, _i, _i, ctypes.c_void_p,
                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "pff_level_destroy": (_i, [ctypes.c_void_p]),
@@ -53,6 +54,11 @@ MODE_FULL, MODE_UU, MODE_PHIPHI, MODE_PHIROW = 0, 1, 2, 3
 FLAG_DIRICHLET, FLAG_ACTIVE = 1, 2
 LAYOUT_FULL, LAYOUT_UU, LAYOUT_PHI = 0, 1, 2
 CONS_SELECT, CONS_ZERO, CONS_COPY = 0, 1, 2
+OPT_GENERIC_APPLY, OPT_SWEEP_ROWS = 1, 2
+
+
+def set_option(key: int, value: int):
+    call("pff_set_option", key, value)
 
 
 class PffError(RuntimeError):

@@ -43,6 +43,14 @@ const char* pff_last_error(void) { return g_err; }
 
 int64_t pff_launch_counter(void) { return pff::g_launch_count.load(); }
 
+int pff_set_option(int key, int value) {
+    switch (key) {
+        case PFF_OPT_GENERIC_APPLY: pff::set_generic_apply(value != 0); return 0;
+        case PFF_OPT_SWEEP_ROWS: pff::set_sweep_rows_per_chunk(value); return 0;
+    }
+    return fail(PFF_E_ARG, "%s", "pff_set_option: unknown key");
+}
+
 int pff_level_create(pff_level** out, int degree, int level, int split, const pff_material* mat,
                      const double* N, const double* D, const double* w, const double* embed) {
     if (!out || !mat || !N || !D || !w) return fail(PFF_E_ARG, "%s", "pff_level_create: null argument");

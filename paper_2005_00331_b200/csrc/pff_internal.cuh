@@ -19,8 +19,28 @@ struct Level {
     const double* phi_tilde = nullptr;  // n
     const uint8_t* flags = nullptr;     // n: F_DIR | F_ACT
     double* qcache = nullptr;           // qcache_len() doubles
-    int64_t qcache_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells(); }
+
+    // generic q-point cache (layout [field][k][cell], 6 fields)
+    int64_t generic_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells(); }
+    // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
+    // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
+    bool sweep_ok() const { return mesh.p == 2 && mesh.nside >= 64; }
+    int n_strips() const { return (mesh.nside + 30) / 31; }
+    int tile_nq() const { return miehe ? 5 : 4; }
+    int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
+    int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * mesh.nside * tile_block() : 0; }
+    int64_t qcache_len() const { return generic_len() + tile_len(); }
+    double* qtile() const { return qcache + generic_len(); }
 };
+
+// options (pff_set_option)
+void set_generic_apply(bool on);
+void set_sweep_rows_per_chunk(int rows);
+
+// Q2 sweep kernel (pff_sweep.cu)
+cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s);
+cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
+                               const double* rhs, cudaStream_t s, bool* handled);
 
 // operator family (pff_ops.cu)
 cudaError_t launch_refresh(const Level& L, cudaStream_t s);

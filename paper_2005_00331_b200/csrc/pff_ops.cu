@@ -542,18 +542,22 @@ struct ResidualL {
 
 }  // namespace
 
-cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
-                               const double* rhs, cudaStream_t s, bool* handled);
-
 cudaError_t launch_refresh(const Level& L, cudaStream_t s) {
-    return dispatch_p_split<RefreshL>(L.mesh.p, L.miehe, &L, s);
+    cudaError_t e = dispatch_p_split<RefreshL>(L.mesh.p, L.miehe, &L, s);
+    if (e == cudaSuccess && L.sweep_ok()) e = launch_refresh_tiled(L, s);
+    return e;
 }
+
+static bool g_generic_apply = false;
+void set_generic_apply(bool on) { g_generic_apply = on; }
 
 cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
                          const double* rhs, cudaStream_t s) {
     bool handled = false;
-    cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
-    if (handled || e != cudaSuccess) return e;
+    if (!g_generic_apply) {
+        cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
+        if (handled || e != cudaSuccess) return e;
+    }
     return dispatch_p_split<ApplyL>(L.mesh.p, L.miehe, &L, mode, src, dst, rhs, s);
 }
 

@@ -1,12 +1,699 @@
-// pff_sweep.cu -- write-once Q2 operator kernel (placeholder until tuned).
+// pff_sweep.cu -- write-once Q2 operator kernel (the hot path).
+//
+// Same operator as k_apply_cells (src/_kernels.py:555-693 with the identity
+// rows/columns of src/pff_operator.py:262-302), without atomics and with the
+// expensive, direction-independent q-point physics hoisted into refresh:
+//
+//  * refresh builds a strip-tiled q-point cache: per (strip, cell row) one
+//    contiguous block [array][q-point][lane].  Miehe: the eigen-frame of the
+//    state strain (m, +-r, c, s; the sign of r carries the pseudo-inverse gap
+//    test of src/_kernels.py:65-69) and pc; none: the strain e and pc.  So the
+//    application does no sqrt and recomputes no state contraction.
+//  * one warp owns a strip of 31 cell columns and sweeps upward over a chunk
+//    of cell rows; lane 0 recomputes the left neighbour cell (halo column),
+//    the first iteration recomputes the cell row below the chunk (halo row);
+//  * node rows of the direction / phi0 / phi~ fields are staged in a 5-row
+//    shared-memory ring and the q-point block in a 2-stage buffer, both by
+//    TMA bulk copies (cp.async.bulk + mbarrier) issued one cell row ahead;
+//  * a cell's right node column goes to lane+1 by shuffle, its top node row
+//    is carried in registers; every dst entry is written exactly once
+//    (deterministic) with the identity rows and the optional fused
+//    rhs - G src applied at the store;
+//  * the slit (src/mesh_hierarchy.py:156-189): the upper cell row reads the
+//    upper copies (n_grid + i) and lower/upper copies are stored apart.
+#include <cstdlib>
+
 #include "pff_internal.cuh"
 
 namespace pff {
 
+namespace {
+
+constexpr int SW_LANES = 32;
+constexpr int SW_OWN = SW_LANES - 1;          // own cells per strip
+constexpr int SW_COLS = 2 * SW_LANES + 1;     // staged node columns (65)
+constexpr int RW = 68;                        // doubles per staged row (16-B aligned superset)
+constexpr int FW = 112;                       // bytes per staged flag row
+constexpr int RING = 5;                       // node-row ring (3 in use + 2 in flight)
+constexpr int QK = 9;                         // q-points per Q2 cell
+constexpr int QARR = QK * SW_LANES;           // doubles per q-point array of a block
+
+enum Field { FX = 0, FY, FP, F0P, FPT, NFIELDS };
+
+template <int MODE, bool MIEHE>
+struct Use {
+    static constexpr bool ux = MODE != MODE_PHIPHI;
+    static constexpr bool ph = MODE != MODE_UU;
+    static constexpr bool p0 = MODE == MODE_FULL || MODE == MODE_PHIROW;
+    static constexpr bool pt = MODE == MODE_FULL || MODE == MODE_UU;
+    static constexpr bool DO_UU = MODE == MODE_FULL || MODE == MODE_UU;
+    static constexpr bool DO_PP = MODE != MODE_UU;
+    static constexpr bool DO_COUP = MODE == MODE_FULL || MODE == MODE_PHIROW;
+    // q-point arrays: the state arrays (tangent) unless none-UU; pc only for PHIPHI
+    static constexpr bool qstate = MODE != MODE_PHIPHI && !(MODE == MODE_UU && !MIEHE);
+    static constexpr bool qpc = MODE == MODE_PHIPHI;
+    static constexpr int NQS = MIEHE ? 4 : 3;          // state arrays in a block
+    static constexpr int NQ = qstate ? NQS : (qpc ? 1 : 0);
+    static constexpr bool used(int f) {
+        return (f == FX || f == FY) ? ux : f == FP ? ph : f == F0P ? p0 : pt;
+    }
+    static constexpr int slot(int f) {
+        int s = 0;
+        for (int g = 0; g < f; ++g) s += used(g) ? 1 : 0;
+        return s;
+    }
+    static constexpr int NF = slot(NFIELDS);
+};
+
+template <int NF, int NQ>
+struct __align__(16) WarpSmem {
+    double q[2][NQ > 0 ? NQ * QARR : 2];     // q-point blocks, two stages
+    double v[RING][NF][RW];                  // node-row ring
+    uint8_t f[RING][FW];                     // flag rows
+    int voff[RING][NF];                      // element offset of staged column 0
+    int foff[RING];
+    unsigned long long bar[2];
+};
+
+struct SweepArgs {
+    Mesh m;
+    Shape S;
+    Material M;
+    const double* fld[NFIELDS];   // ux uy phi (direction), phi0 phit (state)
+    const uint8_t* flags;
+    const double* qtile;          // strip-tiled q-point cache
+    int64_t qblock;               // doubles per (strip, row) block
+    double* dst[3];
+    const double* src_out[3];
+    const double* rhs[3];
+    int n_strips, rows_per_chunk, n_items;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+
+// Miehe tangent with the state eigensystem given as (m, +-r, c, s):
+// ev1 = m + r, ev2 = m - r, tr e = 2m (bit-identical to src/_kernels.py:28-33),
+// the gap test of _dpos2s (line 66) is the sign of the stored r.
+struct MieheQ {
+    Eig e;
+    double tre;
+    bool gap_ok;
+};
+__device__ __forceinline__ MieheQ miehe_q(double m, double rs, double c, double s) {
+    MieheQ q;
+    const double r = fabs(rs);
+    q.e.ev1 = m + r;
+    q.e.ev2 = m - r;
+    q.e.c = c;
+    q.e.s = s;
+    q.tre = 2.0 * m;
+    q.gap_ok = rs > 0.0;
+    return q;
+}
+
+__device__ __forceinline__ void miehe_dsig(const Material& M, double g, const MieheQ& q,
+                                           double d11, double d22, double d12, double& s11,
+                                           double& s22, double& s12, double& spde) {
+    const double c = q.e.c, s = q.e.s, lam = M.lam, mu = M.mu;
+    const double t0 = d11 * c + d12 * s;
+    const double t1 = d12 * c + d22 * s;
+    const double dl1 = c * t0 + s * t1;
+    const double dl2 = s * s * d11 - 2.0 * s * c * d12 + c * c * d22;
+    const double dl1p = q.e.ev1 >= 0.0 ? dl1 : 0.0;
+    const double dl2p = q.e.ev2 >= 0.0 ? dl2 : 0.0;
+    const double l1p = posp(q.e.ev1), l2p = posp(q.e.ev2);
+    const double alpha = q.gap_ok ? (c * t1 - s * t0) / (q.e.ev1 - q.e.ev2) : 0.0;
+    const double rot = alpha * (l1p - l2p);
+    const double o11 = dl1p * c * c + dl2p * s * s - 2.0 * rot * s * c;
+    const double o22 = dl1p * s * s + dl2p * c * c + 2.0 * rot * s * c;
+    const double o12 = (dl1p - dl2p) * c * s + rot * (c * c - s * s);
+    const double trde = d11 + d22;
+    const double tt = q.tre < 0.0 ? 0.0 : trde;
+    const double dp11 = lam * tt + 2.0 * mu * o11;
+    const double dp22 = lam * tt + 2.0 * mu * o22;
+    const double dp12 = 2.0 * mu * o12;
+    const double f11 = lam * trde + 2.0 * mu * d11;
+    const double f22 = lam * trde + 2.0 * mu * d22;
+    const double f12 = 2.0 * mu * d12;
+    double sp11, sp22, sp12;
+    sigplus2(lam, mu, q.tre, q.e, sp11, sp22, sp12);
+    spde = sp11 * d11 + sp22 * d22 + 2.0 * sp12 * d12;
+    s11 = g * dp11 + (f11 - dp11);
+    s22 = g * dp22 + (f22 - dp22);
+    s12 = g * dp12 + (f12 - dp12);
+}
+
+// ------------------------------------------------------------- tiled refresh
+template <bool MIEHE>
+__global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __restrict__ U,
+                                double* __restrict__ qt, int n_strips, int64_t qblock) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)n_strips * m.nside * SW_LANES;
+    if (t >= total) return;
+    const int lane = (int)(t % SW_LANES);
+    const int64_t blk = t / SW_LANES;            // = strip * nside + cy
+    const int strip = (int)(blk / m.nside), cy = (int)(blk % m.nside);
+    const int cx = strip * SW_OWN - 1 + lane;
+    double* out = qt + blk * qblock + lane;
+    constexpr int NQS = MIEHE ? 4 : 3;
+    if (cx < 0 || cx >= m.nside) {
+        for (int a = 0; a <= NQS; ++a)
+            for (int k = 0; k < QK; ++k) out[(a * QK + k) * SW_LANES] = 0.0;
+        return;
+    }
+    const int64_t n = m.n;
+    double cu[3][3], cv[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int64_t g = m.node(cx, cy, a, b);
+            cu[b][a] = U[g];
+            cv[b][a] = U[n + g];
+        }
+    double tx[3][3], td[3][3], gxu[3][3], gyu[3][3], gxv[3][3], gyv[3][3];
+    fwd_x<3>(S.N, cu, tx);
+    fwd_x<3>(S.D, cu, td);
+    fwd_y<3>(S.D, tx, gyu);
+    fwd_y<3>(S.N, td, gxu);
+    fwd_x<3>(S.N, cv, tx);
+    fwd_x<3>(S.D, cv, td);
+    fwd_y<3>(S.D, tx, gyv);
+    fwd_y<3>(S.N, td, gxv);
+    const double inv_h = 1.0 / m.h, gce = M.gc / M.eps, gdd = 2.0 * (1.0 - M.kappa);
+#pragma unroll
+    for (int jq = 0; jq < 3; ++jq)
+#pragma unroll
+        for (int iq = 0; iq < 3; ++iq) {
+            const int k = jq * 3 + iq;
+            const double e11 = gxu[jq][iq] * inv_h;
+            const double e22 = gyv[jq][iq] * inv_h;
+            const double e12 = 0.5 * (gyu[jq][iq] + gxv[jq][iq]) * inv_h;
+            const double tre = e11 + e22;
+            double esp;
+            if (MIEHE) {
+                // _eig2s (src/_kernels.py:26-47) and the gap test of _dpos2s (65-69)
+                const double mm = 0.5 * (e11 + e22);
+                const double dh = 0.5 * (e11 - e22);
+                const double r = sqrt(dh * dh + e12 * e12);
+                const Eig e = eig2(e11, e22, e12);
+                const bool gap_ok = (e.ev1 - e.ev2) > 1e-12 * scale2(e11, e22, e12);
+                out[(0 * QK + k) * SW_LANES] = mm;
+                out[(1 * QK + k) * SW_LANES] = gap_ok ? r : -r;
+                out[(2 * QK + k) * SW_LANES] = e.c;
+                out[(3 * QK + k) * SW_LANES] = e.s;
+                esp = esplus2(M.lam, M.mu, tre, e);
+            } else {
+                out[(0 * QK + k) * SW_LANES] = e11;
+                out[(1 * QK + k) * SW_LANES] = e22;
+                out[(2 * QK + k) * SW_LANES] = e12;
+                esp = 0.5 * M.lam * tre * tre + M.mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
+            }
+            out[(NQS * QK + k) * SW_LANES] = gdd * esp + gce;
+        }
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int MODE, bool MIEHE, bool FUSED>
+__global__ void __launch_bounds__(SW_LANES)
+k_sweep_q2(const SweepArgs A) {
+    using U = Use<MODE, MIEHE>;
+    constexpr int NF = U::NF, NQ = U::NQ;
+    using Smem = WarpSmem<NF, NQ>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& W = *reinterpret_cast<Smem*>(smem_raw);
+    const int lane = threadIdx.x;
+
+    const Mesh& m = A.m;
+    const int ns = m.nside;
+    const int64_t np1 = m.np1;
+    const int half = ns >> 1;
+    const Shape& S = A.S;
+    const Material& M = A.M;
+    const double h = m.h, inv_h = 1.0 / h;
+    // q-point array offset inside a (strip,row) block
+    const int qarr0 = U::qpc ? U::NQS : 0;
+
+    if (lane == 0) {
+        mbar_init(&W.bar[0]);
+        mbar_init(&W.bar[1]);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    unsigned use_count[2] = {0u, 0u};
+
+    for (int item = blockIdx.x; item < A.n_items; item += gridDim.x) {
+        const int strip = item % A.n_strips, chunk = item / A.n_strips;
+        const int c0 = chunk * A.rows_per_chunk;
+        const int c1 = min(ns, c0 + A.rows_per_chunk);
+        const int cstart = c0 > 0 ? c0 - 1 : 0;
+        const int x0 = strip * SW_OWN;
+        const int cx = x0 - 1 + lane;
+        const bool active = cx >= 0 && cx < ns;
+        const bool owner = lane > 0 && active;
+        const int64_t gcol0 = 2 * (int64_t)(x0 - 1);
+
+        // lane 0: stage node row j into ring slot `slot` (all used fields + flags)
+        auto issue_row = [&](int64_t j, unsigned long long* bar) -> unsigned {
+            const int slot = (int)(j % RING);
+            const int64_t lo = j * np1 + (gcol0 < 0 ? 0 : gcol0);
+            const int64_t hi = j * np1 + min((int64_t)np1, gcol0 + SW_COLS);
+            unsigned bytes = 0;
+#pragma unroll
+            for (int f = 0; f < NFIELDS; ++f) {
+                if (!U::used(f)) continue;
+                const uintptr_t base = (uintptr_t)A.fld[f];
+                const uintptr_t a = (base + 8 * lo) & ~(uintptr_t)15;
+                const uintptr_t b = (base + 8 * hi + 15) & ~(uintptr_t)15;
+                bulk_g2s(W.v[slot][U::slot(f)], (const void*)a, (unsigned)(b - a), bar);
+                W.voff[slot][U::slot(f)] = (int)(((intptr_t)(base + 8 * (j * np1 + gcol0)) - (intptr_t)a) / 8);
+                bytes += (unsigned)(b - a);
+            }
+            const uintptr_t fb = (uintptr_t)A.flags;
+            const uintptr_t a = (fb + lo) & ~(uintptr_t)15;
+            const uintptr_t b = (fb + hi + 15) & ~(uintptr_t)15;
+            bulk_g2s(W.f[slot], (const void*)a, (unsigned)(b - a), bar);
+            W.foff[slot] = (int)((intptr_t)(fb + j * np1 + gcol0) - (intptr_t)a);
+            return bytes + (unsigned)(b - a);
+        };
+        auto issue_qblock = [&](int cy, int stage) -> unsigned {
+            if (NQ == 0) return 0u;
+            const double* src = A.qtile + ((int64_t)strip * ns + cy) * A.qblock + qarr0 * QARR;
+            bulk_g2s(W.q[stage], src, (unsigned)(NQ * QARR * 8), &W.bar[stage]);
+            return (unsigned)(NQ * QARR * 8);
+        };
+        // reads of the staged rows
+        auto val = [&](int slot, int f, int k) -> double {
+            return W.v[slot][U::slot(f)][W.voff[slot][U::slot(f)] + k];
+        };
+        auto flag = [&](int slot, int k) -> uint8_t { return W.f[slot][W.foff[slot] + k]; };
+        auto setv = [&](int slot, int f, int k, double x) {
+            W.v[slot][U::slot(f)][W.voff[slot][U::slot(f)] + k] = x;
+        };
+        // identity columns: zero constrained direction entries of a staged row
+        auto mask_row = [&](int slot) {
+            for (int k = lane; k < SW_COLS; k += SW_LANES) {
+                const int64_t gc = gcol0 + k;
+                if (gc < 0 || gc >= np1) continue;
+                const uint8_t f = flag(slot, k);
+                if (U::ux && (f & F_DIR)) {
+                    setv(slot, FX, k, 0.0);
+                    setv(slot, FY, k, 0.0);
+                }
+                if (U::ph && (f & F_ACT)) setv(slot, FP, k, 0.0);
+            }
+        };
+        // the upper cell row reads the upper slit copies of node row i_mid
+        auto patch_slit = [&](int slot) {
+            for (int k = lane; k < SW_COLS; k += SW_LANES) {
+                const int64_t gc = gcol0 + k;
+                if (gc < 0 || gc >= m.i_mid) continue;
+#pragma unroll
+                for (int f = 0; f < NFIELDS; ++f)
+                    if (U::used(f)) setv(slot, f, k, A.fld[f][m.n_grid + gc]);
+                W.f[slot][W.foff[slot] + k] = A.flags[m.n_grid + gc];
+            }
+        };
+        constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
+        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int pc = U::DO_UU ? c : 2;
+                const bool cons = pc < 2 ? (f & F_DIR) : (f & F_ACT);
+                double x = cons ? A.src_out[c][gid] : v[pc];
+                if (FUSED) x = A.rhs[c][gid] - x;
+                A.dst[c][gid] = x;
+            }
+        };
+
+        // ---- prologue: rows of the first window + its q-point block (stage 0 of this item)
+        int stage = 0;
+        if (lane == 0) {
+            unsigned bytes = 0;
+            for (int b = 0; b < 3; ++b) bytes += issue_row(2 * (int64_t)cstart + b, &W.bar[0]);
+            bytes += issue_qblock(cstart, 0);
+            mbar_expect_tx(&W.bar[0], bytes);
+        }
+
+        double carry[3][3] = {};
+        for (int cy = cstart; cy < c1; ++cy) {
+            const int64_t jb = 2 * (int64_t)cy;
+            const bool more = cy + 1 < c1;
+            const int nstage = stage ^ 1;
+            if (more && lane == 0) {
+                fence_proxy_async();
+                unsigned bytes = issue_row(jb + 3, &W.bar[nstage]);
+                bytes += issue_row(jb + 4, &W.bar[nstage]);
+                bytes += issue_qblock(cy + 1, nstage);
+                mbar_expect_tx(&W.bar[nstage], bytes);
+            }
+            mbar_wait(&W.bar[stage], use_count[stage] & 1u);
+            use_count[stage]++;
+            const int s0 = (int)(jb % RING), s1 = (int)((jb + 1) % RING), s2 = (int)((jb + 2) % RING);
+            if (cy == cstart) mask_row(s0);
+            mask_row(s1);
+            mask_row(s2);
+            const bool slit_row = m.level >= 1 && cy == half;
+            if (slit_row) {
+                __syncwarp();
+                patch_slit(s0);
+                __syncwarp();
+                mask_row(s0);
+            }
+            __syncwarp();
+            const int sl[3] = {s0, s1, s2};
+            auto get = [&](int f, int b, int a) -> double { return val(sl[b], f, 2 * lane + a); };
+            const double* qb = W.q[stage];
+            auto qv = [&](int arr, int k) -> double { return qb[arr * QARR + k * SW_LANES + lane]; };
+
+            // ---- cell computation (one cell per lane) -----------------------------
+            double r[3][3][3] = {};   // [comp x, y, phi][b][a]
+#pragma unroll
+            for (int iq = 0; iq < 3; ++iq) {
+                double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3], X0p[3], Xt[3];
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    auto cn = [&](int f) {
+                        return S.N[iq][0] * get(f, b, 0) + S.N[iq][1] * get(f, b, 1) +
+                               S.N[iq][2] * get(f, b, 2);
+                    };
+                    auto cd = [&](int f) {
+                        return S.D[iq][0] * get(f, b, 0) + S.D[iq][1] * get(f, b, 1) +
+                               S.D[iq][2] * get(f, b, 2);
+                    };
+                    if (U::ux) {
+                        XxN[b] = cn(FX); XxD[b] = cd(FX);
+                        XyN[b] = cn(FY); XyD[b] = cd(FY);
+                    }
+                    if (U::ph) { XpN[b] = cn(FP); XpD[b] = cd(FP); }
+                    if (U::p0) X0p[b] = cn(F0P);
+                    if (U::pt) Xt[b] = cn(FPT);
+                }
+                double Tu1[3] = {}, Tu2[3] = {}, Tv1[3] = {}, Tv2[3] = {}, Tp1[3] = {}, Tp2[3] = {};
+#pragma unroll
+                for (int jq = 0; jq < 3; ++jq) {
+                    auto yN = [&](const double (&X)[3]) {
+                        return S.N[jq][0] * X[0] + S.N[jq][1] * X[1] + S.N[jq][2] * X[2];
+                    };
+                    auto yD = [&](const double (&X)[3]) {
+                        return S.D[jq][0] * X[0] + S.D[jq][1] * X[1] + S.D[jq][2] * X[2];
+                    };
+                    const int k = jq * 3 + iq;
+                    const double wq = S.w[jq] * S.w[iq];
+                    const double wg = wq * h, wv = wq * h * h;
+                    double ds11 = 0.0, ds22 = 0.0, ds12 = 0.0, spde = 0.0, pc = 0.0;
+                    if (MIEHE) {
+                        MieheQ q{};
+                        if (U::qstate) q = miehe_q(qv(0, k), qv(1, k), qv(2, k), qv(3, k));
+                        if (U::ux) {
+                            const double d11 = yN(XxD) * inv_h;
+                            const double d22 = yD(XyN) * inv_h;
+                            const double d12 = 0.5 * (yD(XxN) + yN(XyD)) * inv_h;
+                            const double g_t =
+                                U::pt ? (1.0 - M.kappa) * yN(Xt) * yN(Xt) + M.kappa : 1.0;
+                            miehe_dsig(M, g_t, q, d11, d22, d12, ds11, ds22, ds12, spde);
+                        }
+                        if (U::DO_PP)
+                            pc = U::qpc ? qv(0, k)
+                                        : 2.0 * (1.0 - M.kappa) * esplus2(M.lam, M.mu, q.tre, q.e) +
+                                              M.gc / M.eps;
+                    } else {
+                        double e11 = 0.0, e22 = 0.0, e12 = 0.0;
+                        if (U::qstate) { e11 = qv(0, k); e22 = qv(1, k); e12 = qv(2, k); }
+                        if (U::ux) {
+                            const double d11 = yN(XxD) * inv_h;
+                            const double d22 = yD(XyN) * inv_h;
+                            const double d12 = 0.5 * (yD(XxN) + yN(XyD)) * inv_h;
+                            const double g_t =
+                                U::pt ? (1.0 - M.kappa) * yN(Xt) * yN(Xt) + M.kappa : 1.0;
+                            dsig_none(M.lam, M.mu, g_t, e11, e22, e12, d11, d22, d12, ds11, ds22,
+                                      ds12, spde);
+                        }
+                        if (U::DO_PP) {
+                            if (U::qpc) {
+                                pc = qv(0, k);
+                            } else {
+                                const double tre = e11 + e22;
+                                const double esp = 0.5 * M.lam * tre * tre +
+                                                   M.mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
+                                pc = 2.0 * (1.0 - M.kappa) * esp + M.gc / M.eps;
+                            }
+                        }
+                    }
+                    double fv = 0.0, fgx = 0.0, fgy = 0.0;
+                    if (U::DO_PP) {
+                        double pval = pc * yN(XpN);
+                        if (U::DO_COUP) pval += 2.0 * (1.0 - M.kappa) * yN(X0p) * spde;
+                        fv = pval * wv;
+                        fgx = M.gc * M.eps * yN(XpD) * inv_h * wg;
+                        fgy = M.gc * M.eps * yD(XpN) * inv_h * wg;
+                    }
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        const double nb = S.N[jq][b], db = S.D[jq][b];
+                        if (U::DO_UU) {
+                            Tu1[b] = fma(nb, ds11 * wg, Tu1[b]);
+                            Tu2[b] = fma(db, ds12 * wg, Tu2[b]);
+                            Tv1[b] = fma(nb, ds12 * wg, Tv1[b]);
+                            Tv2[b] = fma(db, ds22 * wg, Tv2[b]);
+                        }
+                        if (U::DO_PP) {
+                            Tp1[b] = fma(db, fgy, fma(nb, fv, Tp1[b]));
+                            Tp2[b] = fma(nb, fgx, Tp2[b]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const double na = S.N[iq][a], da = S.D[iq][a];
+                        if (U::DO_UU) {
+                            r[0][b][a] = fma(da, Tu1[b], fma(na, Tu2[b], r[0][b][a]));
+                            r[1][b][a] = fma(da, Tv1[b], fma(na, Tv2[b], r[1][b][a]));
+                        }
+                        if (U::DO_PP) r[2][b][a] = fma(na, Tp1[b], fma(da, Tp2[b], r[2][b][a]));
+                    }
+            }
+            if (!active) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b)
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) r[c][b][a] = 0.0;
+            }
+
+            // ---- node rows 2cy (b=0) and 2cy+1 (b=1) are complete; carry 2cy+2 --------
+            double left[3][3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) left[c][b] = __shfl_up_sync(0xffffffffu, r[c][b][2], 1);
+            const bool own_row = cy >= c0;
+            const bool last_cell = cx == ns - 1;
+            if (own_row && owner) {
+                const int na = last_cell ? 3 : 2;
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const int64_t j = jb + b;
+                    for (int a = 0; a < na; ++a) {
+                        const int64_t gc = 2 * (int64_t)cx + a;
+                        double v[3];
+                        if (b == 0 && slit_row && gc < m.i_mid) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) v[c] = carry[c][a];
+                            store(j * np1 + gc, v, A.flags[j * np1 + gc]);
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) v[c] = r[c][0][a] + (a == 0 ? left[c][0] : 0.0);
+                            store(m.n_grid + gc, v, A.flags[m.n_grid + gc]);
+                            continue;
+                        }
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            v[c] = r[c][b][a] + (a == 0 ? left[c][b] : 0.0) +
+                                   (b == 0 ? carry[c][a] : 0.0);
+                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a));
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) carry[c][a] = r[c][2][a] + (a == 0 ? left[c][2] : 0.0);
+            if (cy == ns - 1 && own_row && owner) {   // top boundary row 2*ns
+                const int64_t j = jb + 2;
+                const int na = last_cell ? 3 : 2;
+                for (int a = 0; a < na; ++a) {
+                    double v[3] = {carry[0][a], carry[1][a], carry[2][a]};
+                    store(j * np1 + 2 * (int64_t)cx + a, v, flag(s2, 2 * lane + a));
+                }
+            }
+            fence_proxy_async();   // our generic smem accesses before the next TMA writes
+            __syncwarp();
+            stage ^= 1;
+        }
+        __syncwarp();
+    }
+}
+
+struct LaunchCfg {
+    bool init = false;
+    int blocks_per_sm = 0;
+};
+
+template <int MODE, bool MIEHE, bool FUSED>
+cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
+    using U = Use<MODE, MIEHE>;
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ>);
+    auto k = k_sweep_q2<MODE, MIEHE, FUSED>;
+    static LaunchCfg cfg;
+    static int n_sm = 0;
+    if (!cfg.init) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.blocks_per_sm, k, SW_LANES, shm);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        if (cfg.blocks_per_sm < 1) cfg.blocks_per_sm = 1;
+        cfg.init = true;
+    }
+    const int ns = a.m.nside;
+    const int slots = cfg.blocks_per_sm * n_sm;
+    int rows = rows_override;
+    if (rows <= 0) {
+        // one full wave: as many chunks per strip as slots allow
+        int chunks = slots / a.n_strips;
+        if (chunks < 1) chunks = 1;
+        if (chunks > ns) chunks = ns;
+        rows = (ns + chunks - 1) / chunks;
+        if (rows < 4) rows = ns < 4 ? ns : 4;
+    }
+    if (rows > ns) rows = ns;
+    a.rows_per_chunk = rows;
+    a.n_items = a.n_strips * ((ns + rows - 1) / rows);
+    const int grid = a.n_items < slots ? a.n_items : slots;
+    k<<<grid, SW_LANES, shm, s>>>(a);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template <bool MIEHE, bool FUSED>
+cudaError_t launch_split(int mode, SweepArgs& a, cudaStream_t s, int rows) {
+    switch (mode) {
+        case MODE_FULL: return launch_mode<MODE_FULL, MIEHE, FUSED>(a, s, rows);
+        case MODE_UU: return launch_mode<MODE_UU, MIEHE, FUSED>(a, s, rows);
+        case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, FUSED>(a, s, rows);
+        case MODE_PHIROW: return launch_mode<MODE_PHIROW, MIEHE, FUSED>(a, s, rows);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int g_rows_override = 0;
+
+}  // namespace
+
+void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
+
+cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
+    const Mesh& m = L.mesh;
+    const int64_t total = (int64_t)L.n_strips() * m.nside * SW_LANES;
+    const unsigned grid = (unsigned)((total + 127) / 128);
+    if (L.miehe)
+        k_refresh_tiled<true><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.qtile(), L.n_strips(),
+                                                   L.tile_block());
+    else
+        k_refresh_tiled<false><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.qtile(), L.n_strips(),
+                                                    L.tile_block());
+    count_launches(1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
                                const double* rhs, cudaStream_t s, bool* handled) {
     *handled = false;
-    return cudaSuccess;
+    if (!L.sweep_ok()) return cudaSuccess;
+    const Mesh& m = L.mesh;
+    const int64_t n = m.n;
+    SweepArgs a;
+    a.m = m;
+    a.S = L.shape;
+    a.M = L.mat;
+    for (int f = 0; f < NFIELDS; ++f) a.fld[f] = nullptr;
+    switch (mode) {
+        case MODE_FULL:
+        case MODE_PHIROW:
+            a.fld[FX] = src; a.fld[FY] = src + n; a.fld[FP] = src + 2 * n; break;
+        case MODE_UU:
+            a.fld[FX] = src; a.fld[FY] = src + n; break;
+        case MODE_PHIPHI:
+            a.fld[FP] = src; break;
+        default: return cudaErrorInvalidValue;
+    }
+    a.fld[F0P] = L.U + 2 * n;
+    a.fld[FPT] = L.phi_tilde;
+    a.flags = L.flags;
+    a.qtile = L.qtile();
+    a.qblock = L.tile_block();
+    for (int c = 0; c < 3; ++c) { a.dst[c] = nullptr; a.src_out[c] = nullptr; a.rhs[c] = nullptr; }
+    if (mode == MODE_FULL || mode == MODE_UU) {
+        const int nc = mode == MODE_FULL ? 3 : 2;
+        for (int c = 0; c < nc; ++c) {
+            a.dst[c] = dst + c * n;
+            a.src_out[c] = src + c * n;
+            a.rhs[c] = rhs ? rhs + c * n : nullptr;
+        }
+    } else {
+        a.dst[0] = dst;
+        a.src_out[0] = mode == MODE_PHIROW ? src + 2 * n : src;
+        a.rhs[0] = rhs;
+    }
+    a.n_strips = L.n_strips();
+    int rows = g_rows_override;
+    if (rows <= 0) {
+        static int env_rows = -1;
+        if (env_rows < 0) {
+            const char* e = getenv("PFF_SWEEP_ROWS");
+            env_rows = e ? atoi(e) : 0;
+        }
+        rows = env_rows;
+    }
+    *handled = true;
+    if (L.miehe)
+        return rhs ? launch_split<true, true>(mode, a, s, rows)
+                   : launch_split<true, false>(mode, a, s, rows);
+    return rhs ? launch_split<false, true>(mode, a, s, rows)
+               : launch_split<false, false>(mode, a, s, rows);
 }
 
 }  // namespace pff

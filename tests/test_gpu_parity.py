@@ -239,3 +239,58 @@ def test_lanczos_and_chebyshev_numpy_callables():
     rhs = np.random.default_rng(0).standard_normal(25)
     z = P.chebyshev_apply(lambda v: v, np.ones(25), rhs, 1.0, 1.2, 32)
     assert np.linalg.norm(z - rhs) <= 1e-13 * np.linalg.norm(rhs)
+
+
+@pytest.fixture
+def generic_apply():
+    from paper_2005_00331_b200 import _lib
+    def run(flag):
+        _lib.set_option(_lib.OPT_GENERIC_APPLY, int(flag))
+    yield run
+    _lib.set_option(_lib.OPT_GENERIC_APPLY, 0)
+    _lib.set_option(_lib.OPT_SWEEP_ROWS, 0)
+
+
+@pytest.mark.parametrize("split", ["none", "miehe"])
+@pytest.mark.parametrize("level,rows", [(1, 0), (5, 3), (6, 1), (6, 31), (7, 5), (7, 64),
+                                        (8, 64), (8, 7), (9, 0), (9, 256)])
+def test_sweep_matches_generic_all_modes(generic_apply, split, level, rows):
+    """The write-once Q2 kernel against the per-cell atomic kernel, every mode,
+    plain and fused, over chunkings that put chunk edges on and off the slit."""
+    from paper_2005_00331_b200 import _lib
+    ost, x = O.baseline_state(2, level, split, seed=level)
+    h = P.build_hierarchy(max(level, 2), 2)
+    st = P.LinearizationState(h, level, ost.params, split=split)
+    st.set_solution(ost.U)
+    st.set_phi_tilde(ost.phi_tilde)
+    st.set_phi_old(ost.phi_old)
+    act = ost.active.copy()
+    act[np.random.default_rng(level).choice(st.n_scalar, 7, replace=False)] = True
+    dn = ost.dirichlet.copy()
+    dn[h.dof_map(level).slit_upper[:2]] = True
+    st.set_active(act)
+    st.set_dirichlet_nodes(np.flatnonzero(dn))
+    st.refresh_cache()
+    n = st.n_scalar
+    xd = torch.from_numpy(x).cuda()
+    rhs = torch.from_numpy(np.random.default_rng(1).standard_normal(3 * n)).cuda()
+    _lib.set_option(_lib.OPT_SWEEP_ROWS, rows)
+    cases = [(0, xd, 3 * n), (1, xd[:2 * n], 2 * n), (2, xd[2 * n:], n), (3, xd, n)]
+    for mode, src, nout in cases:
+        outs = []
+        for flag in (1, 0):
+            generic_apply(flag)
+            y = torch.empty(nout, dtype=torch.float64, device="cuda")
+            st.apply_into(mode, src, y)
+            yf = torch.empty(nout, dtype=torch.float64, device="cuda")
+            st.apply_into(mode, src, yf, rhs[:nout])
+            outs.append((y.cpu().numpy(), yf.cpu().numpy()))
+        (g, gf), (s, sf) = outs
+        k = nout // n
+        assert max(block_rel(s, g, n)) <= 1e-13, (mode, block_rel(s, g, n))
+        assert max(block_rel(sf, gf, n)) <= 1e-13, mode
+    generic_apply(0)
+    if level >= 6:   # the write-once sweep kernel runs from 64x64 cells up: deterministic
+        y1 = P.apply_jacobian(st, xd)
+        y2 = P.apply_jacobian(st, xd)
+        assert torch.equal(y1, y2)
