@@ -390,13 +390,20 @@ k_sweep_q2(const SweepArgs A) {
             }
             __syncwarp();
             const int sl[3] = {s0, s1, s2};
-            auto get = [&](int f, int b, int a) -> double { return val(sl[b], f, 2 * lane + a); };
+            const double* rowp[3][NF];   // this lane's staged column 2*lane, per row and field
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int q = 0; q < NF; ++q) rowp[b][q] = &W.v[sl[b]][q][W.voff[sl[b]][q] + 2 * lane];
+            auto get = [&](int f, int b, int a) -> double { return rowp[b][U::slot(f)][a]; };
             const double* qb = W.q[stage];
             auto qv = [&](int arr, int k) -> double { return qb[arr * QARR + k * SW_LANES + lane]; };
 
             // ---- cell computation (one cell per lane) -----------------------------
             double r[3][3][3] = {};   // [comp x, y, phi][b][a]
-#pragma unroll
+            // rolled over quadrature columns (code size: keeps the body in the
+            // instruction cache); the three q-points of a column are unrolled for ILP
+#pragma unroll 1
             for (int iq = 0; iq < 3; ++iq) {
                 double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3], X0p[3], Xt[3];
 #pragma unroll
