@@ -65,9 +65,10 @@ struct Use {
     static constexpr int NF = slot(NFIELDS);
 };
 
-template <int NF, int NQ>
+template <int NF, int NQ, int NRHS>
 struct __align__(16) WarpSmem {
     double q[2][NQ > 0 ? NQ * QARR : 2];     // q-point blocks, two stages
+    double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];   // fused rhs of this lane's output nodes
     double v[RING][NF][RW];                  // node-row ring
     uint8_t f[RING][FW];                     // flag rows
     int voff[RING][NF];                      // element offset of staged column 0
@@ -117,6 +118,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // Miehe tangent with the state eigensystem given as (m, +-r, c, s):
@@ -247,7 +256,8 @@ __global__ void __launch_bounds__(SW_LANES)
 k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
-    using Smem = WarpSmem<NF, NQ>;
+    constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
+    using Smem = WarpSmem<NF, NQ, FUSED ? NC : 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -318,19 +328,6 @@ k_sweep_q2(const SweepArgs A) {
         auto setv = [&](int slot, int f, int k, double x) {
             W.v[slot][U::slot(f)][W.voff[slot][U::slot(f)] + k] = x;
         };
-        // identity columns: zero constrained direction entries of a staged row
-        auto mask_row = [&](int slot) {
-            for (int k = lane; k < SW_COLS; k += SW_LANES) {
-                const int64_t gc = gcol0 + k;
-                if (gc < 0 || gc >= np1) continue;
-                const uint8_t f = flag(slot, k);
-                if (U::ux && (f & F_DIR)) {
-                    setv(slot, FX, k, 0.0);
-                    setv(slot, FY, k, 0.0);
-                }
-                if (U::ph && (f & F_ACT)) setv(slot, FP, k, 0.0);
-            }
-        };
         // the upper cell row reads the upper slit copies of node row i_mid
         auto patch_slit = [&](int slot) {
             for (int k = lane; k < SW_COLS; k += SW_LANES) {
@@ -342,14 +339,18 @@ k_sweep_q2(const SweepArgs A) {
                 W.f[slot][W.foff[slot] + k] = A.flags[m.n_grid + gc];
             }
         };
-        constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f) {
+        // stores: identity rows take the raw staged src value (slot/column) or,
+        // on the rare paths (slot < 0), a global load; the fused rhs comes from
+        // the per-lane cp.async buffer (rbi >= 0) or a global load
+        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int slot, int k, int rbi) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const int pc = U::DO_UU ? c : 2;
                 const bool cons = pc < 2 ? (f & F_DIR) : (f & F_ACT);
-                double x = cons ? A.src_out[c][gid] : v[pc];
-                if (FUSED) x = A.rhs[c][gid] - x;
+                double x = v[pc];
+                if (cons) x = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k)
+                                        : A.src_out[c][gid];
+                if (FUSED) x = (rbi >= 0 ? W.rb[rbi][c][lane] : A.rhs[c][gid]) - x;
                 A.dst[c][gid] = x;
             }
         };
@@ -375,18 +376,26 @@ k_sweep_q2(const SweepArgs A) {
                 bytes += issue_qblock(cy + 1, nstage);
                 mbar_expect_tx(&W.bar[nstage], bytes);
             }
+            const bool own_row = cy >= c0;
+            const bool last_cell = cx == ns - 1;
+            const int na_out = last_cell ? 3 : 2;
+            if (FUSED && own_row && owner) {   // prefetch rhs of this lane's output nodes
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+                    for (int a = 0; a < na_out; ++a)
+#pragma unroll
+                        for (int c = 0; c < NC; ++c)
+                            cp_async8(&W.rb[b * 3 + a][c][lane],
+                                      A.rhs[c] + (jb + b) * np1 + 2 * (int64_t)cx + a);
+            }
+            cp_async_commit();
             mbar_wait(&W.bar[stage], use_count[stage] & 1u);
             use_count[stage]++;
             const int s0 = (int)(jb % RING), s1 = (int)((jb + 1) % RING), s2 = (int)((jb + 2) % RING);
-            if (cy == cstart) mask_row(s0);
-            mask_row(s1);
-            mask_row(s2);
             const bool slit_row = m.level >= 1 && cy == half;
             if (slit_row) {
                 __syncwarp();
                 patch_slit(s0);
-                __syncwarp();
-                mask_row(s0);
             }
             __syncwarp();
             const int sl[3] = {s0, s1, s2};
@@ -395,7 +404,24 @@ k_sweep_q2(const SweepArgs A) {
             for (int b = 0; b < 3; ++b)
 #pragma unroll
                 for (int q = 0; q < NF; ++q) rowp[b][q] = &W.v[sl[b]][q][W.voff[sl[b]][q] + 2 * lane];
-            auto get = [&](int f, int b, int a) -> double { return rowp[b][U::slot(f)][a]; };
+            // identity columns (src/pff_operator.py:267): constrained direction
+            // entries read as zero; the staged rows keep the raw values
+            unsigned mdir = 0u, mact = 0u;
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const uint8_t fl = flag(sl[b], 2 * lane + a);
+                    mdir |= (fl & F_DIR) ? 1u << (3 * b + a) : 0u;
+                    mact |= (fl & F_ACT) ? 1u << (3 * b + a) : 0u;
+                }
+            auto get = [&](int f, int b, int a) -> double {
+                const double x = rowp[b][U::slot(f)][a];
+                const unsigned bit = 1u << (3 * b + a);
+                if (f == FX || f == FY) return (mdir & bit) ? 0.0 : x;
+                if (f == FP) return (mact & bit) ? 0.0 : x;
+                return x;
+            };
             const double* qb = W.q[stage];
             auto qv = [&](int arr, int k) -> double { return qb[arr * QARR + k * SW_LANES + lane]; };
 
@@ -525,10 +551,9 @@ k_sweep_q2(const SweepArgs A) {
             for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int b = 0; b < 3; ++b) left[c][b] = __shfl_up_sync(0xffffffffu, r[c][b][2], 1);
-            const bool own_row = cy >= c0;
-            const bool last_cell = cx == ns - 1;
+            if (FUSED) cp_async_wait_all();
             if (own_row && owner) {
-                const int na = last_cell ? 3 : 2;
+                const int na = na_out;
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                     const int64_t j = jb + b;
@@ -538,17 +563,17 @@ k_sweep_q2(const SweepArgs A) {
                         if (b == 0 && slit_row && gc < m.i_mid) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = carry[c][a];
-                            store(j * np1 + gc, v, A.flags[j * np1 + gc]);
+                            store(j * np1 + gc, v, A.flags[j * np1 + gc], -1, 0, -1);
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = r[c][0][a] + (a == 0 ? left[c][0] : 0.0);
-                            store(m.n_grid + gc, v, A.flags[m.n_grid + gc]);
+                            store(m.n_grid + gc, v, A.flags[m.n_grid + gc], s0, 2 * lane + a, -1);
                             continue;
                         }
 #pragma unroll
                         for (int c = 0; c < 3; ++c)
                             v[c] = r[c][b][a] + (a == 0 ? left[c][b] : 0.0) +
                                    (b == 0 ? carry[c][a] : 0.0);
-                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a));
+                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a), sl[b], 2 * lane + a, b * 3 + a);
                     }
                 }
             }
@@ -558,10 +583,10 @@ k_sweep_q2(const SweepArgs A) {
                 for (int a = 0; a < 3; ++a) carry[c][a] = r[c][2][a] + (a == 0 ? left[c][2] : 0.0);
             if (cy == ns - 1 && own_row && owner) {   // top boundary row 2*ns
                 const int64_t j = jb + 2;
-                const int na = last_cell ? 3 : 2;
-                for (int a = 0; a < na; ++a) {
+                for (int a = 0; a < na_out; ++a) {
                     double v[3] = {carry[0][a], carry[1][a], carry[2][a]};
-                    store(j * np1 + 2 * (int64_t)cx + a, v, flag(s2, 2 * lane + a));
+                    store(j * np1 + 2 * (int64_t)cx + a, v, flag(s2, 2 * lane + a), s2,
+                          2 * lane + a, -1);
                 }
             }
             fence_proxy_async();   // our generic smem accesses before the next TMA writes
@@ -580,7 +605,8 @@ struct LaunchCfg {
 template <int MODE, bool MIEHE, bool FUSED>
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ>);
+    constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? NC : 0>);
     auto k = k_sweep_q2<MODE, MIEHE, FUSED>;
     static LaunchCfg cfg;
     static int n_sm = 0;
