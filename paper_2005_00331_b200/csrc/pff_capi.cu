@@ -75,6 +75,13 @@ int pff_level_create(pff_level** out, int degree, int level, int split, const pf
             for (int k = 0; k < n1; ++k)
                 for (int m = 0; m < n1; ++m) L->embed.E[c][k][m] = embed[(c * n1 + k) * n1 + m];
     L->mat = pff::Material{mat->lame_lambda, mat->mu, mat->g_c, mat->kappa, mat->eps};
+    if (degree == 2) {
+        const auto& S = L->shape;
+        auto near = [](double a, double b, double tol) { return a - b <= tol && b - a <= tol; };
+        L->q2_struct = near(S.N[1][0], 0.0, 1e-14) && near(S.N[1][1], 1.0, 1e-14) &&
+                       near(S.N[1][2], 0.0, 1e-14) && near(S.D[1][0], -1.0, 1e-13) &&
+                       near(S.D[1][1], 0.0, 1e-13) && near(S.D[1][2], 1.0, 1e-13);
+    }
     L->miehe = split;
     *out = reinterpret_cast<pff_level*>(L);
     return 0;

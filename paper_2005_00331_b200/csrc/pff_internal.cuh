@@ -24,7 +24,8 @@ struct Level {
     int64_t generic_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells(); }
     // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
     // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
-    bool sweep_ok() const { return mesh.p == 2 && mesh.nside >= 64; }
+    bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
+    bool sweep_ok() const { return mesh.p == 2 && mesh.nside >= 64 && q2_struct; }
     int n_strips() const { return (mesh.nside + 30) / 31; }
     int tile_nq() const { return miehe ? 5 : 4; }
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }

@@ -76,7 +76,18 @@ struct __align__(16) WarpSmem {
     unsigned long long bar[2];
 };
 
+// Q2 constants of one application, prepared on the host (exact rescalings)
+struct SweepConst {
+    double N[3][3];    // shape values at the Gauss points (row 1 is (0,1,0))
+    double Dh[3][3];   // shape derivatives / h (row 1 is (-1,0,1)/h)
+    double ih;         // 1/h
+    double wv[9];      // w_jq w_iq h^2 (src/_kernels.py:613-615 order)
+    double cgw[9];     // gc eps wv
+    double lam, mu2, gdd, omk, kappa, gce;
+};
+
 struct SweepArgs {
+    SweepConst K;
     Mesh m;
     Shape S;
     Material M;
@@ -425,116 +436,170 @@ k_sweep_q2(const SweepArgs A) {
             const double* qb = W.q[stage];
             auto qv = [&](int arr, int k) -> double { return qb[arr * QARR + k * SW_LANES + lane]; };
 
-            // ---- cell computation (one cell per lane) -----------------------------
+            // ---- cell computation (one cell per lane), Q2-specialised -----------------
+            // Middle Gauss point: N[1] = (0,1,0), D[1] = (-1,0,1) (checked on the host);
+            // Dh = D/h and the weights wv = w_jq w_iq h^2 make every gradient physical
+            // (h = 2^-l, so the rescalings are exact).  Fully unrolled: all shape
+            // coefficients are constant-bank operands.
+            const SweepConst& K = A.K;
             double r[3][3][3] = {};   // [comp x, y, phi][b][a]
-            // rolled over quadrature columns (code size: keeps the body in the
-            // instruction cache); the three q-points of a column are unrolled for ILP
-#pragma unroll 1
+#pragma unroll
             for (int iq = 0; iq < 3; ++iq) {
+                auto xN = [&](int f, int b) -> double {
+                    if (iq == 1) return get(f, b, 1);
+                    return fma(K.N[iq][2], get(f, b, 2),
+                               fma(K.N[iq][1], get(f, b, 1), K.N[iq][0] * get(f, b, 0)));
+                };
+                auto xD = [&](int f, int b) -> double {
+                    if (iq == 1) return K.ih * (get(f, b, 2) - get(f, b, 0));
+                    return fma(K.Dh[iq][2], get(f, b, 2),
+                               fma(K.Dh[iq][1], get(f, b, 1), K.Dh[iq][0] * get(f, b, 0)));
+                };
                 double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3], X0p[3], Xt[3];
 #pragma unroll
                 for (int b = 0; b < 3; ++b) {
-                    auto cn = [&](int f) {
-                        return S.N[iq][0] * get(f, b, 0) + S.N[iq][1] * get(f, b, 1) +
-                               S.N[iq][2] * get(f, b, 2);
-                    };
-                    auto cd = [&](int f) {
-                        return S.D[iq][0] * get(f, b, 0) + S.D[iq][1] * get(f, b, 1) +
-                               S.D[iq][2] * get(f, b, 2);
-                    };
                     if (U::ux) {
-                        XxN[b] = cn(FX); XxD[b] = cd(FX);
-                        XyN[b] = cn(FY); XyD[b] = cd(FY);
+                        XxN[b] = xN(FX, b); XxD[b] = xD(FX, b);
+                        XyN[b] = xN(FY, b); XyD[b] = xD(FY, b);
                     }
-                    if (U::ph) { XpN[b] = cn(FP); XpD[b] = cd(FP); }
-                    if (U::p0) X0p[b] = cn(F0P);
-                    if (U::pt) Xt[b] = cn(FPT);
+                    if (U::ph) { XpN[b] = xN(FP, b); XpD[b] = xD(FP, b); }
+                    if (U::p0) X0p[b] = xN(F0P, b);
+                    if (U::pt) Xt[b] = xN(FPT, b);
                 }
                 double Tu1[3] = {}, Tu2[3] = {}, Tv1[3] = {}, Tv2[3] = {}, Tp1[3] = {}, Tp2[3] = {};
 #pragma unroll
                 for (int jq = 0; jq < 3; ++jq) {
-                    auto yN = [&](const double (&X)[3]) {
-                        return S.N[jq][0] * X[0] + S.N[jq][1] * X[1] + S.N[jq][2] * X[2];
+                    auto yN = [&](const double (&X)[3]) -> double {
+                        if (jq == 1) return X[1];
+                        return fma(K.N[jq][2], X[2], fma(K.N[jq][1], X[1], K.N[jq][0] * X[0]));
                     };
-                    auto yD = [&](const double (&X)[3]) {
-                        return S.D[jq][0] * X[0] + S.D[jq][1] * X[1] + S.D[jq][2] * X[2];
+                    auto yD = [&](const double (&X)[3]) -> double {
+                        if (jq == 1) return K.ih * (X[2] - X[0]);
+                        return fma(K.Dh[jq][2], X[2], fma(K.Dh[jq][1], X[1], K.Dh[jq][0] * X[0]));
                     };
                     const int k = jq * 3 + iq;
-                    const double wq = S.w[jq] * S.w[iq];
-                    const double wg = wq * h, wv = wq * h * h;
-                    double ds11 = 0.0, ds22 = 0.0, ds12 = 0.0, spde = 0.0, pc = 0.0;
+                    const double wv = K.wv[k];
+                    double s11 = 0.0, s22 = 0.0, s12 = 0.0, spde = 0.0, pc = 0.0;
                     if (MIEHE) {
                         MieheQ q{};
                         if (U::qstate) q = miehe_q(qv(0, k), qv(1, k), qv(2, k), qv(3, k));
                         if (U::ux) {
-                            const double d11 = yN(XxD) * inv_h;
-                            const double d22 = yD(XyN) * inv_h;
-                            const double d12 = 0.5 * (yD(XxN) + yN(XyD)) * inv_h;
-                            const double g_t =
-                                U::pt ? (1.0 - M.kappa) * yN(Xt) * yN(Xt) + M.kappa : 1.0;
+                            const double d11 = yN(XxD);
+                            const double d22 = yD(XyN);
+                            const double d12 = 0.5 * (yD(XxN) + yN(XyD));
+                            double g_t = 1.0;
+                            if (U::pt) {
+                                const double pt = yN(Xt);
+                                g_t = fma(K.omk * pt, pt, K.kappa);
+                            }
+                            double ds11, ds22, ds12;
                             miehe_dsig(M, g_t, q, d11, d22, d12, ds11, ds22, ds12, spde);
+                            s11 = ds11 * wv;
+                            s22 = ds22 * wv;
+                            s12 = ds12 * wv;
                         }
                         if (U::DO_PP)
                             pc = U::qpc ? qv(0, k)
-                                        : 2.0 * (1.0 - M.kappa) * esplus2(M.lam, M.mu, q.tre, q.e) +
-                                              M.gc / M.eps;
+                                        : fma(K.gdd, esplus2(M.lam, M.mu, q.tre, q.e), K.gce);
                     } else {
                         double e11 = 0.0, e22 = 0.0, e12 = 0.0;
                         if (U::qstate) { e11 = qv(0, k); e22 = qv(1, k); e12 = qv(2, k); }
                         if (U::ux) {
-                            const double d11 = yN(XxD) * inv_h;
-                            const double d22 = yD(XyN) * inv_h;
-                            const double d12 = 0.5 * (yD(XxN) + yN(XyD)) * inv_h;
-                            const double g_t =
-                                U::pt ? (1.0 - M.kappa) * yN(Xt) * yN(Xt) + M.kappa : 1.0;
-                            dsig_none(M.lam, M.mu, g_t, e11, e22, e12, d11, d22, d12, ds11, ds22,
-                                      ds12, spde);
+                            const double d11 = yN(XxD);
+                            const double d22 = yD(XyN);
+                            const double d12 = 0.5 * (yD(XxN) + yN(XyD));
+                            double gw = wv;
+                            if (U::pt) {
+                                const double pt = yN(Xt);
+                                gw = fma(K.omk * pt, pt, K.kappa) * wv;
+                            }
+                            const double lt = K.lam * (d11 + d22);
+                            s11 = gw * fma(K.mu2, d11, lt);
+                            s22 = gw * fma(K.mu2, d22, lt);
+                            s12 = (gw * K.mu2) * d12;
+                            if (U::DO_COUP) {
+                                const double ltr = K.lam * (e11 + e22);
+                                spde = fma(fma(K.mu2, e11, ltr), d11,
+                                           fma(fma(K.mu2, e22, ltr), d22, (2.0 * K.mu2 * e12) * d12));
+                            }
                         }
                         if (U::DO_PP) {
                             if (U::qpc) {
                                 pc = qv(0, k);
                             } else {
                                 const double tre = e11 + e22;
-                                const double esp = 0.5 * M.lam * tre * tre +
-                                                   M.mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
-                                pc = 2.0 * (1.0 - M.kappa) * esp + M.gc / M.eps;
+                                const double esp = fma(0.5 * M.lam * tre, tre,
+                                                       M.mu * fma(e11, e11, fma(e22, e22, 2.0 * e12 * e12)));
+                                pc = fma(K.gdd, esp, K.gce);
                             }
                         }
                     }
                     double fv = 0.0, fgx = 0.0, fgy = 0.0;
                     if (U::DO_PP) {
                         double pval = pc * yN(XpN);
-                        if (U::DO_COUP) pval += 2.0 * (1.0 - M.kappa) * yN(X0p) * spde;
+                        if (U::DO_COUP) pval = fma(K.gdd * yN(X0p), spde, pval);
                         fv = pval * wv;
-                        fgx = M.gc * M.eps * yN(XpD) * inv_h * wg;
-                        fgy = M.gc * M.eps * yD(XpN) * inv_h * wg;
+                        fgx = K.cgw[k] * yN(XpD);
+                        fgy = K.cgw[k] * yD(XpN);
                     }
-#pragma unroll
-                    for (int b = 0; b < 3; ++b) {
-                        const double nb = S.N[jq][b], db = S.D[jq][b];
+                    // backward y-pass: T[b] += M[jq][b] f
+                    if (jq == 1) {
                         if (U::DO_UU) {
-                            Tu1[b] = fma(nb, ds11 * wg, Tu1[b]);
-                            Tu2[b] = fma(db, ds12 * wg, Tu2[b]);
-                            Tv1[b] = fma(nb, ds12 * wg, Tv1[b]);
-                            Tv2[b] = fma(db, ds22 * wg, Tv2[b]);
+                            Tu1[1] += s11;
+                            Tv1[1] += s12;
+                            const double t12 = K.ih * s12, t22 = K.ih * s22;
+                            Tu2[0] -= t12; Tu2[2] += t12;
+                            Tv2[0] -= t22; Tv2[2] += t22;
                         }
                         if (U::DO_PP) {
-                            Tp1[b] = fma(db, fgy, fma(nb, fv, Tp1[b]));
-                            Tp2[b] = fma(nb, fgx, Tp2[b]);
+                            const double ty = K.ih * fgy;
+                            Tp1[0] -= ty;
+                            Tp1[1] += fv;
+                            Tp1[2] += ty;
+                            Tp2[1] += fgx;
+                        }
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < 3; ++b) {
+                            const double nb = K.N[jq][b], db = K.Dh[jq][b];
+                            if (U::DO_UU) {
+                                Tu1[b] = fma(nb, s11, Tu1[b]);
+                                Tu2[b] = fma(db, s12, Tu2[b]);
+                                Tv1[b] = fma(nb, s12, Tv1[b]);
+                                Tv2[b] = fma(db, s22, Tv2[b]);
+                            }
+                            if (U::DO_PP) {
+                                Tp1[b] = fma(db, fgy, fma(nb, fv, Tp1[b]));
+                                Tp2[b] = fma(nb, fgx, Tp2[b]);
+                            }
                         }
                     }
                 }
+                // backward x-pass: r[b][a] += Dh[iq][a] T1[b] + N[iq][a] T2[b]
 #pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        const double na = S.N[iq][a], da = S.D[iq][a];
+                for (int b = 0; b < 3; ++b) {
+                    if (iq == 1) {
                         if (U::DO_UU) {
-                            r[0][b][a] = fma(da, Tu1[b], fma(na, Tu2[b], r[0][b][a]));
-                            r[1][b][a] = fma(da, Tv1[b], fma(na, Tv2[b], r[1][b][a]));
+                            const double tu = K.ih * Tu1[b], tv = K.ih * Tv1[b];
+                            r[0][b][0] -= tu; r[0][b][1] += Tu2[b]; r[0][b][2] += tu;
+                            r[1][b][0] -= tv; r[1][b][1] += Tv2[b]; r[1][b][2] += tv;
                         }
-                        if (U::DO_PP) r[2][b][a] = fma(na, Tp1[b], fma(da, Tp2[b], r[2][b][a]));
+                        if (U::DO_PP) {
+                            const double tp = K.ih * Tp2[b];
+                            r[2][b][0] -= tp; r[2][b][1] += Tp1[b]; r[2][b][2] += tp;
+                        }
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const double na = K.N[iq][a], da = K.Dh[iq][a];
+                            if (U::DO_UU) {
+                                r[0][b][a] = fma(da, Tu1[b], fma(na, Tu2[b], r[0][b][a]));
+                                r[1][b][a] = fma(da, Tv1[b], fma(na, Tv2[b], r[1][b][a]));
+                            }
+                            if (U::DO_PP) r[2][b][a] = fma(na, Tp1[b], fma(da, Tp2[b], r[2][b][a]));
+                        }
                     }
+                }
             }
             if (!active) {
 #pragma unroll
@@ -682,6 +747,28 @@ cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, doub
     a.m = m;
     a.S = L.shape;
     a.M = L.mat;
+    {
+        SweepConst& K = a.K;
+        const double h = m.h, ih = 1.0 / h;
+        for (int q = 0; q < 3; ++q)
+            for (int b = 0; b < 3; ++b) {
+                K.N[q][b] = L.shape.N[q][b];
+                K.Dh[q][b] = L.shape.D[q][b] * ih;
+            }
+        K.ih = ih;
+        for (int jq = 0; jq < 3; ++jq)
+            for (int iq = 0; iq < 3; ++iq) {
+                const double wq = L.shape.w[jq] * L.shape.w[iq];
+                K.wv[jq * 3 + iq] = wq * h * h;
+                K.cgw[jq * 3 + iq] = L.mat.gc * L.mat.eps * K.wv[jq * 3 + iq];
+            }
+        K.lam = L.mat.lam;
+        K.mu2 = 2.0 * L.mat.mu;
+        K.gdd = 2.0 * (1.0 - L.mat.kappa);
+        K.omk = 1.0 - L.mat.kappa;
+        K.kappa = L.mat.kappa;
+        K.gce = L.mat.gc / L.mat.eps;
+    }
     for (int f = 0; f < NFIELDS; ++f) a.fld[f] = nullptr;
     switch (mode) {
         case MODE_FULL:
