@@ -191,6 +191,76 @@ __device__ __forceinline__ void miehe_dsig(const Material& M, double g, const Mi
     s12 = g * dp12 + (f12 - dp12);
 }
 
+// Op-minimal form of the same tangent for the sweep kernel (identical maths,
+// rounding differs by a few ulps): the direction-independent part is computed
+// once per q-point, dl2 = tr(de) - dl1 (trace invariance), s = f + (g-1) dp,
+// and sigma+ : de = lambda tr+ tr(de) + 2 mu (l1+ dl1 + l2+ dl2) in the eigenframe.
+struct MieheS {
+    double l1p, l2p, trp, K, c, s, cc, ss, cs, cs2, cms;
+    bool h1, h2, ht;
+};
+__device__ __forceinline__ MieheS miehe_state(double m, double rs, double c, double s) {
+    MieheS q;
+    const double r = fabs(rs);
+    const double ev1 = m + r, ev2 = m - r, tre = 2.0 * m;
+    q.h1 = ev1 >= 0.0;
+    q.h2 = ev2 >= 0.0;
+    q.ht = !(tre < 0.0);
+    q.l1p = posp(ev1);
+    q.l2p = posp(ev2);
+    q.trp = posp(tre);
+    // K = (l1+ - l2+) / gap when the gap test passes: exactly 1 if both eigenvalues
+    // are positive, 0 if none is, a true division only in the mixed case (a zero
+    // numerator would take the slow path of the fp64 division)
+    const bool gap_ok = rs > 0.0;
+    const bool mixed = ev1 > 0.0 && !(ev2 > 0.0);
+    // branch-free reciprocal of the gap: fp32 seed + 3 Newton steps (2^-23 -> 2^-92);
+    // the gap test guarantees gap > 1e-12, well inside the fp32 range
+    const double gap = gap_ok ? ev1 - ev2 : 1.0;
+    double y = (double)__frcp_rn((float)gap);
+    y = y * fma(-gap, y, 2.0);
+    y = y * fma(-gap, y, 2.0);
+    y = y * fma(-gap, y, 2.0);
+    q.K = !gap_ok ? 0.0 : (ev2 > 0.0 ? 1.0 : (mixed ? ev1 * y : 0.0));
+    q.c = c;
+    q.s = s;
+    q.cc = c * c;
+    q.ss = s * s;
+    q.cs = c * s;
+    q.cs2 = 2.0 * q.cs;
+    q.cms = q.cc - q.ss;
+    return q;
+}
+// weighted (x wv) stress increment and sigma+ : de; gm1w = (g - 1) wv
+__device__ __forceinline__ void miehe_apply(double lam, double mu2, const MieheS& q, double gm1w,
+                                            double wv, double d11, double d22, double d12,
+                                            double& s11w, double& s22w, double& s12w,
+                                            double& spde) {
+    const double t0 = fma(d12, q.s, d11 * q.c);
+    const double t1 = fma(d22, q.s, d12 * q.c);
+    const double dl1 = fma(q.s, t1, q.c * t0);
+    const double trde = d11 + d22;
+    const double dl2 = trde - dl1;
+    const double rot = fma(q.c, t1, -(q.s * t0)) * q.K;
+    const double dl1p = q.h1 ? dl1 : 0.0;
+    const double dl2p = q.h2 ? dl2 : 0.0;
+    const double rc = rot * q.cs2;
+    const double o11 = fma(dl1p, q.cc, fma(dl2p, q.ss, -rc));
+    const double o22 = fma(dl1p, q.ss, fma(dl2p, q.cc, rc));
+    const double o12 = fma(dl1p - dl2p, q.cs, rot * q.cms);
+    const double lt = lam * trde;
+    const double ltt = q.ht ? lt : 0.0;
+    s11w = fma(gm1w, fma(mu2, o11, ltt), wv * fma(mu2, d11, lt));
+    s22w = fma(gm1w, fma(mu2, o22, ltt), wv * fma(mu2, d22, lt));
+    s12w = mu2 * fma(gm1w, o12, wv * d12);
+    spde = fma(lam * q.trp, trde, mu2 * fma(q.l1p, dl1, q.l2p * dl2));
+}
+__device__ __forceinline__ double miehe_pc(double lam, double mu, double gdd, double gce,
+                                           const MieheS& q) {
+    const double esp = fma(0.5 * lam * q.trp, q.trp, mu * fma(q.l1p, q.l1p, q.l2p * q.l2p));
+    return fma(gdd, esp, gce);
+}
+
 // ------------------------------------------------------------- tiled refresh
 template <bool MIEHE>
 __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __restrict__ U,
@@ -481,26 +551,22 @@ k_sweep_q2(const SweepArgs A) {
                     const double wv = K.wv[k];
                     double s11 = 0.0, s22 = 0.0, s12 = 0.0, spde = 0.0, pc = 0.0;
                     if (MIEHE) {
-                        MieheQ q{};
-                        if (U::qstate) q = miehe_q(qv(0, k), qv(1, k), qv(2, k), qv(3, k));
+                        MieheS q{};
+                        if (U::qstate) q = miehe_state(qv(0, k), qv(1, k), qv(2, k), qv(3, k));
                         if (U::ux) {
                             const double d11 = yN(XxD);
                             const double d22 = yD(XyN);
                             const double d12 = 0.5 * (yD(XxN) + yN(XyD));
-                            double g_t = 1.0;
+                            double gm1w = -wv;   // (g - 1) wv with g = 1 when unused
                             if (U::pt) {
                                 const double pt = yN(Xt);
-                                g_t = fma(K.omk * pt, pt, K.kappa);
+                                gm1w = (fma(K.omk * pt, pt, K.kappa) - 1.0) * wv;
                             }
-                            double ds11, ds22, ds12;
-                            miehe_dsig(M, g_t, q, d11, d22, d12, ds11, ds22, ds12, spde);
-                            s11 = ds11 * wv;
-                            s22 = ds22 * wv;
-                            s12 = ds12 * wv;
+                            miehe_apply(K.lam, K.mu2, q, gm1w, wv, d11, d22, d12, s11, s22, s12,
+                                        spde);
                         }
                         if (U::DO_PP)
-                            pc = U::qpc ? qv(0, k)
-                                        : fma(K.gdd, esplus2(M.lam, M.mu, q.tre, q.e), K.gce);
+                            pc = U::qpc ? qv(0, k) : miehe_pc(M.lam, M.mu, K.gdd, K.gce, q);
                     } else {
                         double e11 = 0.0, e22 = 0.0, e12 = 0.0;
                         if (U::qstate) { e11 = qv(0, k); e22 = qv(1, k); e12 = qv(2, k); }
