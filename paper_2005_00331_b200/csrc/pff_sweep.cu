@@ -436,26 +436,27 @@ k_sweep_q2(const SweepArgs A) {
             }
         };
 
-        // ---- prologue: rows of the first window + its q-point block (stage 0 of this item)
-        int stage = 0;
-        if (lane == 0) {
-            unsigned bytes = 0;
-            for (int b = 0; b < 3; ++b) bytes += issue_row(2 * (int64_t)cstart + b, &W.bar[0]);
-            bytes += issue_qblock(cstart, 0);
-            mbar_expect_tx(&W.bar[0], bytes);
-        }
-
+        // iteration cy issues the TMA stage of cy+1; the virtual iteration
+        // cy = cstart-1 issues the first window (3 rows) -- one staging call site
+        int stage = 1;
         double carry[3][3] = {};
-        for (int cy = cstart; cy < c1; ++cy) {
+        for (int cy = cstart - 1; cy < c1; ++cy) {
             const int64_t jb = 2 * (int64_t)cy;
             const bool more = cy + 1 < c1;
             const int nstage = stage ^ 1;
             if (more && lane == 0) {
                 fence_proxy_async();
-                unsigned bytes = issue_row(jb + 3, &W.bar[nstage]);
-                bytes += issue_row(jb + 4, &W.bar[nstage]);
+                const bool first = cy < cstart;
+                const int64_t j0 = first ? jb + 2 : jb + 3;
+                unsigned bytes = 0;
+#pragma unroll 1
+                for (int t = 0; t < (first ? 3 : 2); ++t) bytes += issue_row(j0 + t, &W.bar[nstage]);
                 bytes += issue_qblock(cy + 1, nstage);
                 mbar_expect_tx(&W.bar[nstage], bytes);
+            }
+            if (cy < cstart) {   // the virtual iteration only stages the first window
+                stage = nstage;
+                continue;
             }
             const bool own_row = cy >= c0;
             const bool last_cell = cx == ns - 1;
@@ -722,7 +723,7 @@ k_sweep_q2(const SweepArgs A) {
             }
             fence_proxy_async();   // our generic smem accesses before the next TMA writes
             __syncwarp();
-            stage ^= 1;
+            stage = nstage;
         }
         __syncwarp();
     }
