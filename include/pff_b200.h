@@ -79,6 +79,19 @@ int64_t pff_level_n_scalar(const pff_level* L);
 int64_t pff_level_n_cells(const pff_level* L);
 int64_t pff_level_qcache_len(const pff_level* L);
 
+/* Slab window for multi-GPU runs: the handle then owns cell
+ * rows [cy_begin, cy_end) of the global mesh and every array bound to it or
+ * passed to pff_apply is LOCAL: node rows [j_lo, j_hi] = [p*max(cy_begin-1,0),
+ * p*cy_end] (p ghost rows below, one above), x fastest, followed by the n_dup
+ * upper slit copies when row i_mid lies in that range; pff_level_n_scalar()
+ * returns that local length.  pff_apply writes only the owned node rows
+ * [p*cy_begin, p*cy_end) (plus row p*2^l for the top slab, and the slit copies
+ * on the slab owning row i_mid).  Q2 and >= 64x64 cells only; (0, 2^l) resets.
+ * pff_level_window: rows = {j_lo, j_hi, has_slit_copies, local index of the
+ * first slit copy, cy_begin, cy_end}. */
+int pff_level_set_window(pff_level* L, int cy_begin, int cy_end);
+int pff_level_window(const pff_level* L, int64_t* rows);
+
 /* Bind the linearisation point: U (3n), phi_tilde (n), flags (n bytes) and a
  * caller-allocated q-point cache of pff_level_qcache_len() doubles. */
 int pff_level_bind(pff_level* L, const double* U, const double* phi_tilde,

@@ -29,6 +29,8 @@ SIGNATURES = {
     "pff_level_n_scalar": (_i64, [ctypes.c_void_p]),
     "pff_level_n_cells": (_i64, [ctypes.c_void_p]),
     "pff_level_qcache_len": (_i64, [ctypes.c_void_p]),
+    "pff_level_set_window": (_i, [ctypes.c_void_p, _i, _i]),
+    "pff_level_window": (_i, [ctypes.c_void_p, ctypes.c_void_p]),
     "pff_level_bind": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp]),
     "pff_level_refresh": (_i, [ctypes.c_void_p, ctypes.c_void_p]),
     "pff_apply": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),

@@ -93,7 +93,36 @@ int pff_level_destroy(pff_level* L) {
 }
 
 int64_t pff_level_n_scalar(const pff_level* L) {
-    return L ? reinterpret_cast<const Level*>(L)->mesh.n : -1;
+    return L ? reinterpret_cast<const Level*>(L)->local_n() : -1;
+}
+
+int pff_level_set_window(pff_level* h, int cy_begin, int cy_end) {
+    Level* L = reinterpret_cast<Level*>(h);
+    if (!L) return fail(PFF_E_ARG, "%s", "pff_level_set_window: null level");
+    if (cy_begin == 0 && cy_end == L->mesh.nside) {   // whole mesh
+        L->win_begin = 0;
+        L->win_end = -1;
+        return 0;
+    }
+    if (cy_begin < 0 || cy_end > L->mesh.nside || cy_begin >= cy_end)
+        return fail(PFF_E_ARG, "%s", "pff_level_set_window: bad cell-row range");
+    if (!L->sweep_ok())
+        return fail(PFF_E_ARG, "%s", "pff_level_set_window: slab windows need Q2 and >= 64x64 cells");
+    L->win_begin = cy_begin;
+    L->win_end = cy_end;
+    return 0;
+}
+
+int pff_level_window(const pff_level* h, int64_t* rows) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!L || !rows) return fail(PFF_E_ARG, "%s", "pff_level_window: null argument");
+    rows[0] = L->j_lo();
+    rows[1] = L->j_hi();
+    rows[2] = L->local_dup() ? 1 : 0;
+    rows[3] = L->dupoff() - L->row_shift();   // local index of the first slit copy
+    rows[4] = L->cy_begin();
+    rows[5] = L->cy_end();
+    return 0;
 }
 
 int64_t pff_level_n_cells(const pff_level* L) {
@@ -124,7 +153,8 @@ int pff_level_refresh(pff_level* h, void* stream) {
 int pff_apply(const pff_level* h, int mode, const double* src, double* dst, const double* rhs,
               void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
-    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_apply: state not bound");
+    if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
+        return fail(PFF_E_UNBOUND, "%s", "pff_apply: state not bound");
     if (mode < 0 || mode > 3 || !src || !dst) return fail(PFF_E_ARG, "%s", "pff_apply: bad mode or null vector");
     return check(pff::launch_apply(*L, mode, src, dst, rhs, S(stream)), "pff_apply");
 }

@@ -20,8 +20,30 @@ struct Level {
     const uint8_t* flags = nullptr;     // n: F_DIR | F_ACT
     double* qcache = nullptr;           // qcache_len() doubles
 
-    // generic q-point cache (layout [field][k][cell], 6 fields)
-    int64_t generic_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells(); }
+    // Slab window (multi-GPU): this handle owns cell rows
+    // [win_begin, win_end) of the global mesh and holds LOCAL arrays with node
+    // rows [j_lo, j_hi] (p ghost rows below, 1 above) followed by the upper slit
+    // copies when row i_mid lies in that range.  win_end < 0: whole mesh.
+    int win_begin = 0, win_end = -1;
+    bool windowed() const { return win_end >= 0; }
+    int cy_begin() const { return windowed() ? win_begin : 0; }
+    int cy_end() const { return windowed() ? win_end : mesh.nside; }
+    int q_row0() const { return cy_begin() > 0 ? cy_begin() - 1 : 0; }   // first computed cell row
+    int q_rows() const { return cy_end() - q_row0(); }
+    int64_t j_lo() const { return (int64_t)mesh.p * q_row0(); }
+    int64_t j_hi() const { return (int64_t)mesh.p * cy_end(); }
+    bool local_dup() const { return mesh.n_dup > 0 && mesh.i_mid >= j_lo() && mesh.i_mid <= j_hi(); }
+    int64_t local_n() const {
+        return windowed() ? (j_hi() - j_lo() + 1) * mesh.np1 + (local_dup() ? mesh.n_dup : 0) : mesh.n;
+    }
+    // offset of the slit copies relative to the row-shifted base (base - j_lo*np1)
+    int64_t dupoff() const { return windowed() ? (j_hi() + 1) * mesh.np1 : mesh.n_grid; }
+    int64_t row_shift() const { return windowed() ? j_lo() * mesh.np1 : 0; }
+
+    // generic q-point cache (layout [field][k][cell], 6 fields); not kept for windows
+    int64_t generic_len() const {
+        return windowed() ? 0 : 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells();
+    }
     // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
     // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
@@ -29,7 +51,7 @@ struct Level {
     int n_strips() const { return (mesh.nside + 30) / 31; }
     int tile_nq() const { return miehe ? 5 : 4; }
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
-    int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * mesh.nside * tile_block() : 0; }
+    int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
     int64_t qcache_len() const { return generic_len() + tile_len(); }
     double* qtile() const { return qcache + generic_len(); }
 };

@@ -543,6 +543,7 @@ struct ResidualL {
 }  // namespace
 
 cudaError_t launch_refresh(const Level& L, cudaStream_t s) {
+    if (L.windowed()) return launch_refresh_tiled(L, s);   // slabs keep only the tiled cache
     cudaError_t e = dispatch_p_split<RefreshL>(L.mesh.p, L.miehe, &L, s);
     if (e == cudaSuccess && L.sweep_ok()) e = launch_refresh_tiled(L, s);
     return e;
@@ -554,6 +555,10 @@ void set_generic_apply(bool on) { g_generic_apply = on; }
 cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
                          const double* rhs, cudaStream_t s) {
     bool handled = false;
+    if (L.windowed()) {   // slabs run the write-once sweep kernel only
+        cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
+        return handled ? e : cudaErrorNotSupported;
+    }
     if (!g_generic_apply) {
         cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
         if (handled || e != cudaSuccess) return e;
@@ -563,10 +568,12 @@ cudaError_t launch_apply(const Level& L, int mode, const double* src, double* ds
 
 cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, int invert,
                             cudaStream_t s) {
+    if (L.windowed()) return cudaErrorNotSupported;
     return dispatch_p_split<DiagL>(L.mesh.p, L.miehe, &L, dx, dy, dp, invert, s);
 }
 
 cudaError_t launch_residual(const Level& L, double* out, int md, int ma, cudaStream_t s) {
+    if (L.windowed()) return cudaErrorNotSupported;
     return dispatch_p_split<ResidualL>(L.mesh.p, L.miehe, &L, out, md, ma, s);
 }
 

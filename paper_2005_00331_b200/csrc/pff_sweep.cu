@@ -99,6 +99,9 @@ struct SweepArgs {
     const double* src_out[3];
     const double* rhs[3];
     int n_strips, rows_per_chunk, n_items;
+    int cy_begin, cy_end;         // owned cell rows (window)
+    int q_row0, q_rows;           // cell rows held by the tiled q-point cache
+    int64_t dupoff;               // slit copies: fld[f] + dupoff + i
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -264,13 +267,15 @@ __device__ __forceinline__ double miehe_pc(double lam, double mu, double gdd, do
 // ------------------------------------------------------------- tiled refresh
 template <bool MIEHE>
 __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __restrict__ U,
-                                double* __restrict__ qt, int n_strips, int64_t qblock) {
+                                double* __restrict__ qt, int n_strips, int64_t qblock,
+                                int q_row0, int q_rows, int64_t n_local, int64_t row_shift,
+                                int64_t dupoff) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t total = (int64_t)n_strips * m.nside * SW_LANES;
+    const int64_t total = (int64_t)n_strips * q_rows * SW_LANES;
     if (t >= total) return;
     const int lane = (int)(t % SW_LANES);
-    const int64_t blk = t / SW_LANES;            // = strip * nside + cy
-    const int strip = (int)(blk / m.nside), cy = (int)(blk % m.nside);
+    const int64_t blk = t / SW_LANES;            // = strip * q_rows + (cy - q_row0)
+    const int strip = (int)(blk / q_rows), cy = q_row0 + (int)(blk % q_rows);
     const int cx = strip * SW_OWN - 1 + lane;
     double* out = qt + blk * qblock + lane;
     constexpr int NQS = MIEHE ? 4 : 3;
@@ -279,13 +284,14 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
             for (int k = 0; k < QK; ++k) out[(a * QK + k) * SW_LANES] = 0.0;
         return;
     }
-    const int64_t n = m.n;
+    const int64_t n = n_local;
     double cu[3][3], cv[3][3];
 #pragma unroll
     for (int b = 0; b < 3; ++b)
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const int64_t g = m.node(cx, cy, a, b);
+            int64_t g = m.node(cx, cy, a, b);
+            g = g >= m.n_grid ? dupoff + (g - m.n_grid) - row_shift : g - row_shift;
             cu[b][a] = U[g];
             cv[b][a] = U[n + g];
         }
@@ -363,8 +369,8 @@ k_sweep_q2(const SweepArgs A) {
 
     for (int item = blockIdx.x; item < A.n_items; item += gridDim.x) {
         const int strip = item % A.n_strips, chunk = item / A.n_strips;
-        const int c0 = chunk * A.rows_per_chunk;
-        const int c1 = min(ns, c0 + A.rows_per_chunk);
+        const int c0 = A.cy_begin + chunk * A.rows_per_chunk;
+        const int c1 = min(A.cy_end, c0 + A.rows_per_chunk);
         const int cstart = c0 > 0 ? c0 - 1 : 0;
         const int x0 = strip * SW_OWN;
         const int cx = x0 - 1 + lane;
@@ -397,7 +403,8 @@ k_sweep_q2(const SweepArgs A) {
         };
         auto issue_qblock = [&](int cy, int stage) -> unsigned {
             if (NQ == 0) return 0u;
-            const double* src = A.qtile + ((int64_t)strip * ns + cy) * A.qblock + qarr0 * QARR;
+            const double* src =
+                A.qtile + ((int64_t)strip * A.q_rows + (cy - A.q_row0)) * A.qblock + qarr0 * QARR;
             bulk_g2s(W.q[stage], src, (unsigned)(NQ * QARR * 8), &W.bar[stage]);
             return (unsigned)(NQ * QARR * 8);
         };
@@ -416,8 +423,8 @@ k_sweep_q2(const SweepArgs A) {
                 if (gc < 0 || gc >= m.i_mid) continue;
 #pragma unroll
                 for (int f = 0; f < NFIELDS; ++f)
-                    if (U::used(f)) setv(slot, f, k, A.fld[f][m.n_grid + gc]);
-                W.f[slot][W.foff[slot] + k] = A.flags[m.n_grid + gc];
+                    if (U::used(f)) setv(slot, f, k, A.fld[f][A.dupoff + gc]);
+                W.f[slot][W.foff[slot] + k] = A.flags[A.dupoff + gc];
             }
         };
         // stores: identity rows take the raw staged src value (slot/column) or,
@@ -698,7 +705,7 @@ k_sweep_q2(const SweepArgs A) {
                             store(j * np1 + gc, v, A.flags[j * np1 + gc], -1, 0, -1);
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = r[c][0][a] + (a == 0 ? left[c][0] : 0.0);
-                            store(m.n_grid + gc, v, A.flags[m.n_grid + gc], s0, 2 * lane + a, -1);
+                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], s0, 2 * lane + a, -1);
                             continue;
                         }
 #pragma unroll
@@ -753,7 +760,7 @@ cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
         if (cfg.blocks_per_sm < 1) cfg.blocks_per_sm = 1;
         cfg.init = true;
     }
-    const int ns = a.m.nside;
+    const int ns = a.cy_end - a.cy_begin;   // cell rows to cover
     const int slots = cfg.blocks_per_sm * n_sm;
     int rows = rows_override;
     if (rows <= 0) {
@@ -792,14 +799,16 @@ void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
 
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
     const Mesh& m = L.mesh;
-    const int64_t total = (int64_t)L.n_strips() * m.nside * SW_LANES;
+    const int64_t total = (int64_t)L.n_strips() * L.q_rows() * SW_LANES;
     const unsigned grid = (unsigned)((total + 127) / 128);
     if (L.miehe)
         k_refresh_tiled<true><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.qtile(), L.n_strips(),
-                                                   L.tile_block());
+                                                   L.tile_block(), L.q_row0(), L.q_rows(),
+                                                   L.local_n(), L.row_shift(), L.dupoff());
     else
         k_refresh_tiled<false><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.qtile(), L.n_strips(),
-                                                    L.tile_block());
+                                                    L.tile_block(), L.q_row0(), L.q_rows(),
+                                                    L.local_n(), L.row_shift(), L.dupoff());
     count_launches(1);
     return cudaGetLastError();
 }
@@ -809,9 +818,15 @@ cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, doub
     *handled = false;
     if (!L.sweep_ok()) return cudaSuccess;
     const Mesh& m = L.mesh;
-    const int64_t n = m.n;
+    const int64_t n = L.local_n();
+    const int64_t sh = L.row_shift();   // global node j*np1+i lives at local index - sh
     SweepArgs a;
     a.m = m;
+    a.cy_begin = L.cy_begin();
+    a.cy_end = L.cy_end();
+    a.q_row0 = L.q_row0();
+    a.q_rows = L.q_rows();
+    a.dupoff = L.dupoff();
     a.S = L.shape;
     a.M = L.mat;
     {
@@ -840,30 +855,30 @@ cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, doub
     switch (mode) {
         case MODE_FULL:
         case MODE_PHIROW:
-            a.fld[FX] = src; a.fld[FY] = src + n; a.fld[FP] = src + 2 * n; break;
+            a.fld[FX] = src - sh; a.fld[FY] = src + n - sh; a.fld[FP] = src + 2 * n - sh; break;
         case MODE_UU:
-            a.fld[FX] = src; a.fld[FY] = src + n; break;
+            a.fld[FX] = src - sh; a.fld[FY] = src + n - sh; break;
         case MODE_PHIPHI:
-            a.fld[FP] = src; break;
+            a.fld[FP] = src - sh; break;
         default: return cudaErrorInvalidValue;
     }
-    a.fld[F0P] = L.U + 2 * n;
-    a.fld[FPT] = L.phi_tilde;
-    a.flags = L.flags;
+    a.fld[F0P] = L.U + 2 * n - sh;
+    a.fld[FPT] = L.phi_tilde - sh;
+    a.flags = L.flags - sh;
     a.qtile = L.qtile();
     a.qblock = L.tile_block();
     for (int c = 0; c < 3; ++c) { a.dst[c] = nullptr; a.src_out[c] = nullptr; a.rhs[c] = nullptr; }
     if (mode == MODE_FULL || mode == MODE_UU) {
         const int nc = mode == MODE_FULL ? 3 : 2;
         for (int c = 0; c < nc; ++c) {
-            a.dst[c] = dst + c * n;
-            a.src_out[c] = src + c * n;
-            a.rhs[c] = rhs ? rhs + c * n : nullptr;
+            a.dst[c] = dst + c * n - sh;
+            a.src_out[c] = src + c * n - sh;
+            a.rhs[c] = rhs ? rhs + c * n - sh : nullptr;
         }
     } else {
-        a.dst[0] = dst;
-        a.src_out[0] = mode == MODE_PHIROW ? src + 2 * n : src;
-        a.rhs[0] = rhs;
+        a.dst[0] = dst - sh;
+        a.src_out[0] = (mode == MODE_PHIROW ? src + 2 * n : src) - sh;
+        a.rhs[0] = rhs ? rhs - sh : nullptr;
     }
     a.n_strips = L.n_strips();
     int rows = g_rows_override;

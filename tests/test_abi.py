@@ -40,7 +40,16 @@ def test_abi_version_and_host_only_calls():
     assert rc == 0
     assert L.pff_level_n_scalar(h) == 4_199_425
     assert L.pff_level_n_cells(h) == 1024 * 1024
-    assert L.pff_level_qcache_len(h) == 6 * 9 * 1024 * 1024
+    # generic cache + strip-tiled Q2 cache (34 strips x 1024 rows x 5 arrays x 9 q x 32 lanes)
+    assert L.pff_level_qcache_len(h) == 6 * 9 * 1024 * 1024 + 34 * 1024 * 5 * 9 * 32
+    rows = (ctypes.c_int64 * 6)()
+    assert L.pff_level_set_window(h, 256, 512) == 0
+    assert L.pff_level_window(h, rows) == 0
+    assert list(rows) == [510, 1024, 1, 515 * 2049, 256, 512]
+    assert L.pff_level_n_scalar(h) == (1024 - 510 + 1) * 2049 + 1024
+    assert L.pff_level_set_window(h, 0, 1024) == 0
+    assert L.pff_level_n_scalar(h) == 4_199_425
+    assert L.pff_level_set_window(h, 10, 5) < 0
     # unbound state is an error, not a crash
     assert L.pff_apply(h, 0, None, None, None, None) < 0
     assert b"not bound" in L.pff_last_error()

@@ -1,0 +1,205 @@
+"""Slab decomposition: partition bookkeeping on CPU, the
+ghost-row exchange and the distributed operator/dot over gloo with world
+size 2 and 4 (the local cell kernel replaced by the C oracle on CPU), and the
+slab-window CUDA kernel against the whole-mesh kernel on one GPU."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import block_rel
+from oracle import oracle as O
+from paper_2005_00331_b200 import _lib
+from paper_2005_00331_b200.parallel import HaloExchange, SlabPartition, SlabState, owned_dot
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("p,level", [(2, 4), (2, 6), (1, 5), (3, 4)])
+def test_partition_covers_every_node_once(world, p, level):
+    part = SlabPartition(p, level, world)
+    count = np.zeros(part.n, dtype=np.int64)
+    for r in range(world):
+        idx = part.local_index(r)
+        assert idx.size == part.local_n(r)
+        count[idx[part.owned_mask(r)]] += 1
+        lo, hi = part.rows(r)
+        olo, ohi = part.own_rows(r)
+        assert lo <= olo < ohi <= hi + 1
+        if r > 0:
+            assert olo - lo == p            # p ghost rows below
+        if r < world - 1:
+            assert hi == ohi                 # one ghost row above
+    assert np.all(count == 1)
+    # the slit copies belong to exactly one rank, the one owning row i_mid
+    owners = [r for r in range(world) if part.owns_dup(r)]
+    assert len(owners) == 1
+
+
+def test_partition_rejects_bad_worlds():
+    with pytest.raises(ValueError):
+        SlabPartition(2, 4, 3)
+    with pytest.raises(ValueError):
+        SlabPartition(2, 2, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class OracleSlab(SlabState):
+    """SlabState whose local cell kernel is the C oracle (CPU test double):
+    the local slab (owned + ghost rows) is embedded in a zero global vector,
+    the whole-mesh oracle operator applied, and the owned rows kept -- so the
+    owned rows near the slab edges are right only if the ghosts are."""
+
+    def __init__(self, ost, *a, **k):
+        super().__init__(*a, **k)
+        self.ost = ost
+
+    def _local_apply(self, mode, src, dst, rhs):
+        part, n = self.part, self.part.n
+        idx = part.local_index(self.rank)
+        ln = idx.size
+        ncomp_in = {0: 3, 1: 2, 2: 1, 3: 3}[mode]
+        g = np.zeros(3 * n)
+        comps = {0: (0, 1, 2), 1: (0, 1), 2: (2,), 3: (0, 1, 2)}[mode]
+        s = src.numpy()
+        for k, c in enumerate(comps):
+            g[c * n + idx] = s[k * ln:(k + 1) * ln]
+        fn = {0: O.apply_jacobian, 1: lambda st, v: O.apply_block_uu(st, v[:2 * n]),
+              2: lambda st, v: O.apply_block_phiphi(st, v[2 * n:]), 3: O.apply_phi_row}[mode]
+        out = fn(self.ost, g)
+        own = part.owned_mask(self.rank)
+        d = dst.numpy()
+        ncomp_out = {0: 3, 1: 2, 2: 1, 3: 1}[mode]
+        for k in range(ncomp_out):
+            loc = out[k * n + idx]
+            blk = d[k * ln:(k + 1) * ln]
+            blk[own] = loc[own]
+            if rhs is not None:
+                blk[own] = rhs.numpy()[k * ln:(k + 1) * ln][own] - loc[own]
+
+
+def _worker(rank, world, port, level, split, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        part = SlabPartition(2, level, world)
+        ost, x = O.baseline_state(2, level, split, seed=3)
+        ost.refresh_cache()
+        cpu = torch.device("cpu")
+        st = OracleSlab(ost, part, rank, ost.params, split, ost.U, ost.phi_tilde, ost.active,
+                        ost.dirichlet, device=cpu)
+        n, ln = part.n, part.local_n(rank)
+        own = np.tile(part.owned_mask(rank), 3)
+        # 1. ghost exchange: start from owned values only, ghosts must arrive
+        full = torch.from_numpy(part.scatter(x, rank, 3))
+        v = torch.where(torch.from_numpy(own), full, torch.zeros((), dtype=torch.float64))
+        st.halo.exchange(v, 3)
+        lo, hi = part.rows(rank)
+        grid_part = np.tile(np.r_[np.ones((hi - lo + 1) * part.np1, bool),
+                                  np.zeros(ln - (hi - lo + 1) * part.np1, bool)], 1)
+        for c in range(3):
+            blk = slice(c * ln, c * ln + (hi - lo + 1) * part.np1)
+            assert torch.equal(v[blk], full[blk]), ("ghost rows", rank, c)
+        # 2. distributed operator, every mode, plain and fused
+        results = {}
+        for mode, nin, nout in ((0, 3, 3), (1, 2, 2), (2, 1, 1), (3, 3, 1)):
+            comps = {0: (0, 1, 2), 1: (0, 1), 2: (2,), 3: (0, 1, 2)}[mode]
+            src = torch.cat([torch.from_numpy(part.scatter(x[c * n:(c + 1) * n], rank, 1))
+                             * torch.from_numpy(part.owned_mask(rank)).double() for c in comps])
+            dst = st.empty(nout)
+            st.apply_into(mode, src, dst)
+            glob = np.zeros(nout * n)
+            part.gather_into(glob, dst.numpy(), rank, nout)
+            t = torch.from_numpy(glob)
+            dist.all_reduce(t)
+            results[mode] = t.numpy()
+        # 3. distributed dot over owned entries
+        xl = torch.from_numpy(part.scatter(x, rank, 3))
+        dot = owned_dot(part, rank, xl, xl, 3)
+        if rank == 0:
+            q.put(("ok", results, dot))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put(("err", traceback.format_exc(), None))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_gloo_distributed_operator(world, split):
+    level = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, level, split, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, results, dot = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert status == "ok", results
+    ost, x = O.baseline_state(2, level, split, seed=3)
+    ost.refresh_cache()
+    n = ost.n
+    want = {0: O.apply_jacobian(ost, x), 1: O.apply_block_uu(ost, x[:2 * n]),
+            2: O.apply_block_phiphi(ost, x[2 * n:]), 3: O.apply_phi_row(ost, x)}
+    for mode, w in want.items():
+        assert max(block_rel(results[mode], w, n)) <= 1e-14, mode
+    assert dot == pytest.approx(float(x @ x), rel=1e-13)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", ["miehe", "none"])
+@pytest.mark.parametrize("world,level", [(2, 8), (4, 9), (8, 9)])
+def test_slab_window_kernel_matches_whole_mesh(split, world, level):
+    """Emulate the ranks one after another on one GPU (ghosts taken from the
+    global arrays): owned rows of every slab == the whole-mesh application."""
+    import paper_2005_00331_b200 as P
+    ost, x = O.baseline_state(2, level, split, seed=4)
+    h = P.build_hierarchy(level, 2)
+    gst = P.LinearizationState(h, level, ost.params, split=split)
+    gst.set_solution(ost.U)
+    gst.set_phi_tilde(ost.phi_tilde)
+    gst.set_active(ost.active)
+    gst.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    gst.refresh_cache()
+    n = gst.n_scalar
+    part = SlabPartition(2, level, world)
+    rhs = np.random.default_rng(2).standard_normal(3 * n)
+    for mode, nin, nout in ((0, 3, 3), (1, 2, 2), (2, 1, 1), (3, 3, 1)):
+        comps = {0: (0, 1, 2), 1: (0, 1), 2: (2,), 3: (0, 1, 2)}[mode]
+        xin = np.concatenate([x[c * n:(c + 1) * n] for c in comps])
+        xd = torch.from_numpy(xin).cuda()
+        want = torch.empty(nout * n, dtype=torch.float64, device="cuda")
+        gst.apply_into(mode, xd, want)
+        wantf = torch.empty_like(want)
+        rhd = torch.from_numpy(rhs[:nout * n]).cuda()
+        gst.apply_into(mode, xd, wantf, rhd)
+        got = np.zeros(nout * n)
+        gotf = np.zeros(nout * n)
+        for r in range(world):
+            st = SlabState(part, r, ost.params, split, ost.U, ost.phi_tilde, ost.active,
+                           ost.dirichlet)
+            st.refresh_cache()
+            src = torch.from_numpy(part.scatter(xin, r, nin)).cuda()
+            dst = st.empty(nout)
+            st.apply_into(mode, src, dst, exchange=False)
+            part.gather_into(got, dst.cpu().numpy(), r, nout)
+            rl = torch.from_numpy(part.scatter(rhs[:nout * n], r, nout)).cuda()
+            st.apply_into(mode, src, dst, rl, exchange=False)
+            part.gather_into(gotf, dst.cpu().numpy(), r, nout)
+        assert max(block_rel(got, want.cpu().numpy(), n)) <= 1e-15, mode
+        assert max(block_rel(gotf, wantf.cpu().numpy(), n)) <= 1e-15, mode
