@@ -156,6 +156,11 @@ class HaloExchange:
     def exchange(self, vec: torch.Tensor, ncomp: int):
         if self.part.world == 1:
             return
+        if vec.is_cuda and dist.get_backend(self.group) == "gloo":
+            host = vec.cpu()          # gloo point-to-point is host-only (test/debug path)
+            self.exchange(host, ncomp)
+            vec.copy_(host)
+            return
         ops = []
         for c in range(ncomp):
             for peer, a, b in self.recvs:
