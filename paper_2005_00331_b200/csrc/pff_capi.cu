@@ -78,9 +78,13 @@ int pff_level_create(pff_level** out, int degree, int level, int split, const pf
     if (degree == 2) {
         const auto& S = L->shape;
         auto near = [](double a, double b, double tol) { return a - b <= tol && b - a <= tol; };
-        L->q2_struct = near(S.N[1][0], 0.0, 1e-14) && near(S.N[1][1], 1.0, 1e-14) &&
-                       near(S.N[1][2], 0.0, 1e-14) && near(S.D[1][0], -1.0, 1e-13) &&
-                       near(S.D[1][1], 0.0, 1e-13) && near(S.D[1][2], 1.0, 1e-13);
+        bool ok = near(S.N[1][0], 0.0, 1e-14) && near(S.N[1][1], 1.0, 1e-14) &&
+                  near(S.N[1][2], 0.0, 1e-14) && near(S.D[1][0], -1.0, 1e-13) &&
+                  near(S.D[1][1], 0.0, 1e-13) && near(S.D[1][2], 1.0, 1e-13) &&
+                  near(S.w[0], S.w[2], 1e-15);
+        for (int a = 0; a < 3; ++a)   // mirror symmetry of the outer Gauss points
+            ok = ok && near(S.N[2][a], S.N[0][2 - a], 1e-14) && near(S.D[2][a], -S.D[0][2 - a], 1e-13);
+        L->q2_struct = ok;
     }
     L->miehe = split;
     *out = reinterpret_cast<pff_level*>(L);

@@ -22,6 +22,7 @@
 //  * the slit (src/mesh_hierarchy.py:156-189): the upper cell row reads the
 //    upper copies (n_grid + i) and lower/upper copies are stored apart.
 #include <cstdlib>
+#include <type_traits>
 
 #include "pff_internal.cuh"
 
@@ -365,7 +366,7 @@ k_sweep_q2(const SweepArgs A) {
         fence_mbar_init();
     }
     __syncwarp();
-    unsigned use_count[2] = {0u, 0u};
+    unsigned phase = 0u;   // bit s: parity of the next completion of mbarrier s
 
     for (int item = blockIdx.x; item < A.n_items; item += gridDim.x) {
         const int strip = item % A.n_strips, chunk = item / A.n_strips;
@@ -478,8 +479,8 @@ k_sweep_q2(const SweepArgs A) {
                                       A.rhs[c] + (jb + b) * np1 + 2 * (int64_t)cx + a);
             }
             cp_async_commit();
-            mbar_wait(&W.bar[stage], use_count[stage] & 1u);
-            use_count[stage]++;
+            mbar_wait(&W.bar[stage], (phase >> stage) & 1u);
+            phase ^= 1u << stage;
             const int s0 = (int)(jb % RING), s1 = (int)((jb + 1) % RING), s2 = (int)((jb + 2) % RING);
             const bool slit_row = m.level >= 1 && cy == half;
             if (slit_row) {
@@ -521,17 +522,29 @@ k_sweep_q2(const SweepArgs A) {
             // coefficients are constant-bank operands.
             const SweepConst& K = A.K;
             double r[3][3][3] = {};   // [comp x, y, phi][b][a]
-#pragma unroll
-            for (int iq = 0; iq < 3; ++iq) {
+            // One quadrature column.  MID: the middle column iq = 1 (exact
+            // structure); otherwise the outer column iq = 2*side, evaluated as
+            // column 0 on mirrored node data (N[2][a] = N[0][2-a],
+            // D[2][a] = -D[0][2-a], w[2] = w[0]; checked on the host) so both
+            // outer columns share one loop body (instruction-cache footprint).
+            auto column = [&](auto MIDC, auto SIDEC) {
+                constexpr bool MID = decltype(MIDC)::value;
+                const int side = SIDEC;
+                const int iq = MID ? 1 : 2 * side;
+                const int ic = MID ? 1 : 0;        // coefficient / weight column
+                const double sD = (!MID && side) ? -1.0 : 1.0;
+                auto g = [&](int f, int b, int a) -> double {
+                    return MID ? get(f, b, a) : get(f, b, side ? 2 - a : a);
+                };
                 auto xN = [&](int f, int b) -> double {
-                    if (iq == 1) return get(f, b, 1);
-                    return fma(K.N[iq][2], get(f, b, 2),
-                               fma(K.N[iq][1], get(f, b, 1), K.N[iq][0] * get(f, b, 0)));
+                    if (MID) return g(f, b, 1);
+                    return fma(K.N[0][2], g(f, b, 2),
+                               fma(K.N[0][1], g(f, b, 1), K.N[0][0] * g(f, b, 0)));
                 };
                 auto xD = [&](int f, int b) -> double {
-                    if (iq == 1) return K.ih * (get(f, b, 2) - get(f, b, 0));
-                    return fma(K.Dh[iq][2], get(f, b, 2),
-                               fma(K.Dh[iq][1], get(f, b, 1), K.Dh[iq][0] * get(f, b, 0)));
+                    if (MID) return K.ih * (g(f, b, 2) - g(f, b, 0));
+                    return sD * fma(K.Dh[0][2], g(f, b, 2),
+                                    fma(K.Dh[0][1], g(f, b, 1), K.Dh[0][0] * g(f, b, 0)));
                 };
                 double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3], X0p[3], Xt[3];
 #pragma unroll
@@ -556,7 +569,7 @@ k_sweep_q2(const SweepArgs A) {
                         return fma(K.Dh[jq][2], X[2], fma(K.Dh[jq][1], X[1], K.Dh[jq][0] * X[0]));
                     };
                     const int k = jq * 3 + iq;
-                    const double wv = K.wv[k];
+                    const double wv = K.wv[jq * 3 + ic];
                     double s11 = 0.0, s22 = 0.0, s12 = 0.0, spde = 0.0, pc = 0.0;
                     if (MIEHE) {
                         MieheS q{};
@@ -613,8 +626,8 @@ k_sweep_q2(const SweepArgs A) {
                         double pval = pc * yN(XpN);
                         if (U::DO_COUP) pval = fma(K.gdd * yN(X0p), spde, pval);
                         fv = pval * wv;
-                        fgx = K.cgw[k] * yN(XpD);
-                        fgy = K.cgw[k] * yD(XpN);
+                        fgx = K.cgw[jq * 3 + ic] * yN(XpD);
+                        fgy = K.cgw[jq * 3 + ic] * yD(XpN);
                     }
                     // backward y-pass: T[b] += M[jq][b] f
                     if (jq == 1) {
@@ -652,7 +665,7 @@ k_sweep_q2(const SweepArgs A) {
                 // backward x-pass: r[b][a] += Dh[iq][a] T1[b] + N[iq][a] T2[b]
 #pragma unroll
                 for (int b = 0; b < 3; ++b) {
-                    if (iq == 1) {
+                    if (MID) {
                         if (U::DO_UU) {
                             const double tu = K.ih * Tu1[b], tv = K.ih * Tv1[b];
                             r[0][b][0] -= tu; r[0][b][1] += Tu2[b]; r[0][b][2] += tu;
@@ -663,17 +676,37 @@ k_sweep_q2(const SweepArgs A) {
                             r[2][b][0] -= tp; r[2][b][1] += Tp1[b]; r[2][b][2] += tp;
                         }
                     } else {
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) {
-                            const double na = K.N[iq][a], da = K.Dh[iq][a];
-                            if (U::DO_UU) {
-                                r[0][b][a] = fma(da, Tu1[b], fma(na, Tu2[b], r[0][b][a]));
-                                r[1][b][a] = fma(da, Tv1[b], fma(na, Tv2[b], r[1][b][a]));
-                            }
-                            if (U::DO_PP) r[2][b][a] = fma(na, Tp1[b], fma(da, Tp2[b], r[2][b][a]));
+                        // contributions to the mirrored columns a' = (side ? 2-a : a)
+                        auto acc = [&](double (&rb)[3], double t1, double t2) {
+                            const double t1s = sD * t1;
+                            const double c0 = fma(K.Dh[0][0], t1s, K.N[0][0] * t2);
+                            const double c1 = fma(K.Dh[0][1], t1s, K.N[0][1] * t2);
+                            const double c2 = fma(K.Dh[0][2], t1s, K.N[0][2] * t2);
+                            rb[0] += side ? c2 : c0;
+                            rb[1] += c1;
+                            rb[2] += side ? c0 : c2;
+                        };
+                        if (U::DO_UU) {
+                            acc(r[0][b], Tu1[b], Tu2[b]);
+                            acc(r[1][b], Tv1[b], Tv2[b]);
                         }
+                        if (U::DO_PP) acc(r[2][b], Tp2[b], Tp1[b]);
                     }
                 }
+            };
+            using I0 = std::integral_constant<int, 0>;
+            using I1 = std::integral_constant<int, 1>;
+            column(std::true_type{}, I0{});
+            // the Miehe FULL body is large enough to thrash the instruction cache:
+            // there the two outer columns run as one rolled, runtime-mirrored body;
+            // elsewhere they are unrolled (the mirror then folds into constants)
+            constexpr bool COMPACT = MIEHE && MODE == MODE_FULL;
+            if constexpr (COMPACT) {
+#pragma unroll 1
+                for (int side = 0; side < 2; ++side) column(std::false_type{}, side);
+            } else {
+                column(std::false_type{}, I0{});
+                column(std::false_type{}, I1{});
             }
             if (!active) {
 #pragma unroll
