@@ -117,6 +117,10 @@ int pff_residual(const pff_level* L, double* out, int mask_dirichlet, int mask_a
                  void* stream);
 
 /* TransferOperator (src/multigrid.py:97-120) between fine = coarse + 1.
+ * A windowed fine level (slab) transfers its OWNED fine nodes only: restrict
+ * accumulates their P^T contributions into the whole-mesh coarse vector (sum
+ * the ranks' partial coarse vectors with an all-reduce), prolongate fills /
+ * updates its owned fine rows from a whole-mesh coarse vector.
  * prolongate: yf = P xc, or with add_masked: yf += where(cons_f, 0, P xc)
  * (src/multigrid.py:340-342).  restrict: xc = P^T yf, zero_cons: xc[cons_c]=0. */
 int pff_prolongate(const pff_level* fine, const pff_level* coarse, const double* xc,
@@ -158,6 +162,11 @@ int pff_dot(int64_t n, const double* x, const double* y, double* partials, doubl
  * h[0..j] = coefficients, h[j+1] = ||w||. */
 int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* partials,
             double* h, void* stream);
+
+/* multi-dot out[i] = V[i] . w for i < k (CGS2 orthogonalisation of the
+ * distributed GMRES); partials = k * pff_reduce_scratch_len() / 2 doubles */
+int pff_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* partials,
+             double* out, void* stream);
 
 /* out = sum_{i<k} y[i] V[i] (+ out if accumulate); y is a device array */
 int pff_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y, double* out,

@@ -167,7 +167,7 @@ int pff_diagonal(const pff_level* h, double* duu, double* dpp, int invert, void*
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_diagonal: state not bound");
     if (!duu || !dpp) return fail(PFF_E_ARG, "%s", "pff_diagonal: null output");
-    return check(pff::launch_diagonal(*L, duu, duu + L->mesh.n, dpp, invert, S(stream)),
+    return check(pff::launch_diagonal(*L, duu, duu + L->local_n(), dpp, invert, S(stream)),
                  "pff_diagonal");
 }
 
@@ -259,6 +259,13 @@ int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* p
             void* stream) {
     if (n < 0 || j < 0 || !V || !w || !partials || !h || ldv < n) return fail(PFF_E_ARG, "%s", "pff_mgs: bad argument");
     return check(pff::launch_mgs(n, j, V, ldv, w, partials, h, S(stream)), "pff_mgs");
+}
+
+int pff_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* partials,
+             double* out, void* stream) {
+    if (n < 0 || k < 0 || k > 4096 || !V || !w || !partials || !out || ldv < n)
+        return fail(PFF_E_ARG, "%s", "pff_mdot: bad argument");
+    return check(pff::launch_mdot(n, k, V, ldv, w, partials, out, S(stream)), "pff_mdot");
 }
 
 int pff_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y, double* out,

@@ -7,6 +7,27 @@ namespace pff {
 // kernels (and memsets) enqueued by this library; see pff_launch_counter()
 void count_launches(int k);
 
+// Local window of a level as seen by the generic (any-degree) kernels: cells
+// of rows [row0, row0 + ncell/nside); global node id g lives at local index
+// g - shift (grid rows) or dupl + (g - n_grid) (slit copies); n = local length.
+struct Win {
+    int row0;
+    int64_t ncell, shift, dupl, n;
+    int64_t own_lo, own_hi;   // owned node rows
+    int owns_dup;
+    __host__ __device__ __forceinline__ int64_t loc(const Mesh& m, int64_t g) const {
+        return g >= m.n_grid ? dupl + (g - m.n_grid) : g - shift;
+    }
+    // t-th owned node (grid rows first, then the slit copies) -> global id
+    __host__ __device__ __forceinline__ int64_t owned_global(const Mesh& m, int64_t t) const {
+        const int64_t cnt = (own_hi - own_lo) * m.np1;
+        return t < cnt ? own_lo * m.np1 + t : m.n_grid + (t - cnt);
+    }
+    __host__ __device__ __forceinline__ int64_t n_owned(const Mesh& m) const {
+        return (own_hi - own_lo) * m.np1 + (owns_dup ? m.n_dup : 0);
+    }
+};
+
 // Per-level handle contents (the C-ABI's opaque pff_level).
 struct Level {
     Mesh mesh;
@@ -40,10 +61,29 @@ struct Level {
     int64_t dupoff() const { return windowed() ? (j_hi() + 1) * mesh.np1 : mesh.n_grid; }
     int64_t row_shift() const { return windowed() ? j_lo() * mesh.np1 : 0; }
 
-    // generic q-point cache (layout [field][k][cell], 6 fields); not kept for windows
-    int64_t generic_len() const {
-        return windowed() ? 0 : 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * mesh.n_cells();
+    // owned node rows [own_lo, own_hi) and slit copies
+    int64_t own_lo() const { return (int64_t)mesh.p * cy_begin(); }
+    int64_t own_hi() const {
+        return (int64_t)mesh.p * cy_end() + (cy_end() == mesh.nside ? 1 : 0);
     }
+    bool owns_dup() const { return mesh.n_dup > 0 && mesh.i_mid >= own_lo() && mesh.i_mid < own_hi(); }
+    // cell window of the generic kernels: cells of rows [q_row0, cy_end)
+    int64_t local_cells() const { return (int64_t)q_rows() * mesh.nside; }
+    Win win() const {
+        Win w;
+        w.row0 = q_row0();
+        w.ncell = local_cells();
+        w.shift = row_shift();
+        w.dupl = dupoff() - row_shift();
+        w.n = local_n();
+        w.own_lo = own_lo();
+        w.own_hi = own_hi();
+        w.owns_dup = owns_dup() ? 1 : 0;
+        return w;
+    }
+
+    // generic q-point cache (layout [field][k][cell], 6 fields) over the window's cells
+    int64_t generic_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells(); }
     // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
     // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
@@ -101,6 +141,8 @@ cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part
                        double* out, cudaStream_t s);
 cudaError_t launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w,
                        double* partials, double* h, cudaStream_t s);
+cudaError_t launch_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w,
+                        double* partials, double* out, cudaStream_t s);
 cudaError_t launch_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y,
                            double* out, int accumulate, cudaStream_t s);
 cudaError_t launch_lanczos_scale(int64_t n, const double* dhalf, const double* v, double* out,

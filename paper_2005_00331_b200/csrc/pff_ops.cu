@@ -43,16 +43,20 @@ __device__ __forceinline__ void grad_q(const Shape& S, const double (&c)[N1][N1]
 // qc[f][k][cell], f in {e11, e22, e12, g(phi~), g'(phi), pc}, k = jq*q+iq.
 template <int P, bool MIEHE>
 __global__ void __launch_bounds__(CELL_THREADS)
-k_refresh(Mesh m, Shape S, Material M, const double* __restrict__ U,
+k_refresh(Mesh m, Win w, Shape S, Material M, const double* __restrict__ U,
           const double* __restrict__ pt, double* __restrict__ qc) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
-    const int64_t nc = m.n_cells();
+    const int64_t nc = w.ncell;
     int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= nc) return;
-    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    int cx = (int)(cell % m.nside), cy = w.row0 + (int)(cell / m.nside);
     int64_t gid[N1][N1];
     cell_ids<N1>(m, cx, cy, gid);
-    const int64_t n = m.n;
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+        for (int a = 0; a < N1; ++a) gid[b][a] = w.loc(m, gid[b][a]);
+    const int64_t n = w.n;
     double cu[N1][N1], cv[N1][N1], cp[N1][N1], ct[N1][N1];
 #pragma unroll
     for (int b = 0; b < N1; ++b)
@@ -254,13 +258,13 @@ k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
 // quadrature point instead of once per (node, point).
 template <int P, bool MIEHE>
 __global__ void __launch_bounds__(CELL_THREADS)
-k_diag_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc, double* dx,
+k_diag_cells(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc, double* dx,
              double* dy, double* dp) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
-    const int64_t nc = m.n_cells();
+    const int64_t nc = w.ncell;
     int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= nc) return;
-    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    int cx = (int)(cell % m.nside), cy = w.row0 + (int)(cell / m.nside);
     const double h = m.h, inv_h = 1.0 / h;
     const int64_t fs = (int64_t)QQ * nc;
     double ax[N1][N1] = {}, ay[N1][N1] = {}, ap[N1][N1] = {};
@@ -307,7 +311,7 @@ k_diag_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc, double*
     for (int b = 0; b < N1; ++b)
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
-            int64_t g = m.node(cx, cy, a, b);
+            int64_t g = w.loc(m, m.node(cx, cy, a, b));
             atomicAdd(dx + g, ax[b][a]);
             atomicAdd(dy + g, ay[b][a]);
             atomicAdd(dp + g, ap[b][a]);
@@ -461,8 +465,9 @@ template <int P, bool MIEHE>
 struct RefreshL {
     static cudaError_t run(const Level* L, cudaStream_t s) {
         const Mesh& m = L->mesh;
-        k_refresh<P, MIEHE><<<grid_for(m.n_cells(), CELL_THREADS), CELL_THREADS, 0, s>>>(
-            m, L->shape, L->mat, L->U, L->phi_tilde, L->qcache);
+        const Win w = L->win();
+        k_refresh<P, MIEHE><<<grid_for(w.ncell, CELL_THREADS), CELL_THREADS, 0, s>>>(
+            m, w, L->shape, L->mat, L->U, L->phi_tilde, L->qcache);
         count_launches(1);
         return cudaGetLastError();
     }
@@ -516,12 +521,13 @@ struct DiagL {
     static cudaError_t run(const Level* L, double* dx, double* dy, double* dp, int invert,
                            cudaStream_t s) {
         const Mesh& m = L->mesh;
-        cudaMemsetAsync(dx, 0, sizeof(double) * m.n, s);
-        cudaMemsetAsync(dy, 0, sizeof(double) * m.n, s);
-        cudaMemsetAsync(dp, 0, sizeof(double) * m.n, s);
-        k_diag_cells<P, MIEHE><<<grid_for(m.n_cells(), CELL_THREADS), CELL_THREADS, 0, s>>>(
-            m, L->shape, L->mat, L->qcache, dx, dy, dp);
-        k_diag_finalize<<<grid_for(m.n, 256), 256, 0, s>>>(m.n, L->flags, dx, dy, dp, invert);
+        const Win w = L->win();
+        cudaMemsetAsync(dx, 0, sizeof(double) * w.n, s);
+        cudaMemsetAsync(dy, 0, sizeof(double) * w.n, s);
+        cudaMemsetAsync(dp, 0, sizeof(double) * w.n, s);
+        k_diag_cells<P, MIEHE><<<grid_for(w.ncell, CELL_THREADS), CELL_THREADS, 0, s>>>(
+            m, w, L->shape, L->mat, L->qcache, dx, dy, dp);
+        k_diag_finalize<<<grid_for(w.n, 256), 256, 0, s>>>(w.n, L->flags, dx, dy, dp, invert);
         count_launches(5);
         return cudaGetLastError();
     }
@@ -543,7 +549,6 @@ struct ResidualL {
 }  // namespace
 
 cudaError_t launch_refresh(const Level& L, cudaStream_t s) {
-    if (L.windowed()) return launch_refresh_tiled(L, s);   // slabs keep only the tiled cache
     cudaError_t e = dispatch_p_split<RefreshL>(L.mesh.p, L.miehe, &L, s);
     if (e == cudaSuccess && L.sweep_ok()) e = launch_refresh_tiled(L, s);
     return e;
@@ -568,7 +573,6 @@ cudaError_t launch_apply(const Level& L, int mode, const double* src, double* ds
 
 cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, int invert,
                             cudaStream_t s) {
-    if (L.windowed()) return cudaErrorNotSupported;
     return dispatch_p_split<DiagL>(L.mesh.p, L.miehe, &L, dx, dy, dp, invert, s);
 }
 

@@ -48,13 +48,15 @@ __device__ __forceinline__ Owner fine_owner(const Mesh& mf, int64_t gid) {
 }
 
 template <int P>
-__global__ void k_prolong(Mesh mf, Mesh mc, Embed E, const double* __restrict__ xc,
+__global__ void k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
                           double* __restrict__ yf, const uint8_t* __restrict__ flags_f,
                           int add_masked) {
     constexpr int N1 = P + 1;
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= mf.n) return;
-    Owner o = fine_owner(mf, g);
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= wf.n_owned(mf)) return;
+    const int64_t gg = wf.owned_global(mf, t);
+    Owner o = fine_owner(mf, gg);
+    const int64_t g = wf.loc(mf, gg);     // local index of the fine node
     double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int my = 0; my < N1; ++my)
@@ -72,25 +74,27 @@ __global__ void k_prolong(Mesh mf, Mesh mc, Embed E, const double* __restrict__ 
         uint8_t f = flags_f[g];
         if (!(f & F_DIR)) {
             yf[g] += acc[0];
-            yf[mf.n + g] += acc[1];
+            yf[wf.n + g] += acc[1];
         }
-        if (!(f & F_ACT)) yf[2 * mf.n + g] += acc[2];
+        if (!(f & F_ACT)) yf[2 * wf.n + g] += acc[2];
     } else {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) yf[k * mf.n + g] = acc[k];
+        for (int k = 0; k < 3; ++k) yf[k * wf.n + g] = acc[k];
     }
 }
 
 template <int P>
-__global__ void k_restrict(Mesh mf, Mesh mc, Embed E, const double* __restrict__ yf,
+__global__ void k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf,
                            double* xc) {
     constexpr int N1 = P + 1;
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= mf.n) return;
-    Owner o = fine_owner(mf, g);
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= wf.n_owned(mf)) return;
+    const int64_t gg = wf.owned_global(mf, t);
+    Owner o = fine_owner(mf, gg);
+    const int64_t g = wf.loc(mf, gg);
     double v[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) v[k] = yf[k * mf.n + g];
+    for (int k = 0; k < 3; ++k) v[k] = yf[k * wf.n + g];
 #pragma unroll
     for (int my = 0; my < N1; ++my)
 #pragma unroll
@@ -145,11 +149,14 @@ inline unsigned blocks(int64_t n) { return (unsigned)((n + 255) / 256); }
 cudaError_t launch_prolongate(const Level& F, const Level& C, const double* xc, double* yf,
                               int add_masked, cudaStream_t s) {
     if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
+    if (C.windowed()) return cudaErrorNotSupported;   // coarse side is always whole-mesh
+    const Win wf = F.win();
+    const int64_t nf = wf.n_owned(F.mesh);
     switch (F.mesh.p) {
-        case 1: k_prolong<1><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
-        case 2: k_prolong<2><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
-        case 3: k_prolong<3><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
-        case 4: k_prolong<4><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 1: k_prolong<1><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 2: k_prolong<2><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 3: k_prolong<3><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 4: k_prolong<4><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
         default: return cudaErrorInvalidValue;
     }
     count_launches(1);
@@ -159,12 +166,15 @@ cudaError_t launch_prolongate(const Level& F, const Level& C, const double* xc, 
 cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, double* xc,
                             int zero_cons, cudaStream_t s) {
     if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
+    if (C.windowed()) return cudaErrorNotSupported;
+    const Win wf = F.win();
+    const int64_t nf = wf.n_owned(F.mesh);
     cudaMemsetAsync(xc, 0, sizeof(double) * 3 * C.mesh.n, s);
     switch (F.mesh.p) {
-        case 1: k_restrict<1><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
-        case 2: k_restrict<2><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
-        case 3: k_restrict<3><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
-        case 4: k_restrict<4><<<blocks(F.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc); break;
+        case 1: k_restrict<1><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
+        case 2: k_restrict<2><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
+        case 3: k_restrict<3><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
+        case 4: k_restrict<4><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
         default: return cudaErrorInvalidValue;
     }
     if (zero_cons) k_zero_cons3<<<blocks(C.mesh.n), 256, 0, s>>>(C.mesh.n, C.flags, xc);

@@ -145,6 +145,38 @@ k_mgs_step(int64_t n, const double* __restrict__ V, int64_t ldv, double* __restr
     if (threadIdx.x == 0) pout[blockIdx.x] = s;
 }
 
+// multi-dot: part[i][block] = sum over the block's elements of V[i] . w, 8 rows
+// of V per pass (w re-read once per 8 rows); fixed grid -> deterministic
+constexpr int MDOT_ROWS = 8;
+__global__ void __launch_bounds__(RED_THREADS)
+k_mdot_partials(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
+                const double* __restrict__ w, double* __restrict__ part) {
+    for (int i0 = 0; i0 < k; i0 += MDOT_ROWS) {
+        double acc[MDOT_ROWS];
+#pragma unroll
+        for (int r = 0; r < MDOT_ROWS; ++r) acc[r] = 0.0;
+        for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < n;
+             e += (int64_t)RED_BLOCKS * RED_THREADS) {
+            const double we = w[e];
+#pragma unroll
+            for (int r = 0; r < MDOT_ROWS; ++r)
+                if (i0 + r < k) acc[r] = fma(V[(int64_t)(i0 + r) * ldv + e], we, acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < MDOT_ROWS; ++r) {
+            if (i0 + r >= k) break;
+            const double s = block_sum(acc[r]);
+            if (threadIdx.x == 0) part[(int64_t)(i0 + r) * RED_BLOCKS + blockIdx.x] = s;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_mdot_final(const double* __restrict__ part, double* out) {
+    const double s = reduce_partials(part + (int64_t)blockIdx.x * RED_BLOCKS);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 // out = sum_i y[i] V[i]  (+ out)
 __global__ void k_combine(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
                           const double* __restrict__ y, double* __restrict__ out, int accumulate) {
@@ -159,7 +191,7 @@ __global__ void k_combine(int64_t n, int k, const double* __restrict__ V, int64_
 
 cudaError_t launch_cons(const Level& L, int layout, int op, const double* r, double* z,
                         cudaStream_t s) {
-    const int64_t n = L.mesh.n;
+    const int64_t n = L.local_n();
     k_cons<<<blocks(n), 256, 0, s>>>(n, L.flags, layout, op, r, z);
     count_launches(1);
     return cudaGetLastError();
@@ -214,6 +246,15 @@ cudaError_t launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w
     }
     k_reduce_final<<<1, RED_THREADS, 0, s>>>(pa, h + j + 1, 1);
     count_launches(j + 3);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w,
+                        double* partials, double* out, cudaStream_t s) {
+    if (k <= 0) return cudaSuccess;
+    k_mdot_partials<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, k, V, ldv, w, partials);
+    k_mdot_final<<<k, RED_THREADS, 0, s>>>(partials, out);
+    count_launches(2);
     return cudaGetLastError();
 }
 

@@ -149,6 +149,19 @@ class HaloExchange:
             self.sends.append((rank + 1, ohi - p, ohi))       # my top p rows -> their ghosts below
         self.lo, self.np1 = lo, np1
 
+    def zero_ghosts(self, vec: torch.Tensor, ncomp: int):
+        """Zero the ghost rows and a non-owned slit-copy segment, so local dots
+        over the whole local vector are owned dots."""
+        part, rank = self.part, self.rank
+        if part.world == 1:
+            return
+        dup0 = (part.rows(rank)[1] - self.lo + 1) * self.np1
+        for c in range(ncomp):
+            for _, a, b in self.recvs:
+                self._view(vec, c, a, b).zero_()
+            if part.has_dup(rank) and not part.owns_dup(rank):
+                vec[c * self.ln + dup0:(c + 1) * self.ln].zero_()
+
     def _view(self, vec: torch.Tensor, comp: int, a: int, b: int) -> torch.Tensor:
         base = comp * self.ln
         return vec[base + (a - self.lo) * self.np1: base + (b - self.lo) * self.np1]
