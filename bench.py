@@ -247,9 +247,10 @@ def run_ours(args):
         e2e_s = float(t.item()) / e2e_steps
         h2d = d2h = 8 * 3 * st.ln
     newton = None
-    if args.newton and rank == 0:
+    if args.newton:
         try:
-            newton = newton_step_ours(args, P, torch)
+            newton = (newton_step_ours(args, P, torch) if ws == 1
+                      else newton_step_distributed(args, P, torch, ws, rank, dev))
         except Exception as e:   # reported, never silently dropped
             newton = {"error": f"{type(e).__name__}: {e}"}
 
@@ -332,6 +333,47 @@ def newton_step_ours(args, P, torch):
             "total_s": round(t_setup + t_gmres, 4),
             "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
             "note": "gmres_s includes the rhs H2D and solution D2H"}
+
+
+def newton_step_distributed(args, P, torch, ws, rank, dev):
+    """configs[3] / configs[4] over N slabs: the slab finest level, the
+    agglomerated coarse V-cycle and CGS2 GMRES of distributed.py; timed as the
+    max over ranks (barrier + synchronize on both sides)."""
+    import torch.distributed as dist
+    from paper_2005_00331_b200.distributed import DistributedGmg, distributed_gmres
+    level = args.newton_level
+    h, params, U, pt, act, dirn, x = baseline_inputs(2, level, args.split, seed=0, notch=True)
+    n = h.dof_map(level).n_scalar
+    dmask = np.zeros(n, dtype=bool)
+    dmask[dirn] = True
+    rhs = x.copy()
+    rhs[np.concatenate([dmask, dmask, act])] = 0.0
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gmg = DistributedGmg(h, level, rank, ws, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3),
+                         device=dev)
+    gmg.setup(params, args.split, U, pt, pt, act, dmask)
+    rl_h = torch.from_numpy(gmg.part.scatter(rhs, rank, 3)).pin_memory()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t_setup = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    rl = rl_h.to(dev, non_blocking=True)
+    res = distributed_gmres(gmg, rl, P.KrylovConfig(relative_tolerance=1e-8, restart=50))
+    sol = res.solution.cpu()
+    torch.cuda.synchronize()
+    t_gmres = time.perf_counter() - t1
+    t = torch.tensor([t_setup, t_gmres], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_setup, t_gmres = (float(v) for v in t.tolist())
+    return {"config": f"{2 ** level}^2 Q2 notch over {ws} slabs, levels 2..{level} "
+                      f"(finest in slabs, coarser agglomerated), sweeps=3, restart 50, rtol 1e-8",
+            "split": args.split, "iterations": res.iterations, "converged": res.converged,
+            "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
+            "total_s": round(t_setup + t_gmres, 4), "orthogonalisation": "CGS2",
+            "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
+            "timing": "max over ranks, wall clock around synchronised regions"}
 
 
 # ------------------------------------------------------------ CPU sides
