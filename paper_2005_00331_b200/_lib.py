@@ -97,8 +97,14 @@ def load(build_if_missing: bool = True):
     return L
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args):
-    rc = getattr(load(), name)(*args)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    rc = fn(*args)
     if rc != 0:
         msg = load().pff_last_error().decode(errors="replace")
         raise PffError(f"{name} failed ({rc}): {msg}")

@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from functools import cached_property
 
@@ -267,16 +269,104 @@ def chebyshev_apply(apply_fn, diag, rhs, a: float, b: float, sweeps: int):
 # --------------------------------------------------------------- V-cycle
 
 class _BlockApply:
-    """Device block operator of one level, flagged as tensor-native."""
+    """Device block operator of one level, flagged as tensor-native.  Results
+    alternate between two buffers (callers keep at most the previous one)."""
     _pff_device = True
 
     def __init__(self, state, mode, n):
         self.state, self.mode, self.n = state, mode, n
+        self._buf = None
+        self._k = 0
 
     def __call__(self, v):
-        out = _empty(self.n)
+        if self._buf is None:
+            self._buf = (_empty(self.n), _empty(self.n), _empty(self.n))
+        self._k = (self._k + 1) % 3
+        out = self._buf[self._k]
         self.state.apply_into(self.mode, v, out)
         return out
+
+
+# Lanczos start vectors: numpy's default_rng(seed).standard_normal(n), exactly
+# the reference's draw (src/multigrid.py:133-135), so ranges match it.  They
+# depend only on (seed, n): generated once on a worker thread (numpy releases
+# the GIL) that overlaps the GPU setup work, and cached across setups.
+_START = {}
+_START_LOCK = threading.Lock()
+_POOL = None
+
+
+def _start_vector_host(seed: int, n: int) -> np.ndarray:
+    v = np.random.default_rng(seed).standard_normal(n)
+    v /= np.linalg.norm(v)
+    return v
+
+
+def prefetch_start_vectors(keys):
+    global _POOL
+    with _START_LOCK:
+        if _POOL is None:
+            _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="pff-lanczos-rng")
+        for key in keys:
+            if key not in _START:
+                _START[key] = _POOL.submit(_start_vector_host, *key)
+                while len(_START) > 64:            # bounded cache
+                    _START.pop(next(iter(_START)))
+
+
+def start_vector(seed: int, n: int) -> np.ndarray:
+    prefetch_start_vectors([(seed, n)])
+    return _START[(seed, n)].result()
+
+
+class _LanczosRun:
+    """One estimate_lambda_range run split at its two reductions."""
+
+    def __init__(self, level, block, fn, diag, seed, max_it):
+        self.level, self.block, self.fn = level, block, fn
+        self.n = diag.numel()
+        self.dhalf = 1.0 / torch.sqrt(diag)
+        v_h = start_vector(seed, self.n)
+        self.v = torch.from_numpy(v_h).to(diag.device)
+        self.v_prev = torch.zeros_like(self.v)
+        self.tmp = torch.empty_like(self.v)
+        self.w = None
+        self.beta = 0.0
+        self.alphas, self.betas = [], []
+        self.lo = self.hi = 1.0
+        self.prev = None
+        self.left = min(max_it, self.n)
+        self.done = self.left <= 0
+
+    def step_a(self):
+        st = stream_handle()
+        call("pff_mul", self.n, ptr(self.dhalf), ptr(self.v), ptr(self.tmp), st)
+        self.w = self.fn(self.tmp)
+        call("pff_mul", self.n, ptr(self.dhalf), ptr(self.w), ptr(self.w), st)
+        _axpby(-self.beta, self.v_prev, 1.0, self.w)
+
+    def step_b(self, alpha):
+        _axpby(-alpha, self.v, 1.0, self.w)
+        self.alphas.append(alpha)
+        ritz = (scipy.linalg.eigvalsh_tridiagonal(self.alphas, self.betas) if self.betas
+                else np.array([alpha]))
+        self.lo, self.hi = float(ritz[0]), float(ritz[-1])
+
+    def step_c(self, beta):
+        self.beta = beta
+        self.left -= 1
+        if beta < 1e-12 * max(1.0, abs(self.hi)):
+            self.done = True
+            return
+        if self.prev is not None and abs(self.hi - self.prev) <= 1e-4 * abs(self.hi):
+            self.done = True
+            return
+        self.prev = self.hi
+        self.betas.append(beta)
+        self.v_prev, self.v = self.v, self.w
+        call("pff_div", self.n, ptr(self.v), None, beta, ptr(self.v), stream_handle())
+        if self.left <= 0:
+            self.done = True
 
 
 class _LevelWork:
@@ -335,6 +425,13 @@ class GmgPreconditioner:
         self.finest = state.level
         if state.level < self.coarse_level:
             raise ValueError("state level below the coarse level")
+        if ranges is None:   # overlap the start-vector draws with the GPU setup below
+            keys = []
+            for l in range(state.level, self.coarse_level - 1, -1):
+                if not reuse_eigen or l not in self.ranges:
+                    n = self.hierarchy.dof_map(l).n_scalar
+                    keys += [(self.cheb.seed + 101 * l, 2 * n), (self.cheb.seed + 101 * l + 1, n)]
+            prefetch_start_vectors(keys)
         if state._cache_version != state.version:
             state.refresh_cache()
         self.states = {state.level: state}
@@ -348,12 +445,16 @@ class GmgPreconditioner:
             duu, dpp = op.block_diagonals(s, invert=False)
             self.diags[l] = {"uu": duu, "phiphi": dpp}
             self._inv[l] = (1.0 / duu, 1.0 / dpp)
+            if l not in self._work or self._work[l].resphi.numel() != s.n_scalar:
+                self._work[l] = _LevelWork(s.n_scalar)
+        todo = []
+        for l in range(self.coarse_level, state.level + 1):
             if ranges is not None:
                 self.ranges[l] = ranges[l]
             elif not reuse_eigen or l not in self.ranges:
-                self.ranges[l] = self._estimate_ranges(l)
-            if l not in self._work or self._work[l].resphi.numel() != s.n_scalar:
-                self._work[l] = _LevelWork(s.n_scalar)
+                todo.append(l)
+        if todo:
+            self.ranges.update(self._estimate_ranges_batched(todo))
         self._graph = None
         if logger.isEnabledFor(logging.DEBUG):
             logger.debug("gmg setup: levels %d..%d, ranges %s", self.coarse_level, state.level,
@@ -373,6 +474,50 @@ class GmgPreconditioner:
             lo = max(lo, cfg.lambda_min_floor * hi)
             out[block] = (lo, hi)
         return out
+
+    def _estimate_ranges_batched(self, levels):
+        """estimate_lambda_range for every (level, block) at once: the runs are
+        independent, so each round launches the work of all active runs and
+        synchronises once per reduction instead of once per run (identical
+        per-run algebra: src/multigrid.py:123-162, 259-275)."""
+        cfg = self.cheb
+        runs = []
+        for l in levels:
+            s = self.states[l]
+            n = s.n_scalar
+            for blk, mode, nb in (("uu", _lib.MODE_UU, 2 * n), ("phiphi", _lib.MODE_PHIPHI, n)):
+                runs.append(_LanczosRun(l, blk, _BlockApply(s, mode, nb), self.diags[l][blk],
+                                        cfg.seed + 101 * l + (0 if blk == "uu" else 1),
+                                        cfg.lanczos_iterations))
+        R = len(runs)
+        dev = runs[0].v.device
+        partials = torch.empty(R * _lib.load().pff_reduce_scratch_len(), dtype=torch.float64,
+                               device=dev)
+        out = torch.empty(R, dtype=torch.float64, device=dev)
+        plen = _lib.load().pff_reduce_scratch_len()
+        st = stream_handle()
+        while True:
+            act = [i for i, r in enumerate(runs) if not r.done]
+            if not act:
+                break
+            for i in act:
+                runs[i].step_a()
+                r = runs[i]
+                call("pff_dot", r.n, ptr(r.v), ptr(r.w), ptr(partials[i * plen:]), ptr(out[i:]), st)
+            alphas = out.cpu().numpy()
+            for i in act:
+                runs[i].step_b(float(alphas[i]))
+                r = runs[i]
+                call("pff_dot", r.n, ptr(r.w), ptr(r.w), ptr(partials[i * plen:]), ptr(out[i:]), st)
+            norms2 = out.cpu().numpy()
+            for i in act:
+                runs[i].step_c(float(np.sqrt(norms2[i])))
+        res = {}
+        for r in runs:
+            hi = max(r.hi, 1e-30)
+            lo = max(r.lo, cfg.lambda_min_floor * hi)
+            res.setdefault(r.level, {})[r.block] = (lo, hi)
+        return res
 
     # -- linear operator ---------------------------------------------------------
     def apply(self, r):

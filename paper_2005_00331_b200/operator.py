@@ -140,6 +140,7 @@ class LinearizationState:
         self._dir = _Dual(n, bool, False)
         self._flags = None
         self._flags_stamp = None
+        self._bound_key = None
         self._qcache = None
         self._handle = None
         self._version = 0
@@ -249,14 +250,22 @@ class LinearizationState:
             self._flags_stamp = (self._dir.stamp, self._act.stamp)
         return self._flags
 
+    def _bind_key(self):
+        return (self._U.stamp, self._pt.stamp, self._dir.stamp, self._act.stamp,
+                self._U._host_new, self._pt._host_new)
+
     def bind(self):
         """Bind the current device buffers to the level handle; returns it."""
+        key = self._bind_key()
+        if self._handle is not None and self._qcache is not None and key == self._bound_key:
+            return self._handle
         h = self._level_handle()
         if self._qcache is None:
             qlen = _lib.load().pff_level_qcache_len(h)
             self._qcache = torch.empty(qlen, dtype=torch.float64, device=_dev())
         call("pff_level_bind", h, ptr(self._U.device()), ptr(self._pt.device()),
              ptr(self._sync_flags()), ptr(self._qcache))
+        self._bound_key = self._bind_key()
         return h
 
     def device_U(self) -> torch.Tensor:
