@@ -107,6 +107,14 @@ int pff_level_refresh(pff_level* L, void* stream);
 int pff_apply(const pff_level* L, int mode, const double* src, double* dst,
               const double* rhs, void* stream);
 
+/* pff_apply restricted to the owned cell rows [cy_begin, cy_end) of the
+ * level: writes the node rows [p*cy_begin, p*cy_end) (plus the top row / the
+ * slit copies when they fall in the range) and reads node rows
+ * [p*(cy_begin-1), p*cy_end].  Lets a caller pipeline host<->device transfers
+ * of row chunks with the computation.  Q2 sweep levels (>= 64x64 cells) only. */
+int pff_apply_rows(const pff_level* L, int mode, const double* src, double* dst,
+                   const double* rhs, int cy_begin, int cy_end, void* stream);
+
 /* block_diagonal (src/pff_operator.py:305-327 -> src/_kernels.py:700-746):
  * diag_uu (2n), diag_pp (n); constrained entries 1; invert != 0 stores 1/d. */
 int pff_diagonal(const pff_level* L, double* diag_uu, double* diag_pp, int invert,

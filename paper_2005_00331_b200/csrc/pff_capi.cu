@@ -163,6 +163,19 @@ int pff_apply(const pff_level* h, int mode, const double* src, double* dst, cons
     return check(pff::launch_apply(*L, mode, src, dst, rhs, S(stream)), "pff_apply");
 }
 
+int pff_apply_rows(const pff_level* h, int mode, const double* src, double* dst,
+                   const double* rhs, int cy_begin, int cy_end, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_apply_rows: state not bound");
+    if (mode < 0 || mode > 3 || !src || !dst) return fail(PFF_E_ARG, "%s", "pff_apply_rows: bad mode or null vector");
+    bool handled = false;
+    cudaError_t e = pff::launch_sweep_apply_rows(*L, mode, src, dst, rhs, cy_begin, cy_end,
+                                                 S(stream), &handled);
+    if (!handled && e == cudaSuccess)
+        return fail(PFF_E_ARG, "%s", "pff_apply_rows: needs the Q2 sweep kernel (p = 2, >= 64x64 cells)");
+    return check(e, "pff_apply_rows");
+}
+
 int pff_diagonal(const pff_level* h, double* duu, double* dpp, int invert, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_diagonal: state not bound");

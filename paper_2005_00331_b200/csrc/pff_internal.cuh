@@ -104,6 +104,9 @@ void set_sweep_rows_per_chunk(int rows);
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s);
 cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
                                const double* rhs, cudaStream_t s, bool* handled);
+cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src, double* dst,
+                                    const double* rhs, int cy_begin, int cy_end, cudaStream_t s,
+                                    bool* handled);
 
 // operator family (pff_ops.cu)
 cudaError_t launch_refresh(const Level& L, cudaStream_t s);

@@ -848,6 +848,12 @@ cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
 
 cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
                                const double* rhs, cudaStream_t s, bool* handled) {
+    return launch_sweep_apply_rows(L, mode, src, dst, rhs, -1, -1, s, handled);
+}
+
+cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src, double* dst,
+                                    const double* rhs, int cy_begin, int cy_end, cudaStream_t s,
+                                    bool* handled) {
     *handled = false;
     if (!L.sweep_ok()) return cudaSuccess;
     const Mesh& m = L.mesh;
@@ -857,6 +863,12 @@ cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, doub
     a.m = m;
     a.cy_begin = L.cy_begin();
     a.cy_end = L.cy_end();
+    if (cy_begin >= 0) {   // sub-range of the owned cell rows (pipelined host transfers)
+        if (cy_begin < a.cy_begin || cy_end > a.cy_end || cy_begin >= cy_end)
+            return cudaErrorInvalidValue;
+        a.cy_begin = cy_begin;
+        a.cy_end = cy_end;
+    }
     a.q_row0 = L.q_row0();
     a.q_rows = L.q_rows();
     a.dupoff = L.dupoff();

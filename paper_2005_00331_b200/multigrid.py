@@ -158,9 +158,12 @@ class TransferOperator:
         return self._h
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            for h in self._h:
-                _lib._lib.pff_level_destroy(h)
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                for h in self._h:
+                    _lib._lib.pff_level_destroy(h)
+        except Exception:
+            pass
 
     @cached_property
     def P(self) -> sp.csr_matrix:

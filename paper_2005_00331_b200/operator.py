@@ -230,12 +230,12 @@ class LinearizationState:
         return self._handle
 
     def __del__(self):
-        h = getattr(self, "_handle", None)
-        if h is not None and _lib._lib is not None:
-            try:
+        try:
+            h = getattr(self, "_handle", None)
+            if h is not None and _lib._lib is not None:
                 _lib._lib.pff_level_destroy(h)
-            except Exception:
-                pass
+        except Exception:   # interpreter shutdown: modules may already be gone
+            pass
 
     def _sync_flags(self):
         stamp = (self._dir.stamp, self._act.stamp)
@@ -303,8 +303,76 @@ class LinearizationState:
         return dst
 
 
+_PIPE_CHUNKS = 4
+_NC_IN = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 3}
+_NC_OUT = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 1}
+
+
+def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor) -> torch.Tensor:
+    """Host (pinned) -> device -> host application with the transfers of
+    cell-row chunks overlapped with the sweep kernel (pff_apply_rows): H2D of
+    chunk k+1, compute of chunk k and D2H of chunk k-1 run concurrently on
+    three streams.  Same arithmetic as the one-shot path."""
+    dm = state.dof_map
+    n, np1, ng, nd, im = dm.n_scalar, dm.nodes_per_side, dm.n_grid, dm.n_dup, dm.i_mid
+    ns, p = 2 ** state.level, state.hierarchy.degree
+    cin, cout = _NC_IN[mode], _NC_OUT[mode]
+    dev = _dev()
+    h = state.bind()
+    xd = torch.empty(cin * n, dtype=torch.float64, device=dev)
+    yd = torch.empty(cout * n, dtype=torch.float64, device=dev)
+    yh = torch.empty(cout * n, dtype=torch.float64, pin_memory=True)
+    main = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    s_in.wait_stream(main)
+    K = min(_PIPE_CHUNKS, ns)
+    cuts = [k * ns // K for k in range(K + 1)]
+    ev_out = []
+    loaded = -1                      # last node row already on the device
+    dups_in = nd == 0
+    for k in range(K):
+        c0, c1 = cuts[k], cuts[k + 1]
+        hi = min(p * c1 + (1 if c1 < ns else 0), np1 - 1)
+        with torch.cuda.stream(s_in):
+            if hi > loaded:
+                a, b = (loaded + 1) * np1, (hi + 1) * np1
+                for c in range(cin):
+                    xd[c * n + a:c * n + b].copy_(xh[c * n + a:c * n + b], non_blocking=True)
+                loaded = hi
+            if not dups_in and c1 > ns // 2:
+                for c in range(cin):
+                    xd[c * n + ng:(c + 1) * n].copy_(xh[c * n + ng:(c + 1) * n], non_blocking=True)
+                dups_in = True
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+        main.wait_event(ev)
+        call("pff_apply_rows", h, mode, ptr(xd), ptr(yd), None, c0, c1, main.cuda_stream)
+        evc = torch.cuda.Event()
+        evc.record(main)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(evc)
+            a, b = p * c0 * np1, (p * c1 + (1 if c1 == ns else 0)) * np1
+            for c in range(cout):
+                yh[c * n + a:c * n + b].copy_(yd[c * n + a:c * n + b], non_blocking=True)
+            if nd and p * c0 <= im < p * c1 + (1 if c1 == ns else 0):
+                for c in range(cout):
+                    yh[c * n + ng:(c + 1) * n].copy_(yd[c * n + ng:(c + 1) * n], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(s_out)
+            ev_out.append(e)
+    main.wait_stream(s_out)
+    ev_out[-1].synchronize()
+    xd.record_stream(s_in)
+    yd.record_stream(s_out)
+    return yh
+
+
 def _run(state: LinearizationState, mode: int, v, n_in: int, n_out: int):
     state._check_cache()
+    if (isinstance(v, torch.Tensor) and not v.is_cuda and v.is_pinned()
+            and v.dtype == torch.float64 and v.is_contiguous() and v.numel() == n_in
+            and state.hierarchy.degree == 2 and state.level >= 6):
+        return _pipelined(state, mode, v.reshape(-1))
     x, was_np = as_device(v, n_in)
     out = torch.empty(n_out, dtype=torch.float64, device=x.device)
     state.apply_into(mode, x, out)

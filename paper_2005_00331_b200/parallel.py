@@ -233,9 +233,12 @@ class SlabState:
         return self._handle
 
     def __del__(self):
-        h = getattr(self, "_handle", None)
-        if h is not None and _lib._lib is not None:
-            _lib._lib.pff_level_destroy(h)
+        try:
+            h = getattr(self, "_handle", None)
+            if h is not None and _lib._lib is not None:
+                _lib._lib.pff_level_destroy(h)
+        except Exception:
+            pass
 
     def refresh_cache(self):
         call("pff_level_refresh", self.handle(), stream_handle())

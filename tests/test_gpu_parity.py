@@ -294,3 +294,25 @@ def test_sweep_matches_generic_all_modes(generic_apply, split, level, rows):
         y1 = P.apply_jacobian(st, xd)
         y2 = P.apply_jacobian(st, xd)
         assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
+@pytest.mark.parametrize("level", [6, 9])
+def test_pipelined_host_path_matches_device_path(split, level):
+    """apply_* with a pinned host tensor runs the chunked H2D/compute/D2H
+    pipeline (pff_apply_rows); results must equal the device path exactly."""
+    ost, x = O.baseline_state(2, level, split, seed=11)
+    h = P.build_hierarchy(level, 2)
+    st = P.LinearizationState(h, level, ost.params, split=split)
+    st.set_solution(ost.U); st.set_phi_tilde(ost.phi_tilde); st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    n = st.n_scalar
+    xh = torch.from_numpy(x).pin_memory()
+    xd = xh.cuda()
+    for fn, sl in ((P.apply_jacobian, slice(0, 3 * n)), (P.apply_block_uu, slice(0, 2 * n)),
+                   (P.apply_block_phiphi, slice(2 * n, 3 * n)), (P.apply_phi_row, slice(0, 3 * n))):
+        got = fn(st, xh[sl].contiguous().pin_memory())
+        assert not got.is_cuda
+        want = fn(st, xd[sl].contiguous())
+        assert torch.equal(got, want.cpu())
