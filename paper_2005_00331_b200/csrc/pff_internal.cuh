@@ -89,7 +89,7 @@ struct Level {
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
     bool sweep_ok() const { return mesh.p == 2 && mesh.nside >= 64 && q2_struct; }
     int n_strips() const { return (mesh.nside + 30) / 31; }
-    int tile_nq() const { return miehe ? 5 : 4; }
+    int tile_nq() const { return miehe ? 10 : 5; }   // tangent (6 | 1) + coupling (3) + pc
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
     int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
     int64_t qcache_len() const { return generic_len() + tile_len(); }

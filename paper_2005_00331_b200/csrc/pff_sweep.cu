@@ -4,15 +4,18 @@
 // rows/columns of src/pff_operator.py:262-302), without atomics and with the
 // expensive, direction-independent q-point physics hoisted into refresh:
 //
-//  * refresh builds a strip-tiled q-point cache: per (strip, cell row) one
-//    contiguous block [array][q-point][lane].  Miehe: the eigen-frame of the
-//    state strain (m, +-r, c, s; the sign of r carries the pseudo-inverse gap
-//    test of src/_kernels.py:65-69) and pc; none: the strain e and pc.  So the
-//    application does no sqrt and recomputes no state contraction.
+//  * refresh builds a strip-tiled tangent cache: per (strip, cell row) one
+//    contiguous block [array][q-point][lane] holding, with the quadrature
+//    weight w_jq w_iq h^2 folded in, the effective tangent of the reference's
+//    cache_tensors mode (src/_kernels.py:517-548, the solver default of
+//    src/simulation_driver.py:52) as a symmetric 3x3 form (Miehe: 6 arrays;
+//    none: the scalar g(phi~)), the coupling vector dg sigma+ (3) and pc (1).
+//    The application then needs only the direction fields: a q-point costs
+//    ~16 flops of physics instead of re-deriving the split tangent.
 //  * one warp owns a strip of 31 cell columns and sweeps upward over a chunk
 //    of cell rows; lane 0 recomputes the left neighbour cell (halo column),
 //    the first iteration recomputes the cell row below the chunk (halo row);
-//  * node rows of the direction / phi0 / phi~ fields are staged in a 5-row
+//  * node rows of the direction fields are staged in a 5-row
 //    shared-memory ring and the q-point block in a 2-stage buffer, both by
 //    TMA bulk copies (cp.async.bulk + mbarrier) issued one cell row ahead;
 //  * a cell's right node column goes to lane+1 by shuffle, its top node row
@@ -39,25 +42,25 @@ constexpr int RING = 5;                       // node-row ring (3 in use + 2 in 
 constexpr int QK = 9;                         // q-points per Q2 cell
 constexpr int QARR = QK * SW_LANES;           // doubles per q-point array of a block
 
-enum Field { FX = 0, FY, FP, F0P, FPT, NFIELDS };
+enum Field { FX = 0, FY, FP, NFIELDS };
 
+// tangent-cache block: [T (NT arrays)][cw0 cw1 cw2][pc]; the modes read a
+// contiguous sub-range of it
 template <int MODE, bool MIEHE>
 struct Use {
     static constexpr bool ux = MODE != MODE_PHIPHI;
     static constexpr bool ph = MODE != MODE_UU;
-    static constexpr bool p0 = MODE == MODE_FULL || MODE == MODE_PHIROW;
-    static constexpr bool pt = MODE == MODE_FULL || MODE == MODE_UU;
     static constexpr bool DO_UU = MODE == MODE_FULL || MODE == MODE_UU;
     static constexpr bool DO_PP = MODE != MODE_UU;
     static constexpr bool DO_COUP = MODE == MODE_FULL || MODE == MODE_PHIROW;
-    // q-point arrays: the state arrays (tangent) unless none-UU; pc only for PHIPHI
-    static constexpr bool qstate = MODE != MODE_PHIPHI && !(MODE == MODE_UU && !MIEHE);
-    static constexpr bool qpc = MODE == MODE_PHIPHI;
-    static constexpr int NQS = MIEHE ? 4 : 3;          // state arrays in a block
-    static constexpr int NQ = qstate ? NQS : (qpc ? 1 : 0);
-    static constexpr bool used(int f) {
-        return (f == FX || f == FY) ? ux : f == FP ? ph : f == F0P ? p0 : pt;
-    }
+    static constexpr int NT = MIEHE ? 6 : 1;            // tangent arrays
+    static constexpr int NQT = NT + 4;                  // arrays of a block
+    static constexpr int Q0 = MODE == MODE_PHIROW ? NT : MODE == MODE_PHIPHI ? NT + 3 : 0;
+    static constexpr int NQ = MODE == MODE_FULL ? NQT : MODE == MODE_UU ? NT
+                              : MODE == MODE_PHIROW ? 4 : 1;
+    static constexpr int QCW = DO_UU ? NT : 0;          // local index of cw0
+    static constexpr int QPC = NQ - 1;                  // local index of pc
+    static constexpr bool used(int f) { return (f == FX || f == FY) ? ux : ph; }
     static constexpr int slot(int f) {
         int s = 0;
         for (int g = 0; g < f; ++g) s += used(g) ? 1 : 0;
@@ -68,7 +71,7 @@ struct Use {
 
 template <int NF, int NQ, int NRHS>
 struct __align__(16) WarpSmem {
-    double q[2][NQ > 0 ? NQ * QARR : 2];     // q-point blocks, two stages
+    double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
     double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];   // fused rhs of this lane's output nodes
     double v[RING][NF][RW];                  // node-row ring
     uint8_t f[RING][FW];                     // flag rows
@@ -82,19 +85,16 @@ struct SweepConst {
     double N[3][3];    // shape values at the Gauss points (row 1 is (0,1,0))
     double Dh[3][3];   // shape derivatives / h (row 1 is (-1,0,1)/h)
     double ih;         // 1/h
-    double wv[9];      // w_jq w_iq h^2 (src/_kernels.py:613-615 order)
-    double cgw[9];     // gc eps wv
-    double lam, mu2, gdd, omk, kappa, gce;
+    double cgw[9];     // gc eps w_jq w_iq h^2
+    double lam, mu2;
 };
 
 struct SweepArgs {
     SweepConst K;
     Mesh m;
-    Shape S;
-    Material M;
-    const double* fld[NFIELDS];   // ux uy phi (direction), phi0 phit (state)
+    const double* fld[NFIELDS];   // ux uy phi of the direction
     const uint8_t* flags;
-    const double* qtile;          // strip-tiled q-point cache
+    const double* qtile;          // strip-tiled tangent cache
     int64_t qblock;               // doubles per (strip, row) block
     double* dst[3];
     const double* src_out[3];
@@ -195,82 +195,12 @@ __device__ __forceinline__ void miehe_dsig(const Material& M, double g, const Mi
     s12 = g * dp12 + (f12 - dp12);
 }
 
-// Op-minimal form of the same tangent for the sweep kernel (identical maths,
-// rounding differs by a few ulps): the direction-independent part is computed
-// once per q-point, dl2 = tr(de) - dl1 (trace invariance), s = f + (g-1) dp,
-// and sigma+ : de = lambda tr+ tr(de) + 2 mu (l1+ dl1 + l2+ dl2) in the eigenframe.
-struct MieheS {
-    double l1p, l2p, trp, K, c, s, cc, ss, cs, cs2, cms;
-    bool h1, h2, ht;
-};
-__device__ __forceinline__ MieheS miehe_state(double m, double rs, double c, double s) {
-    MieheS q;
-    const double r = fabs(rs);
-    const double ev1 = m + r, ev2 = m - r, tre = 2.0 * m;
-    q.h1 = ev1 >= 0.0;
-    q.h2 = ev2 >= 0.0;
-    q.ht = !(tre < 0.0);
-    q.l1p = posp(ev1);
-    q.l2p = posp(ev2);
-    q.trp = posp(tre);
-    // K = (l1+ - l2+) / gap when the gap test passes: exactly 1 if both eigenvalues
-    // are positive, 0 if none is, a true division only in the mixed case (a zero
-    // numerator would take the slow path of the fp64 division)
-    const bool gap_ok = rs > 0.0;
-    const bool mixed = ev1 > 0.0 && !(ev2 > 0.0);
-    // branch-free reciprocal of the gap: fp32 seed + 3 Newton steps (2^-23 -> 2^-92);
-    // the gap test guarantees gap > 1e-12, well inside the fp32 range
-    const double gap = gap_ok ? ev1 - ev2 : 1.0;
-    double y = (double)__frcp_rn((float)gap);
-    y = y * fma(-gap, y, 2.0);
-    y = y * fma(-gap, y, 2.0);
-    y = y * fma(-gap, y, 2.0);
-    q.K = !gap_ok ? 0.0 : (ev2 > 0.0 ? 1.0 : (mixed ? ev1 * y : 0.0));
-    q.c = c;
-    q.s = s;
-    q.cc = c * c;
-    q.ss = s * s;
-    q.cs = c * s;
-    q.cs2 = 2.0 * q.cs;
-    q.cms = q.cc - q.ss;
-    return q;
-}
-// weighted (x wv) stress increment and sigma+ : de; gm1w = (g - 1) wv
-__device__ __forceinline__ void miehe_apply(double lam, double mu2, const MieheS& q, double gm1w,
-                                            double wv, double d11, double d22, double d12,
-                                            double& s11w, double& s22w, double& s12w,
-                                            double& spde) {
-    const double t0 = fma(d12, q.s, d11 * q.c);
-    const double t1 = fma(d22, q.s, d12 * q.c);
-    const double dl1 = fma(q.s, t1, q.c * t0);
-    const double trde = d11 + d22;
-    const double dl2 = trde - dl1;
-    const double rot = fma(q.c, t1, -(q.s * t0)) * q.K;
-    const double dl1p = q.h1 ? dl1 : 0.0;
-    const double dl2p = q.h2 ? dl2 : 0.0;
-    const double rc = rot * q.cs2;
-    const double o11 = fma(dl1p, q.cc, fma(dl2p, q.ss, -rc));
-    const double o22 = fma(dl1p, q.ss, fma(dl2p, q.cc, rc));
-    const double o12 = fma(dl1p - dl2p, q.cs, rot * q.cms);
-    const double lt = lam * trde;
-    const double ltt = q.ht ? lt : 0.0;
-    s11w = fma(gm1w, fma(mu2, o11, ltt), wv * fma(mu2, d11, lt));
-    s22w = fma(gm1w, fma(mu2, o22, ltt), wv * fma(mu2, d22, lt));
-    s12w = mu2 * fma(gm1w, o12, wv * d12);
-    spde = fma(lam * q.trp, trde, mu2 * fma(q.l1p, dl1, q.l2p * dl2));
-}
-__device__ __forceinline__ double miehe_pc(double lam, double mu, double gdd, double gce,
-                                           const MieheS& q) {
-    const double esp = fma(0.5 * lam * q.trp, q.trp, mu * fma(q.l1p, q.l1p, q.l2p * q.l2p));
-    return fma(gdd, esp, gce);
-}
-
 // ------------------------------------------------------------- tiled refresh
 template <bool MIEHE>
 __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __restrict__ U,
-                                double* __restrict__ qt, int n_strips, int64_t qblock,
-                                int q_row0, int q_rows, int64_t n_local, int64_t row_shift,
-                                int64_t dupoff) {
+                                const double* __restrict__ PT, double* __restrict__ qt,
+                                int n_strips, int64_t qblock, int q_row0, int q_rows,
+                                int64_t n_local, int64_t row_shift, int64_t dupoff) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)n_strips * q_rows * SW_LANES;
     if (t >= total) return;
@@ -279,14 +209,15 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
     const int strip = (int)(blk / q_rows), cy = q_row0 + (int)(blk % q_rows);
     const int cx = strip * SW_OWN - 1 + lane;
     double* out = qt + blk * qblock + lane;
-    constexpr int NQS = MIEHE ? 4 : 3;
+    constexpr int NT = MIEHE ? 6 : 1, NQT = NT + 4;
+    auto put = [&](int arr, int k, double x) { out[(arr * QK + k) * SW_LANES] = x; };
     if (cx < 0 || cx >= m.nside) {
-        for (int a = 0; a <= NQS; ++a)
-            for (int k = 0; k < QK; ++k) out[(a * QK + k) * SW_LANES] = 0.0;
+        for (int a = 0; a < NQT; ++a)
+            for (int k = 0; k < QK; ++k) put(a, k, 0.0);
         return;
     }
     const int64_t n = n_local;
-    double cu[3][3], cv[3][3];
+    double cu[3][3], cv[3][3], cp[3][3], ct[3][3];
 #pragma unroll
     for (int b = 0; b < 3; ++b)
 #pragma unroll
@@ -295,8 +226,10 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
             g = g >= m.n_grid ? dupoff + (g - m.n_grid) - row_shift : g - row_shift;
             cu[b][a] = U[g];
             cv[b][a] = U[n + g];
+            cp[b][a] = U[2 * n + g];
+            ct[b][a] = PT[g];
         }
-    double tx[3][3], td[3][3], gxu[3][3], gyu[3][3], gxv[3][3], gyv[3][3];
+    double tx[3][3], td[3][3], gxu[3][3], gyu[3][3], gxv[3][3], gyv[3][3], p0[3][3], pt[3][3];
     fwd_x<3>(S.N, cu, tx);
     fwd_x<3>(S.D, cu, td);
     fwd_y<3>(S.D, tx, gyu);
@@ -305,36 +238,58 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
     fwd_x<3>(S.D, cv, td);
     fwd_y<3>(S.D, tx, gyv);
     fwd_y<3>(S.N, td, gxv);
-    const double inv_h = 1.0 / m.h, gce = M.gc / M.eps, gdd = 2.0 * (1.0 - M.kappa);
+    fwd_x<3>(S.N, cp, tx);
+    fwd_y<3>(S.N, tx, p0);
+    fwd_x<3>(S.N, ct, tx);
+    fwd_y<3>(S.N, tx, pt);
+    const double h = m.h, inv_h = 1.0 / h, gce = M.gc / M.eps, gdd = 2.0 * (1.0 - M.kappa);
+    const double lam = M.lam, mu = M.mu;
 #pragma unroll
     for (int jq = 0; jq < 3; ++jq)
 #pragma unroll
         for (int iq = 0; iq < 3; ++iq) {
             const int k = jq * 3 + iq;
+            const double wv = S.w[jq] * S.w[iq] * h * h;
             const double e11 = gxu[jq][iq] * inv_h;
             const double e22 = gyv[jq][iq] * inv_h;
             const double e12 = 0.5 * (gyu[jq][iq] + gxv[jq][iq]) * inv_h;
             const double tre = e11 + e22;
-            double esp;
+            const double g = (1.0 - M.kappa) * pt[jq][iq] * pt[jq][iq] + M.kappa;
+            const double dg = gdd * p0[jq][iq];
+            double esp, q11, q22, q12;
             if (MIEHE) {
-                // _eig2s (src/_kernels.py:26-47) and the gap test of _dpos2s (65-69)
+                // the reference's tangent columns for unit directions (src/_kernels.py:519-523)
+                // stored as the symmetric form y = (ds11, ds22, 2 ds12) = T (d11, d22, d12)
                 const double mm = 0.5 * (e11 + e22);
                 const double dh = 0.5 * (e11 - e22);
                 const double r = sqrt(dh * dh + e12 * e12);
                 const Eig e = eig2(e11, e22, e12);
                 const bool gap_ok = (e.ev1 - e.ev2) > 1e-12 * scale2(e11, e22, e12);
-                out[(0 * QK + k) * SW_LANES] = mm;
-                out[(1 * QK + k) * SW_LANES] = gap_ok ? r : -r;
-                out[(2 * QK + k) * SW_LANES] = e.c;
-                out[(3 * QK + k) * SW_LANES] = e.s;
-                esp = esplus2(M.lam, M.mu, tre, e);
+                const MieheQ q = miehe_q(mm, gap_ok ? r : -r, e.c, e.s);
+                double Mc[3][3], sp;
+                miehe_dsig(M, g, q, 1.0, 0.0, 0.0, Mc[0][0], Mc[1][0], Mc[2][0], sp);
+                miehe_dsig(M, g, q, 0.0, 1.0, 0.0, Mc[0][1], Mc[1][1], Mc[2][1], sp);
+                miehe_dsig(M, g, q, 0.0, 0.0, 1.0, Mc[0][2], Mc[1][2], Mc[2][2], sp);
+                put(0, k, wv * Mc[0][0]);
+                put(1, k, wv * 0.5 * (Mc[0][1] + Mc[1][0]));
+                put(2, k, wv * 0.5 * (Mc[0][2] + 2.0 * Mc[2][0]));
+                put(3, k, wv * Mc[1][1]);
+                put(4, k, wv * 0.5 * (Mc[1][2] + 2.0 * Mc[2][1]));
+                put(5, k, wv * 2.0 * Mc[2][2]);
+                sigplus2(lam, mu, tre, e, q11, q22, q12);
+                esp = esplus2(lam, mu, tre, e);
             } else {
-                out[(0 * QK + k) * SW_LANES] = e11;
-                out[(1 * QK + k) * SW_LANES] = e22;
-                out[(2 * QK + k) * SW_LANES] = e12;
-                esp = 0.5 * M.lam * tre * tre + M.mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
+                put(0, k, wv * g);
+                q11 = lam * tre + 2.0 * mu * e11;
+                q22 = lam * tre + 2.0 * mu * e22;
+                q12 = 2.0 * mu * e12;
+                esp = 0.5 * lam * tre * tre + mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
             }
-            out[(NQS * QK + k) * SW_LANES] = gdd * esp + gce;
+            // coupling dg sigma+ : de (src/_kernels.py:633-635) and pc, weighted
+            put(NT + 0, k, wv * dg * q11);
+            put(NT + 1, k, wv * dg * q22);
+            put(NT + 2, k, wv * dg * 2.0 * q12);
+            put(NT + 3, k, wv * (gdd * esp + gce));
         }
 }
 
@@ -354,11 +309,6 @@ k_sweep_q2(const SweepArgs A) {
     const int ns = m.nside;
     const int64_t np1 = m.np1;
     const int half = ns >> 1;
-    const Shape& S = A.S;
-    const Material& M = A.M;
-    const double h = m.h, inv_h = 1.0 / h;
-    // q-point array offset inside a (strip,row) block
-    const int qarr0 = U::qpc ? U::NQS : 0;
 
     if (lane == 0) {
         mbar_init(&W.bar[0]);
@@ -403,9 +353,8 @@ k_sweep_q2(const SweepArgs A) {
             return bytes + (unsigned)(b - a);
         };
         auto issue_qblock = [&](int cy, int stage) -> unsigned {
-            if (NQ == 0) return 0u;
             const double* src =
-                A.qtile + ((int64_t)strip * A.q_rows + (cy - A.q_row0)) * A.qblock + qarr0 * QARR;
+                A.qtile + ((int64_t)strip * A.q_rows + (cy - A.q_row0)) * A.qblock + U::Q0 * QARR;
             bulk_g2s(W.q[stage], src, (unsigned)(NQ * QARR * 8), &W.bar[stage]);
             return (unsigned)(NQ * QARR * 8);
         };
@@ -546,7 +495,7 @@ k_sweep_q2(const SweepArgs A) {
                     return sD * fma(K.Dh[0][2], g(f, b, 2),
                                     fma(K.Dh[0][1], g(f, b, 1), K.Dh[0][0] * g(f, b, 0)));
                 };
-                double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3], X0p[3], Xt[3];
+                double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3];
 #pragma unroll
                 for (int b = 0; b < 3; ++b) {
                     if (U::ux) {
@@ -554,8 +503,6 @@ k_sweep_q2(const SweepArgs A) {
                         XyN[b] = xN(FY, b); XyD[b] = xD(FY, b);
                     }
                     if (U::ph) { XpN[b] = xN(FP, b); XpD[b] = xD(FP, b); }
-                    if (U::p0) X0p[b] = xN(F0P, b);
-                    if (U::pt) Xt[b] = xN(FPT, b);
                 }
                 double Tu1[3] = {}, Tu2[3] = {}, Tv1[3] = {}, Tv2[3] = {}, Tp1[3] = {}, Tp2[3] = {};
 #pragma unroll
@@ -569,63 +516,35 @@ k_sweep_q2(const SweepArgs A) {
                         return fma(K.Dh[jq][2], X[2], fma(K.Dh[jq][1], X[1], K.Dh[jq][0] * X[0]));
                     };
                     const int k = jq * 3 + iq;
-                    const double wv = K.wv[jq * 3 + ic];
-                    double s11 = 0.0, s22 = 0.0, s12 = 0.0, spde = 0.0, pc = 0.0;
-                    if (MIEHE) {
-                        MieheS q{};
-                        if (U::qstate) q = miehe_state(qv(0, k), qv(1, k), qv(2, k), qv(3, k));
-                        if (U::ux) {
-                            const double d11 = yN(XxD);
-                            const double d22 = yD(XyN);
-                            const double d12 = 0.5 * (yD(XxN) + yN(XyD));
-                            double gm1w = -wv;   // (g - 1) wv with g = 1 when unused
-                            if (U::pt) {
-                                const double pt = yN(Xt);
-                                gm1w = (fma(K.omk * pt, pt, K.kappa) - 1.0) * wv;
-                            }
-                            miehe_apply(K.lam, K.mu2, q, gm1w, wv, d11, d22, d12, s11, s22, s12,
-                                        spde);
-                        }
-                        if (U::DO_PP)
-                            pc = U::qpc ? qv(0, k) : miehe_pc(M.lam, M.mu, K.gdd, K.gce, q);
-                    } else {
-                        double e11 = 0.0, e22 = 0.0, e12 = 0.0;
-                        if (U::qstate) { e11 = qv(0, k); e22 = qv(1, k); e12 = qv(2, k); }
-                        if (U::ux) {
-                            const double d11 = yN(XxD);
-                            const double d22 = yD(XyN);
-                            const double d12 = 0.5 * (yD(XxN) + yN(XyD));
-                            double gw = wv;
-                            if (U::pt) {
-                                const double pt = yN(Xt);
-                                gw = fma(K.omk * pt, pt, K.kappa) * wv;
-                            }
+                    // weighted stress increment s = C de (cache_tensors form,
+                    // src/_kernels.py:624-635) and phi-row terms
+                    double s11 = 0.0, s22 = 0.0, s12 = 0.0, d11 = 0.0, d22 = 0.0, d12 = 0.0;
+                    if (U::ux) {
+                        d11 = yN(XxD);
+                        d22 = yD(XyN);
+                        d12 = 0.5 * (yD(XxN) + yN(XyD));
+                    }
+                    if (U::DO_UU) {
+                        if (MIEHE) {
+                            const double t00 = qv(0, k), t01 = qv(1, k), t02 = qv(2, k);
+                            const double t11 = qv(3, k), t12 = qv(4, k), t22 = qv(5, k);
+                            s11 = fma(t00, d11, fma(t01, d22, t02 * d12));
+                            s22 = fma(t01, d11, fma(t11, d22, t12 * d12));
+                            s12 = 0.5 * fma(t02, d11, fma(t12, d22, t22 * d12));
+                        } else {
+                            const double gw = qv(0, k);
                             const double lt = K.lam * (d11 + d22);
                             s11 = gw * fma(K.mu2, d11, lt);
                             s22 = gw * fma(K.mu2, d22, lt);
                             s12 = (gw * K.mu2) * d12;
-                            if (U::DO_COUP) {
-                                const double ltr = K.lam * (e11 + e22);
-                                spde = fma(fma(K.mu2, e11, ltr), d11,
-                                           fma(fma(K.mu2, e22, ltr), d22, (2.0 * K.mu2 * e12) * d12));
-                            }
-                        }
-                        if (U::DO_PP) {
-                            if (U::qpc) {
-                                pc = qv(0, k);
-                            } else {
-                                const double tre = e11 + e22;
-                                const double esp = fma(0.5 * M.lam * tre, tre,
-                                                       M.mu * fma(e11, e11, fma(e22, e22, 2.0 * e12 * e12)));
-                                pc = fma(K.gdd, esp, K.gce);
-                            }
                         }
                     }
                     double fv = 0.0, fgx = 0.0, fgy = 0.0;
                     if (U::DO_PP) {
-                        double pval = pc * yN(XpN);
-                        if (U::DO_COUP) pval = fma(K.gdd * yN(X0p), spde, pval);
-                        fv = pval * wv;
+                        fv = qv(U::QPC, k) * yN(XpN);
+                        if (U::DO_COUP)
+                            fv = fma(qv(U::QCW, k), d11,
+                                     fma(qv(U::QCW + 1, k), d22, fma(qv(U::QCW + 2, k), d12, fv)));
                         fgx = K.cgw[jq * 3 + ic] * yN(XpD);
                         fgy = K.cgw[jq * 3 + ic] * yD(XpN);
                     }
@@ -697,17 +616,8 @@ k_sweep_q2(const SweepArgs A) {
             using I0 = std::integral_constant<int, 0>;
             using I1 = std::integral_constant<int, 1>;
             column(std::true_type{}, I0{});
-            // the Miehe FULL body is large enough to thrash the instruction cache:
-            // there the two outer columns run as one rolled, runtime-mirrored body;
-            // elsewhere they are unrolled (the mirror then folds into constants)
-            constexpr bool COMPACT = MIEHE && MODE == MODE_FULL;
-            if constexpr (COMPACT) {
-#pragma unroll 1
-                for (int side = 0; side < 2; ++side) column(std::false_type{}, side);
-            } else {
-                column(std::false_type{}, I0{});
-                column(std::false_type{}, I1{});
-            }
+            column(std::false_type{}, I0{});
+            column(std::false_type{}, I1{});
             if (!active) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
@@ -835,11 +745,11 @@ cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
     const int64_t total = (int64_t)L.n_strips() * L.q_rows() * SW_LANES;
     const unsigned grid = (unsigned)((total + 127) / 128);
     if (L.miehe)
-        k_refresh_tiled<true><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.qtile(), L.n_strips(),
+        k_refresh_tiled<true><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.phi_tilde, L.qtile(), L.n_strips(),
                                                    L.tile_block(), L.q_row0(), L.q_rows(),
                                                    L.local_n(), L.row_shift(), L.dupoff());
     else
-        k_refresh_tiled<false><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.qtile(), L.n_strips(),
+        k_refresh_tiled<false><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.phi_tilde, L.qtile(), L.n_strips(),
                                                     L.tile_block(), L.q_row0(), L.q_rows(),
                                                     L.local_n(), L.row_shift(), L.dupoff());
     count_launches(1);
@@ -872,8 +782,6 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
     a.q_row0 = L.q_row0();
     a.q_rows = L.q_rows();
     a.dupoff = L.dupoff();
-    a.S = L.shape;
-    a.M = L.mat;
     {
         SweepConst& K = a.K;
         const double h = m.h, ih = 1.0 / h;
@@ -886,15 +794,10 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         for (int jq = 0; jq < 3; ++jq)
             for (int iq = 0; iq < 3; ++iq) {
                 const double wq = L.shape.w[jq] * L.shape.w[iq];
-                K.wv[jq * 3 + iq] = wq * h * h;
-                K.cgw[jq * 3 + iq] = L.mat.gc * L.mat.eps * K.wv[jq * 3 + iq];
+                K.cgw[jq * 3 + iq] = L.mat.gc * L.mat.eps * (wq * h * h);
             }
         K.lam = L.mat.lam;
         K.mu2 = 2.0 * L.mat.mu;
-        K.gdd = 2.0 * (1.0 - L.mat.kappa);
-        K.omk = 1.0 - L.mat.kappa;
-        K.kappa = L.mat.kappa;
-        K.gce = L.mat.gc / L.mat.eps;
     }
     for (int f = 0; f < NFIELDS; ++f) a.fld[f] = nullptr;
     switch (mode) {
@@ -907,8 +810,6 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
             a.fld[FP] = src - sh; break;
         default: return cudaErrorInvalidValue;
     }
-    a.fld[F0P] = L.U + 2 * n - sh;
-    a.fld[FPT] = L.phi_tilde - sh;
     a.flags = L.flags - sh;
     a.qtile = L.qtile();
     a.qblock = L.tile_block();
