@@ -124,6 +124,19 @@ int pff_diagonal(const pff_level* L, double* diag_uu, double* diag_pp, int inver
 int pff_residual(const pff_level* L, double* out, int mask_dirichlet, int mask_active,
                  void* stream);
 
+/* lumped phi mass diagonal (src/active_set_solver.py:60-69 -> src/_kernels.py:828-843):
+ * row sums of the scalar mass matrix over the level's local nodes; bitwise the
+ * reference's summation order.  Needs no bound state. */
+int pff_lumped_mass(const pff_level* L, double* out, void* stream);
+
+/* one complementarity pass of the active-set loop (src/active_set_solver.py:72-82,
+ * 113-118): active[i] = rhs_phi[i]/m[i] + c (phi[i] - phi_old[i]) > 0; freshly
+ * activated dofs with phi != phi_old are reset to phi_old IN PLACE; stats (3
+ * uint64, device) = {|A|, reset dofs, |A xor prev|} (prev may be NULL). */
+int pff_active_set(int64_t n, const double* rhs_phi, double* phi, const double* phi_old,
+                   const double* m_diag, double c, const uint8_t* prev, uint8_t* active,
+                   uint64_t* stats, void* stream);
+
 /* TransferOperator (src/multigrid.py:97-120) between fine = coarse + 1.
  * A windowed fine level (slab) transfers its OWNED fine nodes only: restrict
  * accumulates their P^T contributions into the whole-mesh coarse vector (sum

@@ -720,3 +720,90 @@ def notch_phase(lv: Level, eps: float) -> np.ndarray:
     dx = np.maximum(x - 0.5, 0.0)
     d = np.sqrt(dx * dx + (y - 0.5) ** 2)
     return 1.0 - np.exp(-d / eps)
+
+
+# ------------------------------------------------------- active-set loop
+# src/simulation_driver.py:116-148 (boundary data) and
+# src/active_set_solver.py:31-163 (PDAS loop)
+
+def boundary_program(scenario: str, t: float, du: float = 1e-5) -> dict:
+    """src/simulation_driver.py:116-131."""
+    if t < 0:
+        raise ValueError("time must be nonnegative")
+    if scenario == "tension":
+        return {("top", 0): 0.0, ("top", 1): t * du, ("bottom", 0): 0.0, ("bottom", 1): 0.0}
+    if scenario == "shear":
+        return {("top", 0): t * du, ("top", 1): 0.0, ("bottom", 0): 0.0, ("bottom", 1): 0.0}
+    raise ValueError(f"unknown scenario {scenario!r}")
+
+
+def apply_boundary_values(st: State, values: dict) -> None:
+    """src/simulation_driver.py:134-145."""
+    n = st.n
+    nodes_all = []
+    for (tag, comp), val in values.items():
+        nodes = st.lv.boundary_nodes(tag)
+        st.U[comp * n + nodes] = val
+        nodes_all.append(nodes)
+    st.dirichlet = np.zeros(n, dtype=bool)
+    st.dirichlet[np.unique(np.concatenate(nodes_all))] = True
+    st.cache = None
+
+
+class SolverFailure(RuntimeError):
+    pass
+
+
+@dataclass
+class ActiveSetReport:
+    as_iterations: int = 0
+    gmres_iterations: list = field(default_factory=list)
+    active_counts: list = field(default_factory=list)
+    residual_norms: list = field(default_factory=list)
+    r0_norm: float = 0.0
+    converged: bool = False
+
+
+def active_set_solve_step(st: State, gmg: Gmg, m_diag, c=100.0, tol=1e-8, max_iterations=50,
+                          lin_tol=1e-6, lin_max=1000, restart=100, nthreads=1) -> ActiveSetReport:
+    """src/active_set_solver.py:101-163 (ActiveSetSolver.solve_step)."""
+    rep = ActiveSetReport()
+    n = st.n
+    prev = None
+    for k in range(max_iterations):
+        rhs = -residual(st, nthreads=nthreads)
+        active = determine_active_set(rhs, st.U, st.phi_old, m_diag, c)
+        moved = active & (st.U[2 * n:] != st.phi_old)
+        if np.any(moved):
+            st.U[2 * n:][moved] = st.phi_old[moved]
+            rhs = -residual(st, nthreads=nthreads)
+        st.active = active
+        st.cache = None
+        rhs[2 * n:][active] = 0.0
+        r_norm = float(np.linalg.norm(rhs))
+        if k == 0:
+            rep.r0_norm = max(r_norm, 1e-300)
+        rep.active_counts.append(int(active.sum()))
+        rep.residual_norms.append(r_norm)
+        if prev is not None and np.array_equal(active, prev) and r_norm <= tol * rep.r0_norm:
+            rep.converged = True
+            break
+        st.refresh_cache(nthreads)
+        reuse = prev is not None and np.array_equal(active, prev)
+        gmg.setup(st, reuse_eigen=reuse)
+        A = lambda v: apply_jacobian(st, v, nthreads)  # noqa: E731
+        res = gmres(A, rhs, tol=lin_tol, max_iterations=lin_max, restart=restart,
+                    preconditioner=gmg.apply)
+        if not res.converged:
+            res = gmres(A, rhs, tol=lin_tol, max_iterations=2 * lin_max, restart=restart,
+                        preconditioner=gmg.apply, x0=res.solution)
+            if not res.converged:
+                raise SolverFailure(f"linear solve stagnated at active-set iteration {k}")
+        st.U = st.U + res.solution
+        st.cache = None
+        rep.gmres_iterations.append(res.iterations)
+        rep.as_iterations = k + 1
+        prev = active
+    else:
+        raise SolverFailure(f"active-set loop did not converge within {max_iterations} iterations")
+    return rep

@@ -6,6 +6,8 @@ sm_100a CUDA kernels in ``libpff_b200.so`` (C ABI: include/pff_b200.h).
 """
 
 from ._lib import PffError
+from .active_set import (ActiveSetParams, ActiveSetSolver, SolveReport, SolverFailure,
+                         converged, determine_active_set, lumped_mass_diagonal)
 from .basis import LANE_WIDTHS, MaterialParams, ShapeData, shape_data
 from .krylov import GmresResult, KrylovConfig, gmres_solve
 from .mesh import DofMap, MeshHierarchy, MeshLevel, build_hierarchy
@@ -15,5 +17,7 @@ from .multigrid import (ChebyshevConfig, GmgPreconditioner, TransferOperator,
 from .operator import (JacobianOperator, LinearizationState, StaleCacheError,
                        apply_block_phiphi, apply_block_uu, apply_jacobian, apply_phi_row,
                        block_diagonal, block_diagonals, residual, restrict_state_to_level)
+
+from .simulation import apply_boundary_values, boundary_program, reaction_load
 
 __version__ = "0.1.0"

@@ -191,6 +191,23 @@ int pff_residual(const pff_level* h, double* out, int md, int ma, void* stream) 
     return check(pff::launch_residual(*L, out, md, ma, S(stream)), "pff_residual");
 }
 
+int pff_lumped_mass(const pff_level* h, double* out, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!L || !out) return fail(PFF_E_ARG, "%s", "pff_lumped_mass: null argument");
+    return check(pff::launch_lumped_mass(*L, out, S(stream)), "pff_lumped_mass");
+}
+
+int pff_active_set(int64_t n, const double* rhs_phi, double* phi, const double* phi_old,
+                   const double* m_diag, double c, const uint8_t* prev, uint8_t* active,
+                   uint64_t* stats, void* stream) {
+    if (n < 0 || (n > 0 && (!rhs_phi || !phi || !phi_old || !m_diag || !active)) || !stats)
+        return fail(PFF_E_ARG, "%s", "pff_active_set: bad argument");
+    if (!(c > 0.0)) return fail(PFF_E_ARG, "%s", "pff_active_set: complementarity constant must be positive");
+    return check(pff::launch_active_set(n, rhs_phi, phi, phi_old, m_diag, c, prev, active,
+                                        reinterpret_cast<unsigned long long*>(stats), S(stream)),
+                 "pff_active_set");
+}
+
 int pff_prolongate(const pff_level* f, const pff_level* c, const double* xc, double* yf,
                    int add_masked, void* stream) {
     const Level* F = reinterpret_cast<const Level*>(f);

@@ -117,6 +117,13 @@ cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, 
 cudaError_t launch_residual(const Level& L, double* out, int mask_dirichlet, int mask_active,
                             cudaStream_t s);
 
+// active-set loop (pff_active.cu)
+cudaError_t launch_lumped_mass(const Level& L, double* out, cudaStream_t s);
+cudaError_t launch_active_set(int64_t n, const double* rhs_phi, double* phi,
+                              const double* phi_old, const double* m_diag, double c,
+                              const uint8_t* prev, uint8_t* active, unsigned long long* stats,
+                              cudaStream_t s);
+
 // transfers (pff_transfer.cu)
 cudaError_t launch_prolongate(const Level& fine, const Level& coarse, const double* xc,
                               double* yf, int add_masked, cudaStream_t s);

@@ -274,6 +274,26 @@ class LinearizationState:
     def device_flags(self) -> torch.Tensor:
         return self._sync_flags()
 
+    def device_phi_old(self) -> torch.Tensor:
+        return self._po.device()
+
+    def touch_solution(self):
+        """The device copy of U was modified in place (a kernel wrote it):
+        the host mirror is stale and the version moves on."""
+        self._U.device()
+        self._U._host_new, self._U._dev_new = False, True
+        self._U.stamp += 1
+        self._version += 1
+
+    def add_to_solution(self, dU):
+        """U += dU on the device (state.set_solution(state.U + dU) without
+        the host round trip)."""
+        n3 = 3 * self.n_scalar
+        d, _ = as_device(dU, n3)
+        U = self._U.device()
+        call("pff_axpby", n3, 1.0, ptr(d), 1.0, ptr(U), stream_handle())
+        self.touch_solution()
+
     def refresh_cache(self):
         call("pff_level_refresh", self.bind(), stream_handle())
         self._cache_version = self._version

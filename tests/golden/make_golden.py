@@ -31,7 +31,9 @@ from fracturekit.mesh_hierarchy import build_hierarchy  # noqa: E402
 from fracturekit.multigrid import (ChebyshevConfig, GmgPreconditioner,  # noqa: E402
                                    TransferOperator, chebyshev_apply,
                                    estimate_lambda_range)
-from fracturekit.active_set_solver import lumped_mass_diagonal  # noqa: E402
+from fracturekit.active_set_solver import (ActiveSetParams, ActiveSetSolver,  # noqa: E402
+                                           lumped_mass_diagonal)
+from fracturekit.simulation_driver import apply_boundary_values, boundary_program  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -142,8 +144,59 @@ def restrict_case(p, level, target, seed):
     return d
 
 
+def activeset_case(p, level, split, t, du, notch_phi, baseline_material):
+    """One ActiveSetSolver.solve_step (src/active_set_solver.py:101-163) from a
+    tension load step; the reference tests' default material, or the BASELINE
+    material with a pre-cracked (notch) phase field."""
+    h = build_hierarchy(level, p)
+    prm = params(level) if baseline_material else MaterialParams()
+    st = op.LinearizationState(h, level, prm, split=split)
+    n = st.n_scalar
+    if notch_phi:
+        phi0 = notch(h.dof_map(level), prm.eps)
+        U = st.U.copy()
+        U[2 * n:] = phi0
+        st.set_solution(U)
+        st.set_phi_tilde(phi0)
+        st.set_phi_old(phi0)
+    apply_boundary_values(st, boundary_program("tension", t, du))
+    d = dict(U0=st.U.copy(), phi_tilde=st.phi_tilde.copy(), phi_old=st.phi_old.copy(),
+             dirichlet=st.dirichlet_nodes.copy())
+    m = lumped_mass_diagonal(h, level)
+    gmg = GmgPreconditioner(h, coarse_level=2)
+    solver = ActiveSetSolver(gmg, KrylovConfig(), ActiveSetParams(), m)
+    rep = solver.solve_step(st)
+    d.update(m=m, U=st.U.copy(), active=st.active.copy(),
+             as_iterations=np.array([rep.as_iterations]),
+             gmres_iterations=np.array(rep.gmres_iterations),
+             active_counts=np.array(rep.active_counts),
+             residual_norms=np.array(rep.residual_norms),
+             converged=np.array([int(rep.converged)]),
+             material=np.array([prm.lame_lambda, prm.mu, prm.g_c, prm.kappa, prm.eps]),
+             meta=np.array([p, level, 1 if split == "miehe" else 0, int(notch_phi)]),
+             load=np.array([t, du]))
+    print(f"activeset p{p} l{level} {split}: as {rep.as_iterations} gmres {rep.gmres_iterations}"
+          f" active {rep.active_counts}")
+    return d
+
+
+ACTIVESET = {
+    "as_p1_l3_miehe_t40": (1, 3, "miehe", 40.0, 1e-5, False, False),
+    "as_p1_l4_miehe_t1": (1, 4, "miehe", 1.0, 1e-5, False, False),
+    "as_p2_l4_miehe_notch": (2, 4, "miehe", 1.0, 3e-3, True, True),
+    "as_p2_l6_none_notch": (2, 6, "none", 1.0, 3e-3, True, True),
+    "as_p2_l6_miehe_notch": (2, 6, "miehe", 1.0, 3e-3, True, True),
+}
+
+
 def main():
+    if "--activeset" in sys.argv:   # only the active-set fixtures
+        for name, args in ACTIVESET.items():
+            np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **activeset_case(*args))
+        return
     cases = {}
+    for name, args in ACTIVESET.items():
+        cases[name] = activeset_case(*args)
     for split in ("none", "miehe"):
         cases[f"pr1_{split}"] = operator_case(2, 5, split, 0, with_cache=True)
         for p in (1, 3, 4):
