@@ -16,8 +16,9 @@ from .multigrid import (ChebyshevConfig, GmgPreconditioner, TransferOperator,
                         estimate_lambda_range)
 from .operator import (JacobianOperator, LinearizationState, StaleCacheError,
                        apply_block_phiphi, apply_block_uu, apply_jacobian, apply_phi_row,
-                       block_diagonal, block_diagonals, residual, restrict_state_to_level)
+                       block_diagonal, block_diagonals, extrapolate_phase, residual, restrict_state_to_level)
 
-from .simulation import apply_boundary_values, boundary_program, reaction_load
+from .simulation import (LoadRecord, ScenarioConfig, SimulationResult, apply_boundary_values,
+                         boundary_program, reaction_load, run_simulation)
 
 __version__ = "0.1.0"

@@ -4,8 +4,11 @@
 //
 // Generic path (any p in 1..4): one thread per cell, sum-factorised 1-D
 // contractions in registers, q-point physics restated from
-// src/_kernels.py:555-693, scatter by fp64 atomics into a vector whose
-// constrained rows were initialised first (identity rows/columns,
+// src/_kernels.py:555-693.  Cells are processed in four colour passes
+// (cx mod 2, cy mod 2): cells of one colour share no node, so each pass adds
+// into the output with plain read-modify-writes -- no atomics, and the
+// summation order per node is fixed (deterministic results run to run).  The
+// output's constrained rows are initialised first (identity rows/columns,
 // src/pff_operator.py:262-302).  The Q2 fast path lives in pff_sweep.cu.
 #include "pff_internal.cuh"
 
@@ -18,6 +21,24 @@ constexpr int CELL_THREADS = 128;
 inline unsigned grid_for(int64_t n, int threads) {
     return (unsigned)((n + threads - 1) / threads);
 }
+
+// One colour class of the cells in rows [row0, row0 + rows): colour bit 0 is
+// the parity of cx, bit 1 the parity of cy.
+struct Colour {
+    int c, hx, hy, cy0;
+    __host__ __device__ Colour(int colour, int ns, int row0, int rows) : c(colour) {
+        hx = (ns - (colour & 1) + 1) >> 1;
+        cy0 = row0 + (((row0 & 1) != (colour >> 1)) ? 1 : 0);
+        const int left = row0 + rows - cy0;
+        hy = left > 0 ? (left + 1) >> 1 : 0;
+        if (hx < 0) hx = 0;
+    }
+    __host__ __device__ int64_t count() const { return (int64_t)hx * hy; }
+    __device__ void cell(int64_t t, int& cx, int& cy) const {
+        cx = (c & 1) + 2 * (int)(t % hx);
+        cy = cy0 + 2 * (int)(t / hx);
+    }
+};
 
 template <int N1>
 __device__ __forceinline__ void cell_ids(const Mesh& m, int cx, int cy, int64_t (&gid)[N1][N1]) {
@@ -140,13 +161,15 @@ __global__ void __launch_bounds__(CELL_THREADS)
 k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
               const uint8_t* __restrict__ flags, const double* __restrict__ sx,
               const double* __restrict__ sy, const double* __restrict__ sp, double* dx,
-              double* dy, double* dp, double sign) {
+              double* dy, double* dp, double sign, Colour col) {
     using T = ModeTraits<MODE>;
     constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t nc = m.n_cells();
-    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= nc) return;
-    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= col.count()) return;
+    int cx, cy;
+    col.cell(tid, cx, cy);
+    const int64_t cell = (int64_t)cy * m.nside + cx;
     int64_t gid[N1][N1];
     uint8_t fl[N1][N1];
     cell_ids<N1>(m, cx, cy, gid);
@@ -233,8 +256,8 @@ k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
 #pragma unroll
             for (int a = 0; a < N1; ++a)
                 if (!(fl[b][a] & F_DIR)) {
-                    atomicAdd(dx + gid[b][a], sign * ru[b][a]);
-                    atomicAdd(dy + gid[b][a], sign * rv[b][a]);
+                    dx[gid[b][a]] += sign * ru[b][a];
+                    dy[gid[b][a]] += sign * rv[b][a];
                 }
     }
     if (T::DO_PP) {
@@ -249,7 +272,7 @@ k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
         for (int b = 0; b < N1; ++b)
 #pragma unroll
             for (int a = 0; a < N1; ++a)
-                if (!(fl[b][a] & F_ACT)) atomicAdd(dp + gid[b][a], sign * rp[b][a]);
+                if (!(fl[b][a] & F_ACT)) dp[gid[b][a]] += sign * rp[b][a];
     }
 }
 
@@ -259,12 +282,14 @@ k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
 template <int P, bool MIEHE>
 __global__ void __launch_bounds__(CELL_THREADS)
 k_diag_cells(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc, double* dx,
-             double* dy, double* dp) {
+             double* dy, double* dp, Colour col) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t nc = w.ncell;
-    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= nc) return;
-    int cx = (int)(cell % m.nside), cy = w.row0 + (int)(cell / m.nside);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= col.count()) return;
+    int cx, cy;
+    col.cell(tid, cx, cy);
+    const int64_t cell = (int64_t)(cy - w.row0) * m.nside + cx;
     const double h = m.h, inv_h = 1.0 / h;
     const int64_t fs = (int64_t)QQ * nc;
     double ax[N1][N1] = {}, ay[N1][N1] = {}, ap[N1][N1] = {};
@@ -312,9 +337,9 @@ k_diag_cells(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc, 
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
             int64_t g = w.loc(m, m.node(cx, cy, a, b));
-            atomicAdd(dx + g, ax[b][a]);
-            atomicAdd(dy + g, ay[b][a]);
-            atomicAdd(dp + g, ap[b][a]);
+            dx[g] += ax[b][a];
+            dy[g] += ay[b][a];
+            dp[g] += ap[b][a];
         }
 }
 
@@ -342,12 +367,12 @@ __global__ void k_diag_finalize(int64_t n, const uint8_t* __restrict__ flags, do
 template <int P, bool MIEHE>
 __global__ void __launch_bounds__(CELL_THREADS)
 k_residual_cells(Mesh m, Shape S, Material M, const double* __restrict__ U,
-                 const double* __restrict__ pt, double* out) {
+                 const double* __restrict__ pt, double* out, Colour col) {
     constexpr int N1 = P + 1;
-    const int64_t nc = m.n_cells();
-    int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= nc) return;
-    int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= col.count()) return;
+    int cx, cy;
+    col.cell(tid, cx, cy);
     const int64_t n = m.n;
     int64_t gid[N1][N1];
     cell_ids<N1>(m, cx, cy, gid);
@@ -427,9 +452,9 @@ k_residual_cells(Mesh m, Shape S, Material M, const double* __restrict__ U,
     for (int b = 0; b < N1; ++b)
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
-            atomicAdd(out + gid[b][a], ru[b][a]);
-            atomicAdd(out + n + gid[b][a], rv[b][a]);
-            atomicAdd(out + 2 * n + gid[b][a], rp[b][a]);
+            out[gid[b][a]] += ru[b][a];
+            out[n + gid[b][a]] += rv[b][a];
+            out[2 * n + gid[b][a]] += rp[b][a];
         }
 }
 
@@ -479,39 +504,46 @@ struct ApplyL {
                            const double* rhs, cudaStream_t s) {
         const Mesh& m = L->mesh;
         const int64_t n = m.n;
-        const unsigned gi = grid_for(n, 256), gc = grid_for(m.n_cells(), CELL_THREADS);
+        const unsigned gi = grid_for(n, 256);
         const double sign = rhs ? -1.0 : 1.0;
         const double* q = L->qcache;
         const uint8_t* f = L->flags;
         switch (mode) {
-            case MODE_FULL:
-                k_apply_init<MODE_FULL><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
-                k_apply_cells<P, MIEHE, MODE_FULL><<<gc, CELL_THREADS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, dst, dst + n,
-                    dst + 2 * n, sign);
-                break;
-            case MODE_UU:
-                k_apply_init<MODE_UU><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
-                k_apply_cells<P, MIEHE, MODE_UU><<<gc, CELL_THREADS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, src, src + n, nullptr, dst, dst + n, nullptr,
-                    sign);
-                break;
-            case MODE_PHIPHI:
-                k_apply_init<MODE_PHIPHI><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
-                k_apply_cells<P, MIEHE, MODE_PHIPHI><<<gc, CELL_THREADS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, nullptr, nullptr, src, nullptr, nullptr, dst,
-                    sign);
-                break;
-            case MODE_PHIROW:
-                k_apply_init<MODE_PHIROW><<<gi, 256, 0, s>>>(n, f, src, rhs, dst);
-                k_apply_cells<P, MIEHE, MODE_PHIROW><<<gc, CELL_THREADS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, nullptr, nullptr, dst,
-                    sign);
-                break;
-            default:
-                return cudaErrorInvalidValue;
+            case MODE_FULL: k_apply_init<MODE_FULL><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
+            case MODE_UU: k_apply_init<MODE_UU><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
+            case MODE_PHIPHI: k_apply_init<MODE_PHIPHI><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
+            case MODE_PHIROW: k_apply_init<MODE_PHIROW><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
+            default: return cudaErrorInvalidValue;
         }
-        count_launches(2);
+        count_launches(1);
+        for (int c = 0; c < 4; ++c) {
+            const Colour col(c, m.nside, 0, m.nside);
+            if (col.count() == 0) continue;
+            const unsigned gc = grid_for(col.count(), CELL_THREADS);
+            switch (mode) {
+                case MODE_FULL:
+                    k_apply_cells<P, MIEHE, MODE_FULL><<<gc, CELL_THREADS, 0, s>>>(
+                        m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, dst, dst + n,
+                        dst + 2 * n, sign, col);
+                    break;
+                case MODE_UU:
+                    k_apply_cells<P, MIEHE, MODE_UU><<<gc, CELL_THREADS, 0, s>>>(
+                        m, L->shape, L->mat, q, f, src, src + n, nullptr, dst, dst + n, nullptr,
+                        sign, col);
+                    break;
+                case MODE_PHIPHI:
+                    k_apply_cells<P, MIEHE, MODE_PHIPHI><<<gc, CELL_THREADS, 0, s>>>(
+                        m, L->shape, L->mat, q, f, nullptr, nullptr, src, nullptr, nullptr, dst,
+                        sign, col);
+                    break;
+                case MODE_PHIROW:
+                    k_apply_cells<P, MIEHE, MODE_PHIROW><<<gc, CELL_THREADS, 0, s>>>(
+                        m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, nullptr, nullptr,
+                        dst, sign, col);
+                    break;
+            }
+            count_launches(1);
+        }
         return cudaGetLastError();
     }
 };
@@ -525,10 +557,16 @@ struct DiagL {
         cudaMemsetAsync(dx, 0, sizeof(double) * w.n, s);
         cudaMemsetAsync(dy, 0, sizeof(double) * w.n, s);
         cudaMemsetAsync(dp, 0, sizeof(double) * w.n, s);
-        k_diag_cells<P, MIEHE><<<grid_for(w.ncell, CELL_THREADS), CELL_THREADS, 0, s>>>(
-            m, w, L->shape, L->mat, L->qcache, dx, dy, dp);
+        count_launches(3);
+        for (int c = 0; c < 4; ++c) {
+            const Colour col(c, m.nside, w.row0, (int)(w.ncell / m.nside));
+            if (col.count() == 0) continue;
+            k_diag_cells<P, MIEHE><<<grid_for(col.count(), CELL_THREADS), CELL_THREADS, 0, s>>>(
+                m, w, L->shape, L->mat, L->qcache, dx, dy, dp, col);
+            count_launches(1);
+        }
         k_diag_finalize<<<grid_for(w.n, 256), 256, 0, s>>>(w.n, L->flags, dx, dy, dp, invert);
-        count_launches(5);
+        count_launches(1);
         return cudaGetLastError();
     }
 };
@@ -538,10 +576,16 @@ struct ResidualL {
     static cudaError_t run(const Level* L, double* out, int md, int ma, cudaStream_t s) {
         const Mesh& m = L->mesh;
         cudaMemsetAsync(out, 0, sizeof(double) * 3 * m.n, s);
-        k_residual_cells<P, MIEHE><<<grid_for(m.n_cells(), CELL_THREADS), CELL_THREADS, 0, s>>>(
-            m, L->shape, L->mat, L->U, L->phi_tilde, out);
+        count_launches(1);
+        for (int c = 0; c < 4; ++c) {
+            const Colour col(c, m.nside, 0, m.nside);
+            if (col.count() == 0) continue;
+            k_residual_cells<P, MIEHE><<<grid_for(col.count(), CELL_THREADS), CELL_THREADS, 0, s>>>(
+                m, L->shape, L->mat, L->U, L->phi_tilde, out, col);
+            count_launches(1);
+        }
         k_residual_mask<<<grid_for(m.n, 256), 256, 0, s>>>(m.n, L->flags, out, md, ma);
-        count_launches(3);
+        count_launches(1);
         return cudaGetLastError();
     }
 };

@@ -7,8 +7,10 @@
 // cell row.  The row is the coarse Lagrange basis of the owner's parent cell
 // evaluated through the child embedding; weights with |w| <= 1e-14 are
 // dropped exactly as the reference does (multigrid.py:81-83).
-// Restriction is the exact transpose (multigrid.py:114-120): each fine row
-// scatters its kept weights into the coarse vector.
+// Restriction is the exact transpose (multigrid.py:114-120): one thread per
+// coarse cell gathers the fine rows that cell owns and adds the weighted sums
+// into the cell's coarse nodes, in four colour passes (cx, cy parities) so
+// no two threads touch a coarse node at once -- no atomics, fixed order.
 // Injection restates src/mesh_hierarchy.py:316-338 / pff_operator.py:380-400.
 #include "pff_internal.cuh"
 
@@ -83,28 +85,71 @@ __global__ void k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __res
     }
 }
 
+struct CellColour {
+    int c, hx, hy, cy0;
+};
+
+inline CellColour make_colour(int colour, int ns, int row_lo, int row_hi) {
+    CellColour k;
+    k.c = colour;
+    k.hx = (ns - (colour & 1) + 1) >> 1;
+    k.cy0 = row_lo + (((row_lo & 1) != (colour >> 1)) ? 1 : 0);
+    k.hy = row_hi > k.cy0 ? (row_hi - k.cy0 + 1) >> 1 : 0;
+    return k;
+}
+
+__device__ __forceinline__ bool owned_fine(const Mesh& mf, const Win& wf, int64_t gg) {
+    if (gg >= mf.n_grid) return wf.owns_dup != 0;
+    const int64_t j = gg / mf.np1;
+    return j >= wf.own_lo && j < wf.own_hi;
+}
+
 template <int P>
 __global__ void k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf,
-                           double* xc) {
+                           double* xc, CellColour col) {
     constexpr int N1 = P + 1;
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= wf.n_owned(mf)) return;
-    const int64_t gg = wf.owned_global(mf, t);
-    Owner o = fine_owner(mf, gg);
-    const int64_t g = wf.loc(mf, gg);
-    double v[3];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)col.hx * col.hy) return;
+    const int ccx = (col.c & 1) + 2 * (int)(t % col.hx);
+    const int ccy = col.cy0 + 2 * (int)(t / col.hx);
+    double acc[3][N1][N1] = {};
+    // the fine nodes of the coarse cell's block, each once: rows 0..p of the
+    // lower child, then rows 0..p of the upper child, whose row 0 repeats the
+    // lower child's row p except where the slit splits it (coarse level 0)
+#pragma unroll 1
+    for (int fb = 0; fb <= 2 * P + 1; ++fb) {
+        const bool up = fb > P;
+        const int fcy = 2 * ccy + (up ? 1 : 0), lb = up ? fb - P - 1 : fb;
+#pragma unroll 1
+        for (int fa = 0; fa <= 2 * P; ++fa) {
+            const int fcx = 2 * ccx + (fa > P ? 1 : 0), la = fa > P ? fa - P : fa;
+            const int64_t gg = mf.node(fcx, fcy, la, lb);
+            if (up && lb == 0 && gg == mf.node(fcx, 2 * ccy, la, P)) continue;
+            const Owner o = fine_owner(mf, gg);
+            if (o.ccx != ccx || o.ccy != ccy || !owned_fine(mf, wf, gg)) continue;
+            const int64_t g = wf.loc(mf, gg);
+            double v[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) v[k] = yf[k * wf.n + g];
+            for (int k = 0; k < 3; ++k) v[k] = yf[k * wf.n + g];
+#pragma unroll
+            for (int my = 0; my < N1; ++my)
+#pragma unroll
+                for (int mx = 0; mx < N1; ++mx) {
+                    const double w = E.E[o.chy][o.b][my] * E.E[o.chx][o.a][mx];
+                    if (fabs(w) > 1e-14) {
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) acc[k][my][mx] += w * v[k];
+                    }
+                }
+        }
+    }
 #pragma unroll
     for (int my = 0; my < N1; ++my)
 #pragma unroll
         for (int mx = 0; mx < N1; ++mx) {
-            double w = E.E[o.chy][o.b][my] * E.E[o.chx][o.a][mx];
-            if (fabs(w) > 1e-14) {
-                int64_t c = mc.node(o.ccx, o.ccy, mx, my);
+            const int64_t c = mc.node(ccx, ccy, mx, my);
 #pragma unroll
-                for (int k = 0; k < 3; ++k) atomicAdd(xc + k * mc.n + c, w * v[k]);
-            }
+            for (int k = 0; k < 3; ++k) xc[k * mc.n + c] += acc[k][my][mx];
         }
 }
 
@@ -168,17 +213,31 @@ cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, do
     if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
     if (C.windowed()) return cudaErrorNotSupported;
     const Win wf = F.win();
-    const int64_t nf = wf.n_owned(F.mesh);
     cudaMemsetAsync(xc, 0, sizeof(double) * 3 * C.mesh.n, s);
-    switch (F.mesh.p) {
-        case 1: k_restrict<1><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
-        case 2: k_restrict<2><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
-        case 3: k_restrict<3><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
-        case 4: k_restrict<4><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc); break;
-        default: return cudaErrorInvalidValue;
+    count_launches(1);
+    // coarse cell rows owning the window's fine rows (fine cell rows cyb-1 .. cye)
+    const int nsc = C.mesh.nside;
+    const int cyb = F.cy_begin(), cye = F.cy_end();
+    const int lo = cyb > 0 ? (cyb - 1) / 2 : 0;
+    const int hi = (cye / 2 + 1) < nsc ? cye / 2 + 1 : nsc;
+    for (int c = 0; c < 4; ++c) {
+        const CellColour col = make_colour(c, nsc, lo, hi);
+        const int64_t cnt = (int64_t)col.hx * col.hy;
+        if (cnt <= 0) continue;
+        const unsigned g = (unsigned)((cnt + 127) / 128);
+        switch (F.mesh.p) {
+            case 1: k_restrict<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
+            case 2: k_restrict<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
+            case 3: k_restrict<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
+            case 4: k_restrict<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
+            default: return cudaErrorInvalidValue;
+        }
+        count_launches(1);
     }
-    if (zero_cons) k_zero_cons3<<<blocks(C.mesh.n), 256, 0, s>>>(C.mesh.n, C.flags, xc);
-    count_launches(zero_cons ? 3 : 2);
+    if (zero_cons) {
+        k_zero_cons3<<<blocks(C.mesh.n), 256, 0, s>>>(C.mesh.n, C.flags, xc);
+        count_launches(1);
+    }
     return cudaGetLastError();
 }
 

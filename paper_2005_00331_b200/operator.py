@@ -446,6 +446,19 @@ def block_diagonals(state: LinearizationState, invert: bool = False):
     return duu, dpp
 
 
+def extrapolate_phase(phi_nm1, phi_nm2, t_n: float, t_nm1: float, t_nm2: float):
+    """Linear extrapolation of the phase field from two previous steps
+    (src/pff_operator.py:208-215); device tensors stay on the device."""
+    if not (t_nm2 < t_nm1 < t_n):
+        raise ValueError("time points must be strictly increasing")
+    factor = (t_n - t_nm1) / (t_nm1 - t_nm2)
+    if isinstance(phi_nm1, torch.Tensor) and phi_nm1.is_cuda:
+        return phi_nm1 + factor * (phi_nm1 - phi_nm2)
+    phi_nm1 = np.asarray(phi_nm1, dtype=float)
+    phi_nm2 = np.asarray(phi_nm2, dtype=float)
+    return phi_nm1 + factor * (phi_nm1 - phi_nm2)
+
+
 def residual(state: LinearizationState, mask_dirichlet: bool = True, mask_active: bool = False,
              as_numpy: bool = True):
     """Nonlinear residual (src/pff_operator.py:218-241)."""

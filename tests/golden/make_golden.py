@@ -33,7 +33,9 @@ from fracturekit.multigrid import (ChebyshevConfig, GmgPreconditioner,  # noqa: 
                                    estimate_lambda_range)
 from fracturekit.active_set_solver import (ActiveSetParams, ActiveSetSolver,  # noqa: E402
                                            lumped_mass_diagonal)
-from fracturekit.simulation_driver import apply_boundary_values, boundary_program  # noqa: E402
+from fracturekit.simulation_driver import (ScenarioConfig, apply_boundary_values,  # noqa: E402
+                                           boundary_program, run_simulation)
+from fracturekit import io as ref_io  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -189,7 +191,45 @@ ACTIVESET = {
 }
 
 
+def simulation_case(scenario, level, degree, split, steps, du, vtk_every):
+    """run_simulation (src/simulation_driver.py:189-259) on a small mesh."""
+    cfg = ScenarioConfig(scenario=scenario, level=level, degree=degree, split=split, steps=steps,
+                         du=du, vtk_every=vtk_every)
+    res = run_simulation(cfg)
+    rec = res.records
+    d = dict(step=np.array([r.step for r in rec]), time_s=np.array([r.time_s for r in rec]),
+             u=np.array([r.u_applied_mm for r in rec]),
+             load_x=np.array([r.load_x_kN for r in rec]),
+             load_y=np.array([r.load_y_kN for r in rec]),
+             as_iters=np.array([r.as_iters for r in rec]),
+             gmres_total=np.array([r.gmres_iters_total for r in rec]),
+             active_dofs=np.array([r.active_dofs for r in rec]),
+             snap_steps=np.array([s for s, _ in res.snapshots]),
+             U_final=res.snapshots[-1][1],
+             bounds=np.array([res.irreversibility_violation, res.phi_min, res.phi_max]),
+             meta=np.array([level, degree, 1 if split == "miehe" else 0, steps, vtk_every,
+                            0 if scenario == "tension" else 1]),
+             du=np.array([du]))
+    h = build_hierarchy(level, degree)
+    d["vtk"] = np.frombuffer(ref_io.vtk_text(h.dof_map(level), res.snapshots[-1][1]).encode(),
+                             dtype=np.uint8)
+    print(f"simulation {scenario} p{degree} l{level} {split}: as {d['as_iters'].tolist()} "
+          f"gmres {d['gmres_total'].tolist()} active {d['active_dofs'].tolist()}")
+    return d
+
+
+SIMULATION = {
+    "sim_tension_p1_l3_miehe": ("tension", 3, 1, "miehe", 4, 1e-5, 2),
+    "sim_shear_p2_l3_none": ("shear", 3, 2, "none", 3, 1e-5, 0),
+    "sim_tension_p1_l4_miehe_fast": ("tension", 4, 1, "miehe", 6, 2e-3, 3),
+}
+
+
 def main():
+    if "--simulation" in sys.argv:   # only the run_simulation fixtures
+        for name, args in SIMULATION.items():
+            np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **simulation_case(*args))
+        return
     if "--activeset" in sys.argv:   # only the active-set fixtures
         for name, args in ACTIVESET.items():
             np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **activeset_case(*args))
@@ -197,6 +237,8 @@ def main():
     cases = {}
     for name, args in ACTIVESET.items():
         cases[name] = activeset_case(*args)
+    for name, args in SIMULATION.items():
+        cases[name] = simulation_case(*args)
     for split in ("none", "miehe"):
         cases[f"pr1_{split}"] = operator_case(2, 5, split, 0, with_cache=True)
         for p in (1, 3, 4):

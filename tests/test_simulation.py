@@ -1,0 +1,137 @@
+"""Quasi-static driver (src/simulation_driver.py, src/io.py)
+against the reference's own run_simulation fixtures (tests/golden/sim_*.npz)."""
+
+import logging
+
+import numpy as np
+import pytest
+
+from conftest import block_rel, load_golden
+import paper_2005_00331_b200 as P
+from paper_2005_00331_b200 import io as pio
+
+gpu = pytest.mark.gpu
+SIM_CASES = ["sim_tension_p1_l3_miehe", "sim_shear_p2_l3_none", "sim_tension_p1_l4_miehe_fast"]
+# The fast-loading case has an active-set stop test that lands within 40% of the
+# 1e-8 threshold (reference step 5: |R|/|R0| = 1.38e-8), so round-off in the
+# GMRES solutions may shift one step by one active-set iteration; the physical
+# outputs (loads, final fields, active sets) must still agree.
+EXACT_AS = {"sim_tension_p1_l3_miehe", "sim_shear_p2_l3_none"}
+
+
+def config_of(d, **kw):
+    level, degree, miehe, steps, vtk_every, shear = (int(v) for v in d["meta"])
+    return P.ScenarioConfig(scenario="shear" if shear else "tension", level=level, degree=degree,
+                            split="miehe" if miehe else "none", steps=steps,
+                            du=float(d["du"][0]), vtk_every=vtk_every, **kw)
+
+
+# ---- host side (CPU) ---------------------------------------------------------------
+def test_scenario_config_validation(caplog):
+    for bad in (dict(scenario="bending"), dict(steps=0), dict(level=3, coarse_level=4),
+                dict(split="amor"), dict(workers=0)):
+        with pytest.raises(ValueError):
+            P.ScenarioConfig(**bad)
+    with caplog.at_level(logging.WARNING, logger="paper_2005_00331_b200.simulation"):
+        P.ScenarioConfig(level=4, steps=1)
+    assert any("under-resolved" in r.message for r in caplog.records)
+
+
+def test_extrapolate_phase():
+    a, b = np.array([0.9, 1.0]), np.array([1.0, 1.0])
+    assert np.array_equal(P.extrapolate_phase(a, b, 3.0, 2.0, 1.0), a + 1.0 * (a - b))
+    with pytest.raises(ValueError):
+        P.extrapolate_phase(a, b, 1.0, 2.0, 3.0)
+
+
+@pytest.mark.parametrize("name", SIM_CASES)
+def test_vtk_text_bytes_match_reference(name):
+    d = load_golden(name)
+    level, degree = int(d["meta"][0]), int(d["meta"][1])
+    dm = P.build_hierarchy(level, degree).dof_map(level)
+    assert pio.vtk_text(dm, d["U_final"]).encode() == d["vtk"].tobytes()
+
+
+def test_csv_formats(tmp_path):
+    rec = P.LoadRecord(step=1, time_s=1.0, u_applied_mm=1e-5, load_x_kN=-0.0,
+                       load_y_kN=0.123456789012345, as_iters=3, gmres_iters_total=17,
+                       active_dofs=4, wall_s=0.0123456789)
+    pio.write_load_csv([rec], tmp_path / "l.csv")
+    raw = (tmp_path / "l.csv").read_bytes()
+    assert b"\r" not in raw
+    lines = raw.decode().strip().split("\n")
+    assert lines[0] == pio.CSV_HEADER
+    assert lines[1] == "1,1,1e-05,-0,0.123456789012,3,17,4,0.0123457"
+
+
+# ---- the loop on the device -----------------------------------------------------------
+@gpu
+@pytest.mark.parametrize("name", SIM_CASES)
+def test_run_simulation_matches_reference(name):
+    d = load_golden(name)
+    res = P.run_simulation(config_of(d))
+    r = res.records
+    assert [x.step for x in r] == d["step"].tolist()
+    as_got = [x.as_iters for x in r]
+    if name in EXACT_AS:
+        assert as_got == d["as_iters"].tolist()
+        for got, want, k in zip([x.gmres_iters_total for x in r], d["gmres_total"], d["as_iters"]):
+            assert abs(got - int(want)) <= int(k)    # +-1 per linear solve
+    else:
+        assert max(abs(a - int(b)) for a, b in zip(as_got, d["as_iters"])) <= 1
+    assert [x.active_dofs for x in r] == d["active_dofs"].tolist()
+    # the undriven component is round-off (~1e-19): compare on the load scale
+    scale = max(np.abs(d["load_y"]).max(), np.abs(d["load_x"]).max())
+    for key, col in (("load_x", "load_x_kN"), ("load_y", "load_y_kN")):
+        got = np.array([getattr(x, col) for x in r])
+        assert np.abs(got - d[key]).max() <= 1e-7 * scale, key
+    assert [s for s, _ in res.snapshots] == d["snap_steps"].tolist()
+    n = len(d["U_final"]) // 3
+    assert max(block_rel(res.snapshots[-1][1], d["U_final"], n)) <= 1e-7
+    assert res.irreversibility_violation <= 1e-10
+    assert res.phi_min == pytest.approx(d["bounds"][1], abs=1e-9)
+
+
+@gpu
+def test_csv_output_and_determinism(tmp_path):
+    outs = []
+    for sub in ("a", "b"):
+        cfg = P.ScenarioConfig(scenario="tension", level=3, degree=1, steps=3,
+                               out_dir=tmp_path / sub, vtk_every=2)
+        P.run_simulation(cfg)
+        text = (tmp_path / sub / "tension_loads.csv").read_text()
+        assert (tmp_path / sub / "tension_00002.vtk").exists()
+        assert (tmp_path / sub / "tension_00003.vtk").exists()
+        outs.append("\n".join(",".join(line.split(",")[:-1]) for line in text.split("\n")))
+    assert outs[0] == outs[1]
+    lines = outs[0].strip().split("\n")
+    assert len(lines) == 4 and lines[1].startswith("1,1,")
+
+
+@gpu
+def test_elastic_linearity_and_equilibrium():
+    # reference TestReactionLoad: the isotropic loads grow linearly at first,
+    # and the top and bottom reactions balance
+    res = P.run_simulation(P.ScenarioConfig(scenario="tension", level=3, degree=1, steps=5,
+                                            split="none", vtk_every=0))
+    loads = np.array([x.load_y_kN for x in res.records])
+    u = np.array([x.u_applied_mm for x in res.records])
+    assert np.abs((loads / u) / (loads[0] / u[0]) - 1.0).max() < 0.01
+    h = P.build_hierarchy(3, 1)
+    st = P.LinearizationState(h, 3, P.MaterialParams())
+    st.set_solution(res.snapshots[-1][1])
+    raw = P.residual(st, mask_dirichlet=False)
+    n = st.n_scalar
+    top, bot = h.dof_map(3).boundary_nodes["top"], h.dof_map(3).boundary_nodes["bottom"]
+    sums = [(raw[c * n + top].sum(), raw[c * n + bot].sum()) for c in range(2)]
+    scale = max(abs(v) for pair in sums for v in pair)
+    for t, b in sums:
+        assert abs(t + b) <= 1e-6 * scale
+
+
+@gpu
+def test_unloaded_reaction_is_zero():
+    h = P.build_hierarchy(3, 1)
+    st = P.LinearizationState(h, 3, P.MaterialParams())
+    P.apply_boundary_values(st, P.boundary_program("tension", 0.0))
+    assert P.reaction_load(st) == (0.0, 0.0)
