@@ -93,7 +93,10 @@ int pff_level_set_window(pff_level* L, int cy_begin, int cy_end);
 int pff_level_window(const pff_level* L, int64_t* rows);
 
 /* Bind the linearisation point: U (3n), phi_tilde (n), flags (n bytes) and a
- * caller-allocated q-point cache of pff_level_qcache_len() doubles. */
+ * caller-allocated q-point cache of pff_level_qcache_len() doubles (q-point
+ * state, the Q2 tangent tiles, and the element-vector scratch that the generic
+ * application and the restriction INTO this level use -- so a level's
+ * applications and restrictions into it must be ordered, e.g. one stream). */
 int pff_level_bind(pff_level* L, const double* U, const double* phi_tilde,
                    const uint8_t* flags, double* qcache);
 

@@ -92,9 +92,46 @@ struct Level {
     int tile_nq() const { return miehe ? 10 : 5; }   // tangent (6 | 1) + coupling (3) + pc
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
     int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
-    int64_t qcache_len() const { return generic_len() + tile_len(); }
+    // element-vector scratch of the generic application and of the restriction
+    // into this level: 3 components x (p+1)^2 nodes per local cell
+    int64_t ev_len() const { return 3 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells(); }
+    int64_t qcache_len() const { return generic_len() + tile_len() + ev_len(); }
     double* qtile() const { return qcache + generic_len(); }
+    double* ev() const { return qcache + generic_len() + tile_len(); }
 };
+
+// Cells containing scalar node g (global id) in increasing cell index, with
+// the node's local (a, b) in each; cells of rows outside [row_lo, row_hi) are
+// skipped.  The slit copies: the grid id of a slit node belongs to the lower
+// cell row only, the appended copy n_grid + i to the upper one.
+template <class F>
+__device__ __forceinline__ void node_cells(const Mesh& m, int64_t g, int row_lo, int row_hi,
+                                           F&& f) {
+    const int p = m.p, ns = m.nside;
+    int64_t i, j;
+    int cy_lo = row_lo, cy_hi = row_hi < ns ? row_hi : ns;
+    if (g < m.n_grid) {
+        j = g / m.np1;
+        i = g - j * m.np1;
+        if (m.level >= 1 && j == m.i_mid && i < m.i_mid && cy_hi > (ns >> 1)) cy_hi = ns >> 1;
+    } else {
+        i = g - m.n_grid;
+        j = m.i_mid;
+        if (cy_lo < (ns >> 1)) cy_lo = ns >> 1;
+    }
+    const int cy0 = j > 0 ? (int)((j - 1) / p) : 0, cy1 = (int)(j / p);
+    const int cx0 = i > 0 ? (int)((i - 1) / p) : 0, cx1 = (int)(i / p);
+    for (int cy = cy0; cy <= cy1; ++cy) {
+        if (cy < cy_lo || cy >= cy_hi) continue;
+        const int b = (int)(j - (int64_t)cy * p);
+        if (b < 0 || b > p) continue;
+        for (int cx = cx0; cx <= cx1 && cx < ns; ++cx) {
+            const int a = (int)(i - (int64_t)cx * p);
+            if (a < 0 || a > p) continue;
+            f(cx, cy, a, b);
+        }
+    }
+}
 
 // options (pff_set_option)
 void set_generic_apply(bool on);

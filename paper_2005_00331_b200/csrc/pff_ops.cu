@@ -4,12 +4,13 @@
 //
 // Generic path (any p in 1..4): one thread per cell, sum-factorised 1-D
 // contractions in registers, q-point physics restated from
-// src/_kernels.py:555-693.  Cells are processed in four colour passes
-// (cx mod 2, cy mod 2): cells of one colour share no node, so each pass adds
-// into the output with plain read-modify-writes -- no atomics, and the
-// summation order per node is fixed (deterministic results run to run).  The
-// output's constrained rows are initialised first (identity rows/columns,
-// src/pff_operator.py:262-302).  The Q2 fast path lives in pff_sweep.cu.
+// src/_kernels.py:555-693.  No atomics anywhere, so results are identical run
+// to run: the application writes per-cell element vectors into the level's
+// scratch and a per-node gather sums them in increasing cell index (two
+// launches, full parallelism -- the coarse levels of the V-cycle are latency
+// bound); diagonals and residual add in four colour passes (cx mod 2,
+// cy mod 2: cells of one colour share no node).  Identity rows/columns as in
+// src/pff_operator.py:262-302.  The Q2 fast path lives in pff_sweep.cu.
 #include "pff_internal.cuh"
 
 namespace pff {
@@ -130,29 +131,37 @@ struct ModeTraits {
 };
 
 // dst rows: constrained -> src (identity row); free -> 0, or for the fused
-// residual dst = rhs - J src: constrained -> rhs - src, free -> rhs.
-template <int MODE>
-__global__ void k_apply_init(int64_t n, const uint8_t* __restrict__ flags,
-                             const double* __restrict__ src, const double* __restrict__ rhs,
-                             double* __restrict__ dst) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Per-node gather of the element vectors (fixed cell order) with the identity
+// rows of src/pff_operator.py:262-302; fused form dst = rhs - J src.
+template <int P, int MODE>
+__global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
+                               const double* __restrict__ src, const double* __restrict__ rhs,
+                               const double* __restrict__ ev, double* __restrict__ dst) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t n = m.n, nc = m.n_cells();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint8_t f = flags[i];
-    auto put = [&](int64_t o, int64_t so, bool cons) {
-        double v = cons ? src[so] : 0.0;
-        dst[o] = rhs ? rhs[o] - v : v;
-    };
-    if (MODE == MODE_FULL) {
-        put(i, i, f & F_DIR);
-        put(n + i, n + i, f & F_DIR);
-        put(2 * n + i, 2 * n + i, f & F_ACT);
-    } else if (MODE == MODE_UU) {
-        put(i, i, f & F_DIR);
-        put(n + i, n + i, f & F_DIR);
-    } else if (MODE == MODE_PHIPHI) {
-        put(i, i, f & F_ACT);
-    } else {
-        put(i, 2 * n + i, f & F_ACT);
+    // output components: (element-vector component, src offset, constraint bit)
+    constexpr int NO = MODE == MODE_FULL ? 3 : MODE == MODE_UU ? 2 : 1;
+    int comp[3], soff[3];
+    bool cons[3];
+    for (int c = 0; c < NO; ++c) {
+        comp[c] = (MODE == MODE_FULL || MODE == MODE_UU) ? c : 2;
+        soff[c] = MODE == MODE_PHIROW ? 2 : (MODE == MODE_PHIPHI ? 0 : c);
+        cons[c] = comp[c] < 2 ? (f & F_DIR) : (f & F_ACT);
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    node_cells(m, i, 0, m.nside, [&](int cx, int cy, int a, int b) {
+        const int64_t cell = (int64_t)cy * m.nside + cx;
+#pragma unroll
+        for (int c = 0; c < NO; ++c)
+            acc[c] += ev[(int64_t)(comp[c] * QQ + b * N1 + a) * nc + cell];
+    });
+#pragma unroll
+    for (int c = 0; c < NO; ++c) {
+        const double v = cons[c] ? src[soff[c] * n + i] : acc[c];
+        dst[c * n + i] = rhs ? rhs[c * n + i] - v : v;
     }
 }
 
@@ -160,16 +169,14 @@ template <int P, bool MIEHE, int MODE>
 __global__ void __launch_bounds__(CELL_THREADS)
 k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
               const uint8_t* __restrict__ flags, const double* __restrict__ sx,
-              const double* __restrict__ sy, const double* __restrict__ sp, double* dx,
-              double* dy, double* dp, double sign, Colour col) {
+              const double* __restrict__ sy, const double* __restrict__ sp,
+              double* __restrict__ ev) {
     using T = ModeTraits<MODE>;
     constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t nc = m.n_cells();
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= col.count()) return;
-    int cx, cy;
-    col.cell(tid, cx, cy);
-    const int64_t cell = (int64_t)cy * m.nside + cx;
+    const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= nc) return;
+    const int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
     int64_t gid[N1][N1];
     uint8_t fl[N1][N1];
     cell_ids<N1>(m, cx, cy, gid);
@@ -255,10 +262,10 @@ k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
         for (int b = 0; b < N1; ++b)
 #pragma unroll
             for (int a = 0; a < N1; ++a)
-                if (!(fl[b][a] & F_DIR)) {
-                    dx[gid[b][a]] += sign * ru[b][a];
-                    dy[gid[b][a]] += sign * rv[b][a];
-                }
+            {
+                ev[(int64_t)(b * N1 + a) * nc + cell] = ru[b][a];
+                ev[(int64_t)(QQ + b * N1 + a) * nc + cell] = rv[b][a];
+            }
     }
     if (T::DO_PP) {
         double rp[N1][N1] = {};
@@ -272,7 +279,7 @@ k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
         for (int b = 0; b < N1; ++b)
 #pragma unroll
             for (int a = 0; a < N1; ++a)
-                if (!(fl[b][a] & F_ACT)) dp[gid[b][a]] += sign * rp[b][a];
+                ev[(int64_t)(2 * QQ + b * N1 + a) * nc + cell] = rp[b][a];
     }
 }
 
@@ -504,46 +511,35 @@ struct ApplyL {
                            const double* rhs, cudaStream_t s) {
         const Mesh& m = L->mesh;
         const int64_t n = m.n;
-        const unsigned gi = grid_for(n, 256);
-        const double sign = rhs ? -1.0 : 1.0;
+        const unsigned gi = grid_for(n, 256), gc = grid_for(m.n_cells(), CELL_THREADS);
         const double* q = L->qcache;
         const uint8_t* f = L->flags;
+        double* ev = L->ev();
         switch (mode) {
-            case MODE_FULL: k_apply_init<MODE_FULL><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
-            case MODE_UU: k_apply_init<MODE_UU><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
-            case MODE_PHIPHI: k_apply_init<MODE_PHIPHI><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
-            case MODE_PHIROW: k_apply_init<MODE_PHIROW><<<gi, 256, 0, s>>>(n, f, src, rhs, dst); break;
-            default: return cudaErrorInvalidValue;
+            case MODE_FULL:
+                k_apply_cells<P, MIEHE, MODE_FULL><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
+                k_apply_gather<P, MODE_FULL><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                break;
+            case MODE_UU:
+                k_apply_cells<P, MIEHE, MODE_UU><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, nullptr, ev);
+                k_apply_gather<P, MODE_UU><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                break;
+            case MODE_PHIPHI:
+                k_apply_cells<P, MIEHE, MODE_PHIPHI><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, nullptr, nullptr, src, ev);
+                k_apply_gather<P, MODE_PHIPHI><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                break;
+            case MODE_PHIROW:
+                k_apply_cells<P, MIEHE, MODE_PHIROW><<<gc, CELL_THREADS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
+                k_apply_gather<P, MODE_PHIROW><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                break;
+            default:
+                return cudaErrorInvalidValue;
         }
-        count_launches(1);
-        for (int c = 0; c < 4; ++c) {
-            const Colour col(c, m.nside, 0, m.nside);
-            if (col.count() == 0) continue;
-            const unsigned gc = grid_for(col.count(), CELL_THREADS);
-            switch (mode) {
-                case MODE_FULL:
-                    k_apply_cells<P, MIEHE, MODE_FULL><<<gc, CELL_THREADS, 0, s>>>(
-                        m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, dst, dst + n,
-                        dst + 2 * n, sign, col);
-                    break;
-                case MODE_UU:
-                    k_apply_cells<P, MIEHE, MODE_UU><<<gc, CELL_THREADS, 0, s>>>(
-                        m, L->shape, L->mat, q, f, src, src + n, nullptr, dst, dst + n, nullptr,
-                        sign, col);
-                    break;
-                case MODE_PHIPHI:
-                    k_apply_cells<P, MIEHE, MODE_PHIPHI><<<gc, CELL_THREADS, 0, s>>>(
-                        m, L->shape, L->mat, q, f, nullptr, nullptr, src, nullptr, nullptr, dst,
-                        sign, col);
-                    break;
-                case MODE_PHIROW:
-                    k_apply_cells<P, MIEHE, MODE_PHIROW><<<gc, CELL_THREADS, 0, s>>>(
-                        m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, nullptr, nullptr,
-                        dst, sign, col);
-                    break;
-            }
-            count_launches(1);
-        }
+        count_launches(2);
         return cudaGetLastError();
     }
 };

@@ -104,44 +104,75 @@ __device__ __forceinline__ bool owned_fine(const Mesh& mf, const Win& wf, int64_
     return j >= wf.own_lo && j < wf.own_hi;
 }
 
+// ev == nullptr: colour pass (col) adding into xc; otherwise one pass over the
+// cells of rows [col.cy0, col.cy0 + col.hy) writing element vectors ev[k][my][mx][cell]
 template <int P>
-__global__ void k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf,
-                           double* xc, CellColour col) {
-    constexpr int N1 = P + 1;
+__global__ void __launch_bounds__(128)
+k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, double* xc,
+           CellColour col, double* __restrict__ ev) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)col.hx * col.hy) return;
-    const int ccx = (col.c & 1) + 2 * (int)(t % col.hx);
-    const int ccy = col.cy0 + 2 * (int)(t / col.hx);
+    int ccx, ccy;
+    if (ev) {
+        ccx = (int)(t % col.hx);
+        ccy = col.cy0 + (int)(t / col.hx);
+    } else {
+        ccx = (col.c & 1) + 2 * (int)(t % col.hx);
+        ccy = col.cy0 + 2 * (int)(t / col.hx);
+    }
     double acc[3][N1][N1] = {};
-    // the fine nodes of the coarse cell's block, each once: rows 0..p of the
+    // The fine nodes of the coarse cell's block, each once: rows 0..p of the
     // lower child, then rows 0..p of the upper child, whose row 0 repeats the
-    // lower child's row p except where the slit splits it (coarse level 0)
-#pragma unroll 1
+    // lower child's row p except where the slit splits it (coarse level 0).
+    // First-visit ownership (fine_owner) in closed form: the cell owns a
+    // block node unless it lies on the block's left column (ccx > 0) or
+    // bottom row (ccy > 0) -- those belong to the neighbour -- except the
+    // upper slit copies, owned by the upper cell row.  The owner's child and
+    // local index are the enumeration's own (fcx - 2 ccx, la, fcy - 2 ccy, lb).
+#pragma unroll
     for (int fb = 0; fb <= 2 * P + 1; ++fb) {
         const bool up = fb > P;
-        const int fcy = 2 * ccy + (up ? 1 : 0), lb = up ? fb - P - 1 : fb;
-#pragma unroll 1
-        for (int fa = 0; fa <= 2 * P; ++fa) {
-            const int fcx = 2 * ccx + (fa > P ? 1 : 0), la = fa > P ? fa - P : fa;
-            const int64_t gg = mf.node(fcx, fcy, la, lb);
-            if (up && lb == 0 && gg == mf.node(fcx, 2 * ccy, la, P)) continue;
-            const Owner o = fine_owner(mf, gg);
-            if (o.ccx != ccx || o.ccy != ccy || !owned_fine(mf, wf, gg)) continue;
-            const int64_t g = wf.loc(mf, gg);
-            double v[3];
+        const int chy = up ? 1 : 0, lb = up ? fb - P - 1 : fb;
+        const int fcy = 2 * ccy + chy;
+        const int64_t j = (int64_t)P * fcy + lb;   // fine grid row
 #pragma unroll
-            for (int k = 0; k < 3; ++k) v[k] = yf[k * wf.n + g];
+        for (int fa = 0; fa <= 2 * P; ++fa) {
+            const int chx = fa > P ? 1 : 0, la = fa - P * chx;
+            const int fcx = 2 * ccx + chx;
+            const int64_t i = (int64_t)P * fcx + la;
+            const bool dup = mf.level >= 1 && fcy >= (mf.nside >> 1) && j == mf.i_mid && i < mf.i_mid;
+            if (up && lb == 0 && !dup) continue;                 // repeats the lower child's row p
+            if (fa == 0 && ccx > 0) continue;                    // left neighbour's column
+            if (fb == 0 && ccy > 0 && !dup) continue;            // lower neighbour's row
+            // window ownership of the fine node
+            if (dup ? !wf.owns_dup : (j < wf.own_lo || j >= wf.own_hi)) continue;
+            const int64_t gg = dup ? mf.n_grid + i : j * mf.np1 + i;
+            const int64_t g = wf.loc(mf, gg);
+            const double v0 = yf[g], v1 = yf[wf.n + g], v2 = yf[2 * wf.n + g];
 #pragma unroll
             for (int my = 0; my < N1; ++my)
 #pragma unroll
                 for (int mx = 0; mx < N1; ++mx) {
-                    const double w = E.E[o.chy][o.b][my] * E.E[o.chx][o.a][mx];
+                    const double w = E.E[chy][lb][my] * E.E[chx][la][mx];
                     if (fabs(w) > 1e-14) {
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) acc[k][my][mx] += w * v[k];
+                        acc[0][my][mx] += w * v0;
+                        acc[1][my][mx] += w * v1;
+                        acc[2][my][mx] += w * v2;
                     }
                 }
         }
+    }
+    if (ev) {
+        const int64_t nc = mc.n_cells(), cell = (int64_t)ccy * mc.nside + ccx;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int my = 0; my < N1; ++my)
+#pragma unroll
+                for (int mx = 0; mx < N1; ++mx)
+                    ev[(int64_t)(k * QQ + my * N1 + mx) * nc + cell] = acc[k][my][mx];
+        return;
     }
 #pragma unroll
     for (int my = 0; my < N1; ++my)
@@ -151,6 +182,30 @@ __global__ void k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __re
 #pragma unroll
             for (int k = 0; k < 3; ++k) xc[k * mc.n + c] += acc[k][my][mx];
         }
+}
+
+// coarse node gather of the element vectors (cell rows [lo, hi)), zeroing the
+// constrained rows when asked (src/multigrid.py:338)
+template <int P>
+__global__ void k_restrict_gather(Mesh mc, const double* __restrict__ ev, double* __restrict__ xc,
+                                  int lo, int hi, const uint8_t* __restrict__ flags, int zero_cons) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mc.n) return;
+    const int64_t nc = mc.n_cells();
+    double acc[3] = {0.0, 0.0, 0.0};
+    node_cells(mc, c, lo, hi, [&](int cx, int cy, int a, int b) {
+        const int64_t cell = (int64_t)cy * mc.nside + cx;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += ev[(int64_t)(k * QQ + b * N1 + a) * nc + cell];
+    });
+    if (zero_cons) {
+        const uint8_t f = flags[c];
+        if (f & F_DIR) acc[0] = acc[1] = 0.0;
+        if (f & F_ACT) acc[2] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) xc[k * mc.n + c] = acc[k];
 }
 
 // rc[cons_c] = 0 (src/multigrid.py:338)
@@ -213,23 +268,50 @@ cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, do
     if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
     if (C.windowed()) return cudaErrorNotSupported;
     const Win wf = F.win();
-    cudaMemsetAsync(xc, 0, sizeof(double) * 3 * C.mesh.n, s);
-    count_launches(1);
     // coarse cell rows owning the window's fine rows (fine cell rows cyb-1 .. cye)
     const int nsc = C.mesh.nside;
     const int cyb = F.cy_begin(), cye = F.cy_end();
     const int lo = cyb > 0 ? (cyb - 1) / 2 : 0;
     const int hi = (cye / 2 + 1) < nsc ? cye / 2 + 1 : nsc;
+    if (zero_cons && !C.flags) return cudaErrorInvalidValue;
+    if (C.qcache) {   // element vectors in the coarse level's scratch + node gather
+        CellColour all;
+        all.c = 0;
+        all.hx = nsc;
+        all.cy0 = lo;
+        all.hy = hi - lo;
+        const unsigned g = (unsigned)(((int64_t)all.hx * all.hy + 127) / 128);
+        double* ev = C.ev();
+        switch (F.mesh.p) {
+            case 1: k_restrict<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+            case 2: k_restrict<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+            case 3: k_restrict<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+            case 4: k_restrict<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+            default: return cudaErrorInvalidValue;
+        }
+        const unsigned gn = blocks(C.mesh.n);
+        switch (F.mesh.p) {
+            case 1: k_restrict_gather<1><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
+            case 2: k_restrict_gather<2><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
+            case 3: k_restrict_gather<3><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
+            case 4: k_restrict_gather<4><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
+        }
+        count_launches(2);
+        return cudaGetLastError();
+    }
+    // no scratch bound to the coarse level: four colour passes into xc
+    cudaMemsetAsync(xc, 0, sizeof(double) * 3 * C.mesh.n, s);
+    count_launches(1);
     for (int c = 0; c < 4; ++c) {
         const CellColour col = make_colour(c, nsc, lo, hi);
         const int64_t cnt = (int64_t)col.hx * col.hy;
         if (cnt <= 0) continue;
         const unsigned g = (unsigned)((cnt + 127) / 128);
         switch (F.mesh.p) {
-            case 1: k_restrict<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
-            case 2: k_restrict<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
-            case 3: k_restrict<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
-            case 4: k_restrict<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col); break;
+            case 1: k_restrict<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col, nullptr); break;
+            case 2: k_restrict<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col, nullptr); break;
+            case 3: k_restrict<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col, nullptr); break;
+            case 4: k_restrict<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, col, nullptr); break;
             default: return cudaErrorInvalidValue;
         }
         count_launches(1);

@@ -308,7 +308,7 @@ class LinearizationState:
         (src/pff_operator.py:186-191 names; stored cell-fastest on device)."""
         self._check_cache()
         q, nc = self.shape.q, self.mesh.n_cells
-        qc = self._qcache.view(6, q, q, nc)
+        qc = self._qcache[:6 * q * q * nc].view(6, q, q, nc)
         names = ("e11", "e22", "e12", "gt", "dg", "pc")
         return {k: qc[i].permute(2, 0, 1) for i, k in enumerate(names)}
 
