@@ -127,6 +127,13 @@ int pff_diagonal(const pff_level* L, double* diag_uu, double* diag_pp, int inver
 int pff_residual(const pff_level* L, double* out, int mask_dirichlet, int mask_active,
                  void* stream);
 
+/* dense per-cell Jacobian matrices G_k (src/pff_operator.py:328-340 ->
+ * src/_kernels.py:754-826) for the assembled comparison path: gk holds
+ * n_cells x (3 (p+1)^2)^2 doubles, [cell][row][col], rows/cols ordered
+ * (u_x | u_y | phi) x local node b*(p+1)+a.  Needs a refreshed state; whole
+ * mesh only. */
+int pff_cell_matrices(const pff_level* L, double* gk, void* stream);
+
 /* lumped phi mass diagonal (src/active_set_solver.py:60-69 -> src/_kernels.py:828-843):
  * row sums of the scalar mass matrix over the level's local nodes; bitwise the
  * reference's summation order.  Needs no bound state. */

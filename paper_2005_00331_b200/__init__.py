@@ -14,11 +14,13 @@ from .mesh import DofMap, MeshHierarchy, MeshLevel, build_hierarchy
 from .multigrid import (ChebyshevConfig, GmgPreconditioner, TransferOperator,
                         build_prolongation, chebyshev_apply, estimate_lambda_max,
                         estimate_lambda_range)
-from .operator import (JacobianOperator, LinearizationState, StaleCacheError,
+from .operator import (AssemblyMemoryError, JacobianOperator, SparseOracle, assemble_oracle,
+                       cell_matrices, LinearizationState, StaleCacheError,
                        apply_block_phiphi, apply_block_uu, apply_jacobian, apply_phi_row,
                        block_diagonal, block_diagonals, extrapolate_phase, residual, restrict_state_to_level)
 
-from .simulation import (LoadRecord, ScenarioConfig, SimulationResult, apply_boundary_values,
-                         boundary_program, reaction_load, run_simulation)
+from .simulation import (BenchRecord, LoadRecord, MemoryReport, ScenarioConfig, SimulationResult,
+                         apply_boundary_values, benchmark_vmult, boundary_program, memory_report,
+                         reaction_load, run_simulation)
 
 __version__ = "0.1.0"

@@ -191,6 +191,13 @@ int pff_residual(const pff_level* h, double* out, int md, int ma, void* stream) 
     return check(pff::launch_residual(*L, out, md, ma, S(stream)), "pff_residual");
 }
 
+int pff_cell_matrices(const pff_level* h, double* gk, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_cell_matrices: state not bound");
+    if (!gk) return fail(PFF_E_ARG, "%s", "pff_cell_matrices: null output");
+    return check(pff::launch_cell_matrices(*L, gk, S(stream)), "pff_cell_matrices");
+}
+
 int pff_lumped_mass(const pff_level* h, double* out, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!L || !out) return fail(PFF_E_ARG, "%s", "pff_lumped_mass: null argument");

@@ -154,6 +154,9 @@ cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, 
 cudaError_t launch_residual(const Level& L, double* out, int mask_dirichlet, int mask_active,
                             cudaStream_t s);
 
+// dense per-cell matrices (pff_assemble.cu)
+cudaError_t launch_cell_matrices(const Level& L, double* gk, cudaStream_t s);
+
 // active-set loop (pff_active.cu)
 cudaError_t launch_lumped_mass(const Level& L, double* out, cudaStream_t s);
 cudaError_t launch_active_set(int64_t n, const double* rhs_phi, double* phi,

@@ -10,6 +10,10 @@ in libpff_b200.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import time
+import warnings
+from dataclasses import dataclass
+from functools import cached_property
 
 import numpy as np
 import torch
@@ -22,6 +26,11 @@ from .mesh import MeshHierarchy
 
 class StaleCacheError(RuntimeError):
     """Raised when the Jacobian is applied at an outdated linearization."""
+
+
+class AssemblyMemoryError(MemoryError):
+    """Raised when the assembled (sparse) Jacobian does not fit into memory
+    (src/pff_operator.py:28-29)."""
 
 
 def _dev():
@@ -467,6 +476,88 @@ def residual(state: LinearizationState, mask_dirichlet: bool = True, mask_active
     call("pff_residual", state.bind(), ptr(out), int(mask_dirichlet), int(mask_active),
          stream_handle())
     return out.cpu().numpy() if as_numpy else out
+
+
+# ------------------------------------------------------------ assembled path
+# the assembled Jacobian the paper compares the matrix-free
+# application against (src/pff_operator.py:199-205, 328-377), built on the device.
+
+@dataclass
+class SparseOracle:
+    """Assembled CSR Jacobian with identity constraint rows/columns.  ``device``
+    is a CUDA sparse-CSR tensor (cuSPARSE SpMV via ``matvec``); ``matrix`` a
+    scipy CSR copy on the host, made on first access (the reference's field)."""
+
+    device: torch.Tensor
+    state_version: int
+    assembly_seconds: float
+
+    @property
+    def shape(self):
+        return tuple(self.device.shape)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.device._nnz())
+
+    @cached_property
+    def matrix(self):
+        import scipy.sparse as sp
+        A = self.device
+        return sp.csr_matrix((A.values().cpu().numpy(), A.col_indices().cpu().numpy(),
+                              A.crow_indices().cpu().numpy()), shape=self.shape)
+
+    def matvec(self, x):
+        """A x (cuSPARSE); numpy in -> numpy out, CUDA tensor in -> CUDA out."""
+        xd, was_np = as_device(x, self.shape[1])
+        return back(torch.mv(self.device, xd), was_np)
+
+
+def cell_matrices(state: LinearizationState, as_numpy: bool = True):
+    """Dense local Jacobian matrices G_k of every cell, (n_cells, 3 nloc, 3 nloc)
+    (src/pff_operator.py:328-340), from ``pff_cell_matrices``."""
+    state._check_cache()
+    nl = 3 * state.dof_map.n_local
+    gk = torch.empty((state.mesh.n_cells, nl, nl), dtype=torch.float64, device=_dev())
+    call("pff_cell_matrices", state.bind(), ptr(gk), stream_handle())
+    return gk.cpu().numpy() if as_numpy else gk
+
+
+def assemble_oracle(state: LinearizationState) -> SparseOracle:
+    """Scatter the cellwise dense matrices into CSR with identity constraints
+    (src/pff_operator.py:343-377), entirely on the device; running out of
+    device memory raises :class:`AssemblyMemoryError`."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dm = state.dof_map
+    n, nloc = dm.n_scalar, dm.n_local
+    dev = _dev()
+    try:
+        gk = cell_matrices(state, as_numpy=False)
+        conn = torch.from_numpy(dm.conn).to(dev)
+        full = torch.cat([conn + c * n for c in range(3)], dim=1)         # (cells, 3 nloc)
+        rows = full.repeat_interleave(3 * nloc, dim=1).reshape(-1)
+        cols = full.repeat(1, 3 * nloc).reshape(-1)
+        vals = gk.reshape(-1)                                              # (cell, row, col)
+        del gk, full
+        mask = torch.from_numpy(state.constrained_mask()).to(dev)
+        keep = ~(mask[rows] | mask[cols])
+        rows, cols, vals = rows[keep], cols[keep], vals[keep]
+        cd = torch.nonzero(mask).reshape(-1)
+        idx = torch.stack([torch.cat([rows, cd]), torch.cat([cols, cd])])
+        del rows, cols, keep
+        vals = torch.cat([vals, torch.ones(cd.numel(), dtype=torch.float64, device=dev)])
+        with warnings.catch_warnings():   # torch flags sparse CSR as beta
+            warnings.simplefilter("ignore", UserWarning)
+            A = torch.sparse_coo_tensor(idx, vals, (3 * n, 3 * n),
+                                        check_invariants=False).coalesce().to_sparse_csr()
+        torch.cuda.synchronize()
+    except torch.cuda.OutOfMemoryError as exc:
+        raise AssemblyMemoryError(
+            f"sparse oracle at level {state.level}, degree {dm.degree} does not fit in "
+            "device memory") from exc
+    return SparseOracle(device=A, state_version=state.version,
+                        assembly_seconds=time.perf_counter() - t0)
 
 
 def restrict_state_to_level(state: LinearizationState, target: int) -> LinearizationState:

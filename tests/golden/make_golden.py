@@ -34,7 +34,7 @@ from fracturekit.multigrid import (ChebyshevConfig, GmgPreconditioner,  # noqa: 
 from fracturekit.active_set_solver import (ActiveSetParams, ActiveSetSolver,  # noqa: E402
                                            lumped_mass_diagonal)
 from fracturekit.simulation_driver import (ScenarioConfig, apply_boundary_values,  # noqa: E402
-                                           boundary_program, run_simulation)
+                                           boundary_program, memory_report, run_simulation)
 from fracturekit import io as ref_io  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -218,6 +218,27 @@ def simulation_case(scenario, level, degree, split, steps, du, vtk_every):
     return d
 
 
+def assembled_case(p, level, split, seed):
+    """cell_matrices / assemble_oracle (src/pff_operator.py:328-377)."""
+    h = build_hierarchy(max(level, 2), p)
+    st, x = make(h, level, split, seed)
+    d = inputs(st, x)
+    d["gk"] = op.cell_matrices(st)
+    mat = op.assemble_oracle(st).matrix
+    d["Ax"] = mat @ x
+    d["nnz"] = np.array([mat.nnz])
+    d["meta"] = np.array([p, level, seed, 1 if split == "miehe" else 0])
+    return d
+
+
+def memory_case():
+    rows = []
+    for level, degree in ((3, 2), (5, 1), (5, 4), (3, 4)):
+        rep = memory_report(ScenarioConfig(scenario="tension", level=level, degree=degree, steps=1))
+        rows.append([level, degree, rep.dofs, rep.csr_bytes])
+    return dict(rows=np.array(rows, dtype=np.int64))
+
+
 SIMULATION = {
     "sim_tension_p1_l3_miehe": ("tension", 3, 1, "miehe", 4, 1e-5, 2),
     "sim_shear_p2_l3_none": ("shear", 3, 2, "none", 3, 1e-5, 0),
@@ -226,6 +247,13 @@ SIMULATION = {
 
 
 def main():
+    if "--assembled" in sys.argv:   # only the assembled-path fixtures
+        for p, level, split, seed in ((2, 2, "miehe", 4), (2, 2, "none", 4), (1, 3, "miehe", 8),
+                                      (3, 2, "miehe", 2)):
+            np.savez_compressed(os.path.join(OUT, f"asm_p{p}_l{level}_{split}.npz"),
+                                **assembled_case(p, level, split, seed))
+        np.savez_compressed(os.path.join(OUT, "memory_report.npz"), **memory_case())
+        return
     if "--simulation" in sys.argv:   # only the run_simulation fixtures
         for name, args in SIMULATION.items():
             np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **simulation_case(*args))
