@@ -219,8 +219,8 @@ def run_ours(args):
     e2e_steps = max(3, min(20, args.steps))
     if ws == 1:
         xh = torch.from_numpy(x).pin_memory()
-        for _ in range(3):            # warm the pinned-buffer cache and the stream pool
-            P.apply_jacobian(st, xh)
+        for _ in range(3):            # warm the pinned-buffer cache with the timed loop's
+            yh = P.apply_jacobian(st, xh)   # pattern (previous result alive: two blocks)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
