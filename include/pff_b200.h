@@ -43,7 +43,10 @@ enum { PFF_FLAG_DIRICHLET = 1, PFF_FLAG_ACTIVE = 2 };
 
 /* vector layouts for the masking helpers */
 enum { PFF_LAYOUT_FULL = 0, PFF_LAYOUT_UU = 1, PFF_LAYOUT_PHI = 2 };
-enum { PFF_CONS_SELECT = 0, PFF_CONS_ZERO = 1, PFF_CONS_COPY = 2 };
+/* SELECT: z = cons ? r : 0;  ZERO: z[cons] = 0;  COPY: z[cons] = r[cons];
+ * EXCLUDE: z = cons ? 0 : r  (= r - G z0 for z0 = SELECT(r): the first smoother
+ * residual of a V-cycle level, without an operator application) */
+enum { PFF_CONS_SELECT = 0, PFF_CONS_ZERO = 1, PFF_CONS_COPY = 2, PFF_CONS_EXCLUDE = 3 };
 
 /* MaterialParams, src/material_model.py:20-44 */
 typedef struct {

@@ -252,7 +252,7 @@ int pff_inject_u8(const pff_level* f, const pff_level* c, const uint8_t* src, ui
 int pff_cons(const pff_level* h, int layout, int op, const double* r, double* z, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!L || !L->flags) return fail(PFF_E_UNBOUND, "%s", "pff_cons: flags not bound");
-    if (layout < 0 || layout > 2 || op < 0 || op > 2 || !z || (op != 1 && !r))
+    if (layout < 0 || layout > 2 || op < 0 || op > 3 || !z || (op != 1 && !r))
         return fail(PFF_E_ARG, "%s", "pff_cons: bad argument");
     return check(pff::launch_cons(*L, layout, op, r, z, S(stream)), "pff_cons");
 }

@@ -31,6 +31,8 @@ __global__ void k_cons(int64_t n, const uint8_t* __restrict__ flags, int layout,
         const bool cons = is_cons(f, layout, c);
         if (op == 0)
             z[k] = cons ? r[k] : 0.0;
+        else if (op == 3)
+            z[k] = cons ? 0.0 : r[k];
         else if (cons)
             z[k] = op == 1 ? 0.0 : r[k];
     }

@@ -183,9 +183,13 @@ class DistributedGmg:
                     self.fine.apply_into(mode, d, cr, cr)
         self._axpby(1.0, acc, 1.0, out)
 
-    def _smooth(self, z, r):
+    def _smooth(self, z, r, first=False):
         ln, W, c = self.fine.ln, self.w, self.cheb
-        self.fine.apply_into(_lib.MODE_FULL, z, W["res"], r)
+        if first:   # z = SELECT(r): the residual is r with constrained rows zeroed
+            call("pff_cons", self.fine.handle(), _lib.LAYOUT_FULL, _lib.CONS_EXCLUDE, ptr(r),
+                 ptr(W["res"]), stream_handle())
+        else:
+            self.fine.apply_into(_lib.MODE_FULL, z, W["res"], r)
         hi = self.ranges["uu"][1]
         self._cheb(_lib.MODE_UU, W["res"][:2 * ln], c.c * hi, c.C * hi, c.sweeps, z[:2 * ln])
         self.fine.apply_into(_lib.MODE_PHIROW, z, W["resphi"], r[2 * ln:])
@@ -197,7 +201,7 @@ class DistributedGmg:
         st = stream_handle()
         fh = self.fine.handle()
         call("pff_cons", fh, _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
-        self._smooth(z, r)
+        self._smooth(z, r, first=True)
         res = self.w["res"]
         self.fine.apply_into(_lib.MODE_FULL, z, res, r)
         ch = self.coarse_state.bind()

@@ -585,11 +585,17 @@ class GmgPreconditioner:
         if not assign:
             _axpby(1.0, acc, 1.0, out)
 
-    def _smooth(self, l, z, r):
+    def _smooth(self, l, z, r, first=False):
         s = self.states[l]
         n = s.n_scalar
         W = self._work[l]
-        s.apply_into(_lib.MODE_FULL, z, W.res, r)
+        if first:
+            # z = SELECT(r): r - G z is r with the constrained rows zeroed, exactly
+            # (identity rows/columns), so no operator application is needed
+            call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_EXCLUDE, ptr(r), ptr(W.res),
+                 stream_handle())
+        else:
+            s.apply_into(_lib.MODE_FULL, z, W.res, r)
         hi = self.ranges[l]["uu"][1]
         self._cheb(l, _lib.MODE_UU, W.res[:2 * n], self.cheb.c * hi, self.cheb.C * hi,
                    self.cheb.sweeps, z[:2 * n], False)
@@ -621,7 +627,7 @@ class GmgPreconditioner:
         W, Wc = self._work[l], self._work[l - 1]
         st = stream_handle()
         call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
-        self._smooth(l, z, r)
+        self._smooth(l, z, r, first=True)
         s.apply_into(_lib.MODE_FULL, z, W.res, r)
         call("pff_restrict", s.bind(), sc.bind(), ptr(W.res), ptr(Wc.r), 1, st)
         self._vcycle(l - 1, Wc.r, Wc.z)
