@@ -197,6 +197,17 @@ int pff_dot(int64_t n, const double* x, const double* y, double* partials, doubl
 int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* partials,
             double* h, void* stream);
 
+/* Arnoldi column j orthogonalised by low-synchronisation MGS (inverse
+ * compact-WY form of src/krylov.py:76-84): h[0..j] are the MGS coefficients,
+ * computed from V[0..j] . w and the Gram rows gram[i][k] = v_i . v_k (k < i,
+ * row-major, leading dimension ldg > j; row j is written by this call, rows
+ * < j must hold the earlier calls' rows of the same restart cycle); w is
+ * replaced by w - V h and h[j+1] = |w|.  Two passes over V instead of MGS's
+ * 2(j+1) dependent steps.  partials: (2 j + 3) * pff_reduce_scratch_len() / 2
+ * doubles. */
+int pff_mgs_lowsync(int64_t n, int j, const double* V, int64_t ldv, double* w, double* gram,
+                    int64_t ldg, double* partials, double* h, void* stream);
+
 /* multi-dot out[i] = V[i] . w for i < k (CGS2 orthogonalisation of the
  * distributed GMRES); partials = k * pff_reduce_scratch_len() / 2 doubles */
 int pff_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* partials,

@@ -54,6 +54,8 @@ SIGNATURES = {
     "pff_reduce_scratch_len": (_i64, []),
     "pff_dot": (_i, [_i64, _c_dp, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_mgs": (_i, [_i64, _i, _c_dp, _i64, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
+    "pff_mgs_lowsync": (_i, [_i64, _i, _c_dp, _i64, _c_dp, _c_dp, _i64, _c_dp, _c_dp,
+                             ctypes.c_void_p]),
     "pff_mdot": (_i, [_i64, _i, _c_dp, _i64, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_combine": (_i, [_i64, _i, _c_dp, _i64, _c_dp, _c_dp, _i, ctypes.c_void_p]),
 }

@@ -298,6 +298,14 @@ int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* p
     return check(pff::launch_mgs(n, j, V, ldv, w, partials, h, S(stream)), "pff_mgs");
 }
 
+int pff_mgs_lowsync(int64_t n, int j, const double* V, int64_t ldv, double* w, double* gram,
+                    int64_t ldg, double* partials, double* h, void* stream) {
+    if (n < 0 || j < 0 || j > 1023 || !V || !w || !gram || ldg <= j || !partials || !h || ldv < n)
+        return fail(PFF_E_ARG, "%s", "pff_mgs_lowsync: bad argument");
+    return check(pff::launch_lsmgs(n, j, V, ldv, w, gram, ldg, partials, h, S(stream)),
+                 "pff_mgs_lowsync");
+}
+
 int pff_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* partials,
              double* out, void* stream) {
     if (n < 0 || k < 0 || k > 4096 || !V || !w || !partials || !out || ldv < n)

@@ -191,6 +191,8 @@ cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part
                        double* out, cudaStream_t s);
 cudaError_t launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w,
                        double* partials, double* h, cudaStream_t s);
+cudaError_t launch_lsmgs(int64_t n, int j, const double* V, int64_t ldv, double* w,
+                         double* gram, int64_t ldg, double* partials, double* h, cudaStream_t s);
 cudaError_t launch_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w,
                         double* partials, double* out, cudaStream_t s);
 cudaError_t launch_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y,

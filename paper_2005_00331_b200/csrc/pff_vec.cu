@@ -147,9 +147,9 @@ k_mgs_step(int64_t n, const double* __restrict__ V, int64_t ldv, double* __restr
     if (threadIdx.x == 0) pout[blockIdx.x] = s;
 }
 
-// multi-dot: part[i][block] = sum over the block's elements of V[i] . w, 8 rows
-// of V per pass (w re-read once per 8 rows); fixed grid -> deterministic
-constexpr int MDOT_ROWS = 8;
+// multi-dot: part[i][block] = sum over the block's elements of V[i] . w, 4 rows
+// of V per pass (w re-read once per 4 rows); fixed grid -> deterministic
+constexpr int MDOT_ROWS = 4;   // 8 rows per pass halves the achieved bandwidth (tools/micro/ortho_micro.cu)
 __global__ void __launch_bounds__(RED_THREADS)
 k_mdot_partials(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
                 const double* __restrict__ w, double* __restrict__ part) {
@@ -177,6 +177,90 @@ __global__ void __launch_bounds__(RED_THREADS)
 k_mdot_final(const double* __restrict__ part, double* out) {
     const double s = reduce_partials(part + (int64_t)blockIdx.x * RED_BLOCKS);
     if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// Low-synchronisation MGS (inverse compact-WY form) for Arnoldi column j:
+// one pass computes r = V[0..j] . w and the new Gram row t = V[0..j-1] . V[j];
+// the MGS coefficients follow exactly from h_i = r_i - sum_{k<i} (v_i.v_k) h_k
+// (the recurrence MGS evaluates with updated w), then one pass forms
+// w -= V h and |w|^2.  4 basis rows per pass, fixed grid -> deterministic.
+__global__ void __launch_bounds__(RED_THREADS)
+k_lsmgs_partials(int64_t n, int j, const double* __restrict__ V, int64_t ldv,
+                 const double* __restrict__ w, double* __restrict__ part) {
+    const double* vj = V + (int64_t)j * ldv;
+    for (int i0 = 0; i0 <= j; i0 += MDOT_ROWS) {
+        double ar[MDOT_ROWS], at[MDOT_ROWS];
+#pragma unroll
+        for (int r = 0; r < MDOT_ROWS; ++r) ar[r] = at[r] = 0.0;
+        for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < n;
+             e += (int64_t)RED_BLOCKS * RED_THREADS) {
+            const double we = w[e], ve = vj[e];
+#pragma unroll
+            for (int r = 0; r < MDOT_ROWS; ++r)
+                if (i0 + r <= j) {
+                    const double vi = V[(int64_t)(i0 + r) * ldv + e];
+                    ar[r] = fma(vi, we, ar[r]);
+                    at[r] = fma(vi, ve, at[r]);
+                }
+        }
+#pragma unroll
+        for (int r = 0; r < MDOT_ROWS; ++r) {
+            if (i0 + r > j) break;
+            const double sr = block_sum(ar[r]);
+            const double st = block_sum(at[r]);
+            if (threadIdx.x == 0) {
+                part[(int64_t)(2 * (i0 + r)) * RED_BLOCKS + blockIdx.x] = sr;
+                part[(int64_t)(2 * (i0 + r) + 1) * RED_BLOCKS + blockIdx.x] = st;
+            }
+        }
+    }
+}
+
+// one block: finish the 2(j+1) sums (one warp per sum, fixed order), store
+// the Gram row j, forward-substitute h
+constexpr int SOLVE_THREADS = 1024;
+__global__ void __launch_bounds__(SOLVE_THREADS)
+k_lsmgs_solve(int j, const double* __restrict__ part, double* __restrict__ gram, int64_t ldg,
+              double* __restrict__ h) {
+    __shared__ double r[1024];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int q = wid; q < 2 * (j + 1); q += SOLVE_THREADS / 32) {
+        const double* p = part + (int64_t)q * RED_BLOCKS;
+        double v = 0.0;
+        for (int k = lane; k < RED_BLOCKS; k += 32) v += p[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+            const int i = q >> 1;
+            if ((q & 1) == 0) r[i] = v;
+            else if (i < j) gram[(int64_t)j * ldg + i] = v;   // v_j . v_i, i < j
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i <= j; ++i) {
+            double hi = r[i];
+            for (int k = 0; k < i; ++k) hi = fma(-gram[(int64_t)i * ldg + k], h[k], hi);
+            h[i] = hi;
+        }
+    }
+}
+
+// w -= sum_i h[i] V[i]; part = per-block |w|^2
+__global__ void __launch_bounds__(RED_THREADS)
+k_lsmgs_update(int64_t n, int j, const double* __restrict__ V, int64_t ldv,
+               const double* __restrict__ h, double* __restrict__ w, double* __restrict__ part) {
+    double v = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < n;
+         e += (int64_t)RED_BLOCKS * RED_THREADS) {
+        double acc = 0.0;
+        for (int i = 0; i <= j; ++i) acc = fma(h[i], V[(int64_t)i * ldv + e], acc);
+        const double we = w[e] - acc;
+        w[e] = we;
+        v = fma(we, we, v);
+    }
+    const double s = block_sum(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 // out = sum_i y[i] V[i]  (+ out)
@@ -248,6 +332,17 @@ cudaError_t launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w
     }
     k_reduce_final<<<1, RED_THREADS, 0, s>>>(pa, h + j + 1, 1);
     count_launches(j + 3);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lsmgs(int64_t n, int j, const double* V, int64_t ldv, double* w,
+                         double* gram, int64_t ldg, double* partials, double* h, cudaStream_t s) {
+    k_lsmgs_partials<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, j, V, ldv, w, partials);
+    k_lsmgs_solve<<<1, SOLVE_THREADS, 0, s>>>(j, partials, gram, ldg, h);
+    double* pn = partials + (int64_t)2 * (j + 1) * RED_BLOCKS;
+    k_lsmgs_update<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, j, V, ldv, h, w, pn);
+    k_reduce_final<<<1, RED_THREADS, 0, s>>>(pn, h + j + 1, 1);
+    count_launches(4);
     return cudaGetLastError();
 }
 
