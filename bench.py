@@ -309,6 +309,7 @@ def newton_step_ours(args, P, torch):
     dmask[dirn] = True
     rhs[np.concatenate([dmask, dmask, act])] = 0.0
     rhs_h = torch.from_numpy(rhs).pin_memory()
+    sol_h = torch.empty(rhs_h.numel(), dtype=torch.float64, pin_memory=True)
 
     def one():
         st = P.LinearizationState(h, level, params, split=args.split)
@@ -331,7 +332,7 @@ def newton_step_ours(args, P, torch):
         res = P.gmres_solve(P.JacobianOperator(st), rhs_d,
                             P.KrylovConfig(relative_tolerance=1e-8, restart=50),
                             preconditioner=gmg.apply)
-        res.solution.cpu()
+        sol_h.copy_(res.solution)             # D2H into pinned memory
         torch.cuda.synchronize()
         return res, t_setup, time.perf_counter() - t1
 
@@ -368,13 +369,14 @@ def newton_step_distributed(args, P, torch, ws, rank, dev):
                          device=dev)
     gmg.setup(params, args.split, U, pt, pt, act, dmask)
     rl_h = torch.from_numpy(gmg.part.scatter(rhs, rank, 3)).pin_memory()
+    sol_h = torch.empty(rl_h.numel(), dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
     dist.barrier()
     t_setup = time.perf_counter() - t0
     t1 = time.perf_counter()
     rl = rl_h.to(dev, non_blocking=True)
     res = distributed_gmres(gmg, rl, P.KrylovConfig(relative_tolerance=1e-8, restart=50))
-    sol = res.solution.cpu()
+    sol_h.copy_(res.solution)                 # D2H into pinned memory
     torch.cuda.synchronize()
     t_gmres = time.perf_counter() - t1
     t = torch.tensor([t_setup, t_gmres], device=dev)
