@@ -165,121 +165,175 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
     }
 }
 
+// Cooperative variant: p+1 lanes per cell (32/(p+1) cells per warp).  Lane t
+// owns node row b = t for the x-passes and Gauss column iq = t for the
+// y-passes and the q-point physics; the two transposes go through shared
+// memory.  Per-lane state is ~1/(p+1) of the thread-per-cell kernel, so high
+// orders neither spill nor thrash the instruction cache, and the latency of a
+// cell on the small multigrid levels drops by ~(p+1).  Same arithmetic
+// (src/_kernels.py:555-693), same element-vector output.
+constexpr int COOP_WARPS = 4;
+
 template <int P, bool MIEHE, int MODE>
-__global__ void __launch_bounds__(CELL_THREADS)
-k_apply_cells(Mesh m, Shape S, Material M, const double* __restrict__ qc,
-              const uint8_t* __restrict__ flags, const double* __restrict__ sx,
-              const double* __restrict__ sy, const double* __restrict__ sp,
-              double* __restrict__ ev) {
+__global__ void __launch_bounds__(32 * COOP_WARPS)
+k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
+             const uint8_t* __restrict__ flags, const double* __restrict__ sx,
+             const double* __restrict__ sy, const double* __restrict__ sp,
+             double* __restrict__ ev) {
     using T = ModeTraits<MODE>;
-    constexpr int N1 = P + 1, QQ = N1 * N1;
+    constexpr int N1 = P + 1, QQ = N1 * N1, CPW = 32 / N1;
+    constexpr int NA = 6;   // staged arrays per cell
+    __shared__ double buf[COOP_WARPS][CPW][NA][N1][N1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = lane / N1, t = lane - c * N1;
     const int64_t nc = m.n_cells();
-    const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= nc) return;
-    const int cx = (int)(cell % m.nside), cy = (int)(cell / m.nside);
-    int64_t gid[N1][N1];
-    uint8_t fl[N1][N1];
-    cell_ids<N1>(m, cx, cy, gid);
-#pragma unroll
-    for (int b = 0; b < N1; ++b)
-#pragma unroll
-        for (int a = 0; a < N1; ++a) fl[b][a] = flags[gid[b][a]];
-
-    double gxu[N1][N1], gyu[N1][N1], gxv[N1][N1], gyv[N1][N1];
-    double vp[N1][N1], gxp[N1][N1], gyp[N1][N1];
-    if (T::NEED_U) {
-        double c[N1][N1];
-#pragma unroll
-        for (int b = 0; b < N1; ++b)
-#pragma unroll
-            for (int a = 0; a < N1; ++a) c[b][a] = (fl[b][a] & F_DIR) ? 0.0 : sx[gid[b][a]];
-        grad_q<N1>(S, c, gxu, gyu);
-#pragma unroll
-        for (int b = 0; b < N1; ++b)
-#pragma unroll
-            for (int a = 0; a < N1; ++a) c[b][a] = (fl[b][a] & F_DIR) ? 0.0 : sy[gid[b][a]];
-        grad_q<N1>(S, c, gxv, gyv);
-    }
-    if (T::DO_PP) {
-        double c[N1][N1], tx[N1][N1], td[N1][N1];
-#pragma unroll
-        for (int b = 0; b < N1; ++b)
-#pragma unroll
-            for (int a = 0; a < N1; ++a) c[b][a] = (fl[b][a] & F_ACT) ? 0.0 : sp[gid[b][a]];
-        fwd_x<N1>(S.N, c, tx);
-        fwd_x<N1>(S.D, c, td);
-        fwd_y<N1>(S.N, tx, vp);
-        fwd_y<N1>(S.D, tx, gyp);
-        fwd_y<N1>(S.N, td, gxp);
-    }
-
+    const int64_t cell = ((int64_t)blockIdx.x * COOP_WARPS + warp) * CPW + c;
+    const bool on = c < CPW && cell < nc;
+    const int cx = on ? (int)(cell % m.nside) : 0, cy = on ? (int)(cell / m.nside) : 0;
     const double h = m.h, inv_h = 1.0 / h;
-    const int64_t fs = (int64_t)QQ * nc;
-    double s11[N1][N1], s22[N1][N1], s12[N1][N1], fv[N1][N1], fgx[N1][N1], fgy[N1][N1];
+    double (&B)[NA][N1][N1] = buf[warp][c < CPW ? c : 0];
+
+    // ---- phase 1: node row b = t, x-pass (value and derivative) per field
+    if (on) {
+        double ux[N1], uy[N1], up[N1];
 #pragma unroll
-    for (int jq = 0; jq < N1; ++jq)
+        for (int a = 0; a < N1; ++a) {
+            const int64_t g = m.node(cx, cy, a, t);
+            const uint8_t f = flags[g];
+            ux[a] = uy[a] = up[a] = 0.0;
+            if (T::NEED_U) {
+                ux[a] = (f & F_DIR) ? 0.0 : sx[g];
+                uy[a] = (f & F_DIR) ? 0.0 : sy[g];
+            }
+            if (T::DO_PP) up[a] = (f & F_ACT) ? 0.0 : sp[g];
+        }
 #pragma unroll
         for (int iq = 0; iq < N1; ++iq) {
+            double xn_u = 0.0, xd_u = 0.0, xn_v = 0.0, xd_v = 0.0, xn_p = 0.0, xd_p = 0.0;
+#pragma unroll
+            for (int a = 0; a < N1; ++a) {
+                const double na = S.N[iq][a], da = S.D[iq][a];
+                if (T::NEED_U) {
+                    xn_u = fma(na, ux[a], xn_u);
+                    xd_u = fma(da, ux[a], xd_u);
+                    xn_v = fma(na, uy[a], xn_v);
+                    xd_v = fma(da, uy[a], xd_v);
+                }
+                if (T::DO_PP) {
+                    xn_p = fma(na, up[a], xn_p);
+                    xd_p = fma(da, up[a], xd_p);
+                }
+            }
+            B[0][t][iq] = xn_u;
+            B[1][t][iq] = xd_u;
+            B[2][t][iq] = xn_v;
+            B[3][t][iq] = xd_v;
+            B[4][t][iq] = xn_p;
+            B[5][t][iq] = xd_p;
+        }
+    }
+    __syncwarp();
+    // ---- phase 2: Gauss column iq = t: y-pass, physics, backward y-pass
+    double X[NA][N1];
+#pragma unroll
+    for (int A = 0; A < NA; ++A)
+#pragma unroll
+        for (int b = 0; b < N1; ++b) X[A][b] = on ? B[A][b][t] : 0.0;
+    double Tr[NA][N1];   // uD uN vD vN pN pD
+#pragma unroll
+    for (int A = 0; A < NA; ++A)
+#pragma unroll
+        for (int b = 0; b < N1; ++b) Tr[A][b] = 0.0;
+    if (on) {
+        const int iq = t;
+        const int64_t fs = (int64_t)QQ * nc;
+#pragma unroll
+        for (int jq = 0; jq < N1; ++jq) {
+            double yn[NA], yd[NA];
+#pragma unroll
+            for (int A = 0; A < NA; ++A) {
+                double sn = 0.0, sd = 0.0;
+#pragma unroll
+                for (int b = 0; b < N1; ++b) {
+                    sn = fma(S.N[jq][b], X[A][b], sn);
+                    sd = fma(S.D[jq][b], X[A][b], sd);
+                }
+                yn[A] = sn;
+                yd[A] = sd;
+            }
             const double wq = S.w[jq] * S.w[iq];
             const double wg = wq * h, wv = wq * h * h;
             const double* q = qc + (int64_t)(jq * N1 + iq) * nc + cell;
-            double coup = 0.0;
+            double s11 = 0.0, s22 = 0.0, s12 = 0.0, coup = 0.0;
             if (T::NEED_U) {
-                double d11 = gxu[jq][iq] * inv_h;
-                double d22 = gyv[jq][iq] * inv_h;
-                double d12 = 0.5 * (gyu[jq][iq] + gxv[jq][iq]) * inv_h;
+                const double d11 = yn[1] * inv_h;                 // N_y (D_x u)
+                const double d22 = yd[2] * inv_h;                 // D_y (N_x v)
+                const double d12 = 0.5 * (yd[0] + yn[3]) * inv_h;
                 double ds11, ds22, ds12, spde;
                 dsig<MIEHE>(M.lam, M.mu, q[3 * fs], q[0], q[fs], q[2 * fs], d11, d22, d12, ds11,
                             ds22, ds12, spde);
                 coup = q[4 * fs] * spde;
+                s11 = ds11 * wg;
+                s22 = ds22 * wg;
+                s12 = ds12 * wg;
+            }
+            double fv = 0.0, fgx = 0.0, fgy = 0.0;
+            if (T::DO_PP) {
+                double pval = q[5 * fs] * yn[4];
+                if (T::DO_COUP) pval += coup;
+                fv = pval * wv;
+                fgx = M.gc * M.eps * yn[5] * inv_h * wg;
+                fgy = M.gc * M.eps * yd[4] * inv_h * wg;
+            }
+#pragma unroll
+            for (int b = 0; b < N1; ++b) {
+                const double nb = S.N[jq][b], db = S.D[jq][b];
                 if (T::DO_UU) {
-                    s11[jq][iq] = ds11 * wg;
-                    s22[jq][iq] = ds22 * wg;
-                    s12[jq][iq] = ds12 * wg;
+                    Tr[0][b] = fma(nb, s11, Tr[0][b]);
+                    Tr[1][b] = fma(db, s12, Tr[1][b]);
+                    Tr[2][b] = fma(nb, s12, Tr[2][b]);
+                    Tr[3][b] = fma(db, s22, Tr[3][b]);
+                }
+                if (T::DO_PP) {
+                    Tr[4][b] = fma(db, fgy, fma(nb, fv, Tr[4][b]));
+                    Tr[5][b] = fma(nb, fgx, Tr[5][b]);
                 }
             }
-            if (T::DO_PP) {
-                double pval = q[5 * fs] * vp[jq][iq];
-                if (T::DO_COUP) pval += coup;
-                fv[jq][iq] = pval * wv;
-                fgx[jq][iq] = M.gc * M.eps * gxp[jq][iq] * inv_h * wg;
-                fgy[jq][iq] = M.gc * M.eps * gyp[jq][iq] * inv_h * wg;
-            }
         }
-
-    double t[N1][N1];
-    if (T::DO_UU) {
-        double ru[N1][N1] = {}, rv[N1][N1] = {};
-        bwd_y<N1>(S.N, s11, t);
-        bwd_x_add<N1>(S.D, t, ru);
-        bwd_y<N1>(S.D, s12, t);
-        bwd_x_add<N1>(S.N, t, ru);
-        bwd_y<N1>(S.N, s12, t);
-        bwd_x_add<N1>(S.D, t, rv);
-        bwd_y<N1>(S.D, s22, t);
-        bwd_x_add<N1>(S.N, t, rv);
-#pragma unroll
-        for (int b = 0; b < N1; ++b)
-#pragma unroll
-            for (int a = 0; a < N1; ++a)
-            {
-                ev[(int64_t)(b * N1 + a) * nc + cell] = ru[b][a];
-                ev[(int64_t)(QQ + b * N1 + a) * nc + cell] = rv[b][a];
-            }
     }
-    if (T::DO_PP) {
-        double rp[N1][N1] = {};
-        bwd_y<N1>(S.N, fv, t);
-        bwd_x_add<N1>(S.N, t, rp);
-        bwd_y<N1>(S.N, fgx, t);
-        bwd_x_add<N1>(S.D, t, rp);
-        bwd_y<N1>(S.D, fgy, t);
-        bwd_x_add<N1>(S.N, t, rp);
+    __syncwarp();
+    if (on) {
 #pragma unroll
-        for (int b = 0; b < N1; ++b)
+        for (int A = 0; A < NA; ++A)
 #pragma unroll
-            for (int a = 0; a < N1; ++a)
-                ev[(int64_t)(2 * QQ + b * N1 + a) * nc + cell] = rp[b][a];
+            for (int b = 0; b < N1; ++b) B[A][b][t] = Tr[A][b];
+    }
+    __syncwarp();
+    // ---- phase 3: node row b = t, backward x-pass, element vectors
+    if (!on) return;
+    double Rr[NA][N1];
+#pragma unroll
+    for (int A = 0; A < NA; ++A)
+#pragma unroll
+        for (int iq = 0; iq < N1; ++iq) Rr[A][iq] = B[A][t][iq];
+#pragma unroll
+    for (int a = 0; a < N1; ++a) {
+        double ru = 0.0, rv = 0.0, rp = 0.0;
+#pragma unroll
+        for (int iq = 0; iq < N1; ++iq) {
+            const double na = S.N[iq][a], da = S.D[iq][a];
+            if (T::DO_UU) {
+                ru = fma(da, Rr[0][iq], fma(na, Rr[1][iq], ru));
+                rv = fma(da, Rr[2][iq], fma(na, Rr[3][iq], rv));
+            }
+            if (T::DO_PP) rp = fma(na, Rr[4][iq], fma(da, Rr[5][iq], rp));
+        }
+        const int loc = t * N1 + a;
+        if (T::DO_UU) {
+            ev[(int64_t)loc * nc + cell] = ru;
+            ev[(int64_t)(QQ + loc) * nc + cell] = rv;
+        }
+        if (T::DO_PP) ev[(int64_t)(2 * QQ + loc) * nc + cell] = rp;
     }
 }
 
@@ -511,28 +565,30 @@ struct ApplyL {
                            const double* rhs, cudaStream_t s) {
         const Mesh& m = L->mesh;
         const int64_t n = m.n;
-        const unsigned gi = grid_for(n, 256), gc = grid_for(m.n_cells(), CELL_THREADS);
+        const unsigned gi = grid_for(n, 256);
+        constexpr int CPB = COOP_WARPS * (32 / (P + 1));   // cells per block
+        const unsigned gc = grid_for(m.n_cells(), CPB);
         const double* q = L->qcache;
         const uint8_t* f = L->flags;
         double* ev = L->ev();
         switch (mode) {
             case MODE_FULL:
-                k_apply_cells<P, MIEHE, MODE_FULL><<<gc, CELL_THREADS, 0, s>>>(
+                k_apply_coop<P, MIEHE, MODE_FULL><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
                 k_apply_gather<P, MODE_FULL><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
                 break;
             case MODE_UU:
-                k_apply_cells<P, MIEHE, MODE_UU><<<gc, CELL_THREADS, 0, s>>>(
+                k_apply_coop<P, MIEHE, MODE_UU><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, src, src + n, nullptr, ev);
                 k_apply_gather<P, MODE_UU><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
                 break;
             case MODE_PHIPHI:
-                k_apply_cells<P, MIEHE, MODE_PHIPHI><<<gc, CELL_THREADS, 0, s>>>(
+                k_apply_coop<P, MIEHE, MODE_PHIPHI><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, nullptr, nullptr, src, ev);
                 k_apply_gather<P, MODE_PHIPHI><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
                 break;
             case MODE_PHIROW:
-                k_apply_cells<P, MIEHE, MODE_PHIROW><<<gc, CELL_THREADS, 0, s>>>(
+                k_apply_coop<P, MIEHE, MODE_PHIROW><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
                 k_apply_gather<P, MODE_PHIROW><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
                 break;

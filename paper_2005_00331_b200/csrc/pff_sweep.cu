@@ -1,6 +1,6 @@
 // pff_sweep.cu -- write-once Q2 operator kernel (the hot path).
 //
-// Same operator as k_apply_cells (src/_kernels.py:555-693 with the identity
+// Same operator as k_apply_coop (src/_kernels.py:555-693 with the identity
 // rows/columns of src/pff_operator.py:262-302), without atomics and with the
 // expensive, direction-independent q-point physics hoisted into refresh:
 //

@@ -19,10 +19,11 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--level", type=int, default=10)
 ap.add_argument("--generic", type=int, default=0)
 ap.add_argument("--rows", type=int, default=0)
+ap.add_argument("--degree", type=int, default=2)
 a = ap.parse_args()
 _lib.set_option(_lib.OPT_GENERIC_APPLY, a.generic)
 _lib.set_option(_lib.OPT_SWEEP_ROWS, a.rows)
-h, params, U, pt, act, dirn, x = bench.baseline_inputs(2, a.level, a.split)
+h, params, U, pt, act, dirn, x = bench.baseline_inputs(a.degree, a.level, a.split)
 st = P.LinearizationState(h, a.level, params, split=a.split)
 st.set_solution(U)
 st.set_phi_tilde(pt)

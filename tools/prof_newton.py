@@ -49,7 +49,7 @@ agg = defaultdict(lambda: [0, 0.0])
 for e in prof.events():
     if e.device_type == torch.autograd.DeviceType.CUDA:
         name = e.name
-        for key in ("k_sweep_q2", "k_apply_cells", "k_apply_init", "k_prolong", "k_restrict",
+        for key in ("k_sweep_q2", "k_apply_coop", "k_apply_gather", "k_prolong", "k_restrict",
                     "k_cheb_init", "k_cheb_step", "k_cons", "k_axpby", "k_mgs_step",
                     "k_dot_partials", "k_reduce_final", "k_combine", "k_div", "k_zero_cons3",
                     "Memset", "Memcpy", "k_mul"):
