@@ -93,7 +93,7 @@ struct Level {
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
     int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
     // element-vector scratch of the generic application and of the restriction
-    // into this level: 3 components x (p+1)^2 nodes per local cell
+    // into this level: [component][cell][local node], 3 x cells x (p+1)^2
     int64_t ev_len() const { return 3 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells(); }
     int64_t qcache_len() const { return generic_len() + tile_len() + ev_len(); }
     double* qtile() const { return qcache + generic_len(); }

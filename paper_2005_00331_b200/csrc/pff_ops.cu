@@ -156,7 +156,7 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
         const int64_t cell = (int64_t)cy * m.nside + cx;
 #pragma unroll
         for (int c = 0; c < NO; ++c)
-            acc[c] += ev[(int64_t)(comp[c] * QQ + b * N1 + a) * nc + cell];
+            acc[c] += ev[((int64_t)comp[c] * nc + cell) * QQ + b * N1 + a];
     });
 #pragma unroll
     for (int c = 0; c < NO; ++c) {
@@ -173,9 +173,12 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
 // cell on the small multigrid levels drops by ~(p+1).  Same arithmetic
 // (src/_kernels.py:555-693), same element-vector output.
 constexpr int COOP_WARPS = 4;
+#ifndef COOP_MIN_BLOCKS
+#define COOP_MIN_BLOCKS 3
+#endif
 
 template <int P, bool MIEHE, int MODE>
-__global__ void __launch_bounds__(32 * COOP_WARPS)
+__global__ void __launch_bounds__(32 * COOP_WARPS, COOP_MIN_BLOCKS)
 k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
              const uint8_t* __restrict__ flags, const double* __restrict__ sx,
              const double* __restrict__ sy, const double* __restrict__ sp,
@@ -330,10 +333,10 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
         }
         const int loc = t * N1 + a;
         if (T::DO_UU) {
-            ev[(int64_t)loc * nc + cell] = ru;
-            ev[(int64_t)(QQ + loc) * nc + cell] = rv;
+            ev[cell * QQ + loc] = ru;
+            ev[(nc + cell) * QQ + loc] = rv;
         }
-        if (T::DO_PP) ev[(int64_t)(2 * QQ + loc) * nc + cell] = rp;
+        if (T::DO_PP) ev[(2 * nc + cell) * QQ + loc] = rp;
     }
 }
 

@@ -105,7 +105,7 @@ __device__ __forceinline__ bool owned_fine(const Mesh& mf, const Win& wf, int64_
 }
 
 // ev == nullptr: colour pass (col) adding into xc; otherwise one pass over the
-// cells of rows [col.cy0, col.cy0 + col.hy) writing element vectors ev[k][my][mx][cell]
+// cells of rows [col.cy0, col.cy0 + col.hy) writing element vectors ev[k][cell][my][mx]
 template <int P>
 __global__ void __launch_bounds__(128)
 k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, double* xc,
@@ -171,7 +171,7 @@ k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, dou
             for (int my = 0; my < N1; ++my)
 #pragma unroll
                 for (int mx = 0; mx < N1; ++mx)
-                    ev[(int64_t)(k * QQ + my * N1 + mx) * nc + cell] = acc[k][my][mx];
+                    ev[((int64_t)k * nc + cell) * QQ + my * N1 + mx] = acc[k][my][mx];
         return;
     }
 #pragma unroll
@@ -197,7 +197,7 @@ __global__ void k_restrict_gather(Mesh mc, const double* __restrict__ ev, double
     node_cells(mc, c, lo, hi, [&](int cx, int cy, int a, int b) {
         const int64_t cell = (int64_t)cy * mc.nside + cx;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc[k] += ev[(int64_t)(k * QQ + b * N1 + a) * nc + cell];
+        for (int k = 0; k < 3; ++k) acc[k] += ev[((int64_t)k * nc + cell) * QQ + b * N1 + a];
     });
     if (zero_cons) {
         const uint8_t f = flags[c];
