@@ -126,6 +126,16 @@ int pff_apply_rows(const pff_level* L, int mode, const double* src, double* dst,
 int pff_diagonal(const pff_level* L, double* diag_uu, double* diag_pp, int invert,
                  void* stream);
 
+/* One Chebyshev smoothing step fused into the block application
+ * (src/multigrid.py:186-195): cr = rhs - G d (mode PFF_MODE_UU or
+ * PFF_MODE_PHIPHI, identity rows/columns as pff_apply; rhs may alias cr), then
+ * d_out = c1 d + c2 invd .* cr and acc += d_out, per entry in the same pass.
+ * d_out must not alias d.  Bitwise identical to pff_apply(mode, d, cr, rhs)
+ * followed by pff_cheb_step. */
+int pff_apply_cheb(const pff_level* L, int mode, const double* d, double* d_out,
+                   const double* rhs, double* cr, const double* invd, double* acc, double c1,
+                   double c2, void* stream);
+
 /* residual (src/pff_operator.py:218-241 -> src/_kernels.py:319-440), 3n */
 int pff_residual(const pff_level* L, double* out, int mask_dirichlet, int mask_active,
                  void* stream);

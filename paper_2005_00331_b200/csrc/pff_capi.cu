@@ -163,6 +163,18 @@ int pff_apply(const pff_level* h, int mode, const double* src, double* dst, cons
     return check(pff::launch_apply(*L, mode, src, dst, rhs, S(stream)), "pff_apply");
 }
 
+int pff_apply_cheb(const pff_level* h, int mode, const double* d, double* d_out,
+                   const double* rhs, double* cr, const double* invd, double* acc, double c1,
+                   double c2, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
+        return fail(PFF_E_UNBOUND, "%s", "pff_apply_cheb: state not bound");
+    if ((mode != 1 && mode != 2) || !d || !d_out || !rhs || !cr || !invd || !acc || d_out == d)
+        return fail(PFF_E_ARG, "%s", "pff_apply_cheb: mode must be UU or PHIPHI, d_out != d");
+    const pff::ChebArgs cb{invd, d_out, acc, c1, c2};
+    return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb");
+}
+
 int pff_apply_rows(const pff_level* h, int mode, const double* src, double* dst,
                    const double* rhs, int cy_begin, int cy_end, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);

@@ -64,6 +64,14 @@ struct Mesh {
     }
 };
 
+// Chebyshev smoother update d' = c1 d + c2 D^-1 r (src/multigrid.py:189-195),
+// one explicit rounding sequence shared by the standalone step and the
+// steps fused into the block applications (bitwise identical results)
+__device__ __forceinline__ double cheb_update(double c1, double d, double c2, double invd,
+                                             double r) {
+    return fma(c2, invd * r, c1 * d);
+}
+
 // ------------------------------------------------------------- physics
 // 2-D symmetric tensors as (11, 22, 12) triples; restated from
 // src/_kernels.py:26-123 (same branch structure, selects instead of ifs).

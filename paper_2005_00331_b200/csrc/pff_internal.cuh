@@ -133,6 +133,15 @@ __device__ __forceinline__ void node_cells(const Mesh& m, int64_t g, int row_lo,
     }
 }
 
+// a Chebyshev step fused into a block application (pff_apply_cheb): after
+// cr = cr - G d, d_out = c1 d + c2 invd cr and acc += d_out, per component
+struct ChebArgs {
+    const double* invd;
+    double* dout;
+    double* acc;
+    double c1, c2;
+};
+
 // options (pff_set_option)
 void set_generic_apply(bool on);
 void set_sweep_rows_per_chunk(int rows);
@@ -140,15 +149,16 @@ void set_sweep_rows_per_chunk(int rows);
 // Q2 sweep kernel (pff_sweep.cu)
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s);
 cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
-                               const double* rhs, cudaStream_t s, bool* handled);
+                               const double* rhs, cudaStream_t s, bool* handled,
+                               const ChebArgs* cheb = nullptr);
 cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src, double* dst,
                                     const double* rhs, int cy_begin, int cy_end, cudaStream_t s,
-                                    bool* handled);
+                                    bool* handled, const ChebArgs* cheb = nullptr);
 
 // operator family (pff_ops.cu)
 cudaError_t launch_refresh(const Level& L, cudaStream_t s);
 cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
-                         const double* rhs, cudaStream_t s);
+                         const double* rhs, cudaStream_t s, const ChebArgs* cheb = nullptr);
 cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, int invert,
                             cudaStream_t s);
 cudaError_t launch_residual(const Level& L, double* out, int mask_dirichlet, int mask_active,

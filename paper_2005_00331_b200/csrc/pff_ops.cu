@@ -136,7 +136,8 @@ struct ModeTraits {
 template <int P, int MODE>
 __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
                                const double* __restrict__ src, const double* __restrict__ rhs,
-                               const double* __restrict__ ev, double* __restrict__ dst) {
+                               const double* __restrict__ ev, double* __restrict__ dst,
+                               ChebArgs cheb) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t n = m.n, nc = m.n_cells();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -160,8 +161,15 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
     });
 #pragma unroll
     for (int c = 0; c < NO; ++c) {
-        const double v = cons[c] ? src[soff[c] * n + i] : acc[c];
-        dst[c * n + i] = rhs ? rhs[c * n + i] - v : v;
+        const double sv = src[soff[c] * n + i];
+        const double v = cons[c] ? sv : acc[c];
+        const double x = rhs ? rhs[c * n + i] - v : v;
+        dst[c * n + i] = x;
+        if (cheb.dout) {   // fused Chebyshev step on the residual just formed
+            const double dn = cheb_update(cheb.c1, sv, cheb.c2, cheb.invd[c * n + i], x);
+            cheb.dout[c * n + i] = dn;
+            cheb.acc[c * n + i] += dn;
+        }
     }
 }
 
@@ -565,7 +573,9 @@ struct RefreshL {
 template <int P, bool MIEHE>
 struct ApplyL {
     static cudaError_t run(const Level* L, int mode, const double* src, double* dst,
-                           const double* rhs, cudaStream_t s) {
+                           const double* rhs, cudaStream_t s, const ChebArgs* cheb) {
+        ChebArgs cb{nullptr, nullptr, nullptr, 0.0, 0.0};
+        if (cheb) cb = *cheb;
         const Mesh& m = L->mesh;
         const int64_t n = m.n;
         const unsigned gi = grid_for(n, 256);
@@ -578,22 +588,22 @@ struct ApplyL {
             case MODE_FULL:
                 k_apply_coop<P, MIEHE, MODE_FULL><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
-                k_apply_gather<P, MODE_FULL><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                k_apply_gather<P, MODE_FULL><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             case MODE_UU:
                 k_apply_coop<P, MIEHE, MODE_UU><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, src, src + n, nullptr, ev);
-                k_apply_gather<P, MODE_UU><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                k_apply_gather<P, MODE_UU><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             case MODE_PHIPHI:
                 k_apply_coop<P, MIEHE, MODE_PHIPHI><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, nullptr, nullptr, src, ev);
-                k_apply_gather<P, MODE_PHIPHI><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                k_apply_gather<P, MODE_PHIPHI><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             case MODE_PHIROW:
                 k_apply_coop<P, MIEHE, MODE_PHIROW><<<gc, 32 * COOP_WARPS, 0, s>>>(
                     m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
-                k_apply_gather<P, MODE_PHIROW><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst);
+                k_apply_gather<P, MODE_PHIROW><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             default:
                 return cudaErrorInvalidValue;
@@ -657,17 +667,19 @@ static bool g_generic_apply = false;
 void set_generic_apply(bool on) { g_generic_apply = on; }
 
 cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
-                         const double* rhs, cudaStream_t s) {
+                         const double* rhs, cudaStream_t s, const ChebArgs* cheb) {
     bool handled = false;
+    if (cheb && (!rhs || (mode != MODE_UU && mode != MODE_PHIPHI) || cheb->dout == src))
+        return cudaErrorInvalidValue;
     if (L.windowed()) {   // slabs run the write-once sweep kernel only
-        cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
+        cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled, cheb);
         return handled ? e : cudaErrorNotSupported;
     }
     if (!g_generic_apply) {
-        cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled);
+        cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled, cheb);
         if (handled || e != cudaSuccess) return e;
     }
-    return dispatch_p_split<ApplyL>(L.mesh.p, L.miehe, &L, mode, src, dst, rhs, s);
+    return dispatch_p_split<ApplyL>(L.mesh.p, L.miehe, &L, mode, src, dst, rhs, s, cheb);
 }
 
 cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, int invert,

@@ -69,10 +69,12 @@ struct Use {
     static constexpr int NF = slot(NFIELDS);
 };
 
-template <int NF, int NQ, int NRHS>
+template <int NF, int NQ, int NRHS, int NCH = 0>
 struct __align__(16) WarpSmem {
     double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
     double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];   // fused rhs of this lane's output nodes
+    double ib[6][NCH > 0 ? NCH : 1][SW_LANES];     // fused Chebyshev: D^-1 and acc of them
+    double ab[6][NCH > 0 ? NCH : 1][SW_LANES];
     double v[RING][NF][RW];                  // node-row ring
     uint8_t f[RING][FW];                     // flag rows
     int voff[RING][NF];                      // element offset of staged column 0
@@ -99,6 +101,11 @@ struct SweepArgs {
     double* dst[3];
     const double* src_out[3];
     const double* rhs[3];
+    // fused Chebyshev step (CHEB): dout = c1 src + c2 invd dst, acc += dout
+    const double* invd[3];
+    double* dout[3];
+    double* acc[3];
+    double c1, c2;
     int n_strips, rows_per_chunk, n_items;
     int cy_begin, cy_end;         // owned cell rows (window)
     int q_row0, q_rows;           // cell rows held by the tiled q-point cache
@@ -294,13 +301,13 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int MODE, bool MIEHE, bool FUSED>
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
 __global__ void __launch_bounds__(SW_LANES)
 k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
-    using Smem = WarpSmem<NF, NQ, FUSED ? NC : 0>;
+    using Smem = WarpSmem<NF, NQ, FUSED ? NC : 0, CHEB ? NC : 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -386,10 +393,20 @@ k_sweep_q2(const SweepArgs A) {
                 const int pc = U::DO_UU ? c : 2;
                 const bool cons = pc < 2 ? (f & F_DIR) : (f & F_ACT);
                 double x = v[pc];
-                if (cons) x = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k)
-                                        : A.src_out[c][gid];
+                // raw src value of this row (the identity row's entry, the Chebyshev d)
+                double sv = 0.0;
+                if (cons || CHEB)
+                    sv = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k) : A.src_out[c][gid];
+                if (cons) x = sv;
                 if (FUSED) x = (rbi >= 0 ? W.rb[rbi][c][lane] : A.rhs[c][gid]) - x;
                 A.dst[c][gid] = x;
+                if (CHEB) {
+                    const double iv = rbi >= 0 ? W.ib[rbi][c][lane] : A.invd[c][gid];
+                    const double av = rbi >= 0 ? W.ab[rbi][c][lane] : A.acc[c][gid];
+                    const double dn = cheb_update(A.c1, sv, A.c2, iv, x);
+                    A.dout[c][gid] = dn;
+                    A.acc[c][gid] = av + dn;
+                }
             }
         };
 
@@ -423,9 +440,14 @@ k_sweep_q2(const SweepArgs A) {
                 for (int b = 0; b < 2; ++b)
                     for (int a = 0; a < na_out; ++a)
 #pragma unroll
-                        for (int c = 0; c < NC; ++c)
-                            cp_async8(&W.rb[b * 3 + a][c][lane],
-                                      A.rhs[c] + (jb + b) * np1 + 2 * (int64_t)cx + a);
+                        for (int c = 0; c < NC; ++c) {
+                            const int64_t gi = (jb + b) * np1 + 2 * (int64_t)cx + a;
+                            cp_async8(&W.rb[b * 3 + a][c][lane], A.rhs[c] + gi);
+                            if (CHEB) {
+                                cp_async8(&W.ib[b * 3 + a][c][lane], A.invd[c] + gi);
+                                cp_async8(&W.ab[b * 3 + a][c][lane], A.acc[c] + gi);
+                            }
+                        }
             }
             cp_async_commit();
             mbar_wait(&W.bar[stage], (phase >> stage) & 1u);
@@ -684,12 +706,12 @@ struct LaunchCfg {
     int blocks_per_sm = 0;
 };
 
-template <int MODE, bool MIEHE, bool FUSED>
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? NC : 0>);
-    auto k = k_sweep_q2<MODE, MIEHE, FUSED>;
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? NC : 0, CHEB ? NC : 0>);
+    auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB>;
     static LaunchCfg cfg;
     static int n_sm = 0;
     if (!cfg.init) {
@@ -734,6 +756,15 @@ cudaError_t launch_split(int mode, SweepArgs& a, cudaStream_t s, int rows) {
     return cudaErrorInvalidValue;
 }
 
+template <bool MIEHE>
+cudaError_t launch_cheb(int mode, SweepArgs& a, cudaStream_t s, int rows) {
+    switch (mode) {
+        case MODE_UU: return launch_mode<MODE_UU, MIEHE, true, true>(a, s, rows);
+        case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, true, true>(a, s, rows);
+    }
+    return cudaErrorInvalidValue;
+}
+
 int g_rows_override = 0;
 
 }  // namespace
@@ -757,13 +788,14 @@ cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
 }
 
 cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
-                               const double* rhs, cudaStream_t s, bool* handled) {
-    return launch_sweep_apply_rows(L, mode, src, dst, rhs, -1, -1, s, handled);
+                               const double* rhs, cudaStream_t s, bool* handled,
+                               const ChebArgs* cheb) {
+    return launch_sweep_apply_rows(L, mode, src, dst, rhs, -1, -1, s, handled, cheb);
 }
 
 cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src, double* dst,
                                     const double* rhs, int cy_begin, int cy_end, cudaStream_t s,
-                                    bool* handled) {
+                                    bool* handled, const ChebArgs* cheb) {
     *handled = false;
     if (!L.sweep_ok()) return cudaSuccess;
     const Mesh& m = L.mesh;
@@ -826,6 +858,19 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         a.src_out[0] = (mode == MODE_PHIROW ? src + 2 * n : src) - sh;
         a.rhs[0] = rhs ? rhs - sh : nullptr;
     }
+    for (int c = 0; c < 3; ++c) { a.invd[c] = nullptr; a.dout[c] = nullptr; a.acc[c] = nullptr; }
+    a.c1 = a.c2 = 0.0;
+    if (cheb) {
+        if (!rhs || (mode != MODE_UU && mode != MODE_PHIPHI)) return cudaErrorInvalidValue;
+        const int nc = mode == MODE_UU ? 2 : 1;
+        for (int c = 0; c < nc; ++c) {
+            a.invd[c] = cheb->invd + c * n - sh;
+            a.dout[c] = cheb->dout + c * n - sh;
+            a.acc[c] = cheb->acc + c * n - sh;
+        }
+        a.c1 = cheb->c1;
+        a.c2 = cheb->c2;
+    }
     a.n_strips = L.n_strips();
     int rows = g_rows_override;
     if (rows <= 0) {
@@ -837,6 +882,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         rows = env_rows;
     }
     *handled = true;
+    if (cheb) return L.miehe ? launch_cheb<true>(mode, a, s, rows) : launch_cheb<false>(mode, a, s, rows);
     if (L.miehe)
         return rhs ? launch_split<true, true>(mode, a, s, rows)
                    : launch_split<true, false>(mode, a, s, rows);

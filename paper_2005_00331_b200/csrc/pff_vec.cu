@@ -54,7 +54,7 @@ __global__ void k_cheb_step(int64_t n, const double* __restrict__ invd,
                             double* __restrict__ d, double* __restrict__ acc) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double v = c1 * d[i] + c2 * (invd[i] * r[i]);
+    double v = cheb_update(c1, d[i], c2, invd[i], r[i]);
     d[i] = v;
     acc[i] += v;
 }

@@ -31,6 +31,8 @@ from .mesh import MeshHierarchy
 
 logger = logging.getLogger(__name__)
 
+FUSE_CHEB = True   # Chebyshev steps fused into the block applications (pff_apply_cheb)
+
 
 @dataclass
 class ChebyshevConfig:
@@ -379,6 +381,7 @@ class _LevelWork:
         self.res = _empty(3 * n)
         self.resphi = _empty(n)
         self.d = _empty(2 * n)
+        self.d2 = _empty(2 * n)     # ping-pong partner of d (fused Chebyshev steps)
         self.acc = _empty(2 * n)
         self.cr = _empty(2 * n)
 
@@ -572,7 +575,21 @@ class GmgPreconditioner:
         sigma1 = theta / delta
         st = stream_handle()
         call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0, st)
-        if sweeps > 1:
+        if sweeps > 1 and FUSE_CHEB:
+            # each step: cr = (rhs | cr) - G d, d' = c1 d + c2 D^-1 cr, acc += d' in ONE
+            # pass over the level (d ping-pongs between two buffers)
+            h = s.bind()
+            d_in, d_out = d, W.d2[:nb]
+            src = rhs
+            rho_old = 1.0 / sigma1
+            for k in range(1, sweeps):
+                rho = 1.0 / (2.0 * sigma1 - rho_old)
+                call("pff_apply_cheb", h, mode, ptr(d_in), ptr(d_out), ptr(src), ptr(cr),
+                     ptr(inv), ptr(acc), rho * rho_old, 2.0 * rho / delta, st)
+                rho_old = rho
+                src = cr
+                d_in, d_out = d_out, d_in
+        elif sweeps > 1:
             s.apply_into(mode, d, cr, rhs)
             rho_old = 1.0 / sigma1
             for k in range(1, sweeps):

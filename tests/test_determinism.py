@@ -78,3 +78,22 @@ def test_gmres_vcycle_bitwise_repeatable():
                             preconditioner=gmg.apply)
         sols.append((res.iterations, res.solution.clone()))
     assert sols[0][0] == sols[1][0] and torch.equal(sols[0][1], sols[1][1])
+
+
+@pytest.mark.parametrize("level,split", [(7, "miehe"), (7, "none"), (5, "miehe")])
+def test_fused_chebyshev_vcycle_bitwise_equal(level, split):
+    """pff_apply_cheb (Chebyshev steps fused into the block applications) gives
+    the same bits as pff_apply + pff_cheb_step."""
+    from paper_2005_00331_b200 import multigrid as MG
+    h, st, x, _ = state(2, level, split)
+    outs = []
+    for fuse in (False, True):
+        MG.FUSE_CHEB = fuse
+        try:
+            gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3),
+                                      use_graph=False)
+            gmg.setup(st)
+            outs.append(gmg.apply(torch.from_numpy(x).cuda()).clone())
+        finally:
+            MG.FUSE_CHEB = True
+    assert torch.equal(outs[0], outs[1])
