@@ -166,6 +166,22 @@ class HaloExchange:
         base = comp * self.ln
         return vec[base + (a - self.lo) * self.np1: base + (b - self.lo) * self.np1]
 
+    def overlappable(self, vec: torch.Tensor) -> bool:
+        """True when the exchange runs asynchronously on the device (NCCL)."""
+        return (self.part.world > 1 and vec.is_cuda
+                and dist.get_backend(self.group) != "gloo")
+
+    def start(self, vec: torch.Tensor, ncomp: int):
+        """Post the ghost-row sends/receives (NCCL); returns the work handles.
+        ``wait()`` on them orders the current stream after the transfers."""
+        ops = []
+        for c in range(ncomp):
+            for peer, a, b in self.recvs:
+                ops.append(dist.P2POp(dist.irecv, self._view(vec, c, a, b), peer, self.group))
+            for peer, a, b in self.sends:
+                ops.append(dist.P2POp(dist.isend, self._view(vec, c, a, b), peer, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
     def exchange(self, vec: torch.Tensor, ncomp: int):
         if self.part.world == 1:
             return
@@ -249,9 +265,22 @@ class SlabState:
     def apply_into(self, mode: int, src: torch.Tensor, dst: torch.Tensor,
                    rhs: torch.Tensor | None = None, exchange: bool = True):
         """dst(owned rows) = G src  (or rhs - G src); src ghost rows are
-        refreshed from the neighbours first."""
+        refreshed from the neighbours first.  With NCCL the exchange overlaps
+        the interior cell rows (they read owned node rows only); the two
+        boundary cell rows run once the ghost rows have arrived."""
         ncomp = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1,
                  _lib.MODE_PHIROW: 3}[mode]
+        c0, c1 = self.part.cells(self.rank)
+        if exchange and c1 - c0 >= 3 and self.halo.overlappable(src) \
+                and type(self)._local_apply is SlabState._local_apply:
+            works = self.halo.start(src, ncomp)
+            h, st = self.handle(), stream_handle()
+            call("pff_apply_rows", h, mode, ptr(src), ptr(dst), ptr(rhs), c0 + 1, c1 - 1, st)
+            for w in works:
+                w.wait()
+            call("pff_apply_rows", h, mode, ptr(src), ptr(dst), ptr(rhs), c0, c0 + 1, st)
+            call("pff_apply_rows", h, mode, ptr(src), ptr(dst), ptr(rhs), c1 - 1, c1, st)
+            return dst
         if exchange:
             self.halo.exchange(src, ncomp)
         self._local_apply(mode, src, dst, rhs)

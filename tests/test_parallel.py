@@ -203,3 +203,33 @@ def test_slab_window_kernel_matches_whole_mesh(split, world, level):
             part.gather_into(gotf, dst.cpu().numpy(), r, nout)
         assert max(block_rel(got, want.cpu().numpy(), n)) <= 1e-15, mode
         assert max(block_rel(gotf, wantf.cpu().numpy(), n)) <= 1e-15, mode
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 8])
+def test_overlapped_slab_decomposition_bitwise(world):
+    """The NCCL path of SlabState.apply_into runs the interior cell rows while
+    the ghost rows are in flight, then the two boundary rows: the three
+    pff_apply_rows launches must give exactly the single-launch result."""
+    import paper_2005_00331_b200 as P
+    from paper_2005_00331_b200._lib import call, ptr, stream_handle
+    level = 7
+    ost, x = O.baseline_state(2, level, "miehe", seed=6)
+    part = SlabPartition(2, level, world)
+    rhs = np.random.default_rng(3).standard_normal(3 * ost.n)
+    for r in range(world):
+        st = SlabState(part, r, ost.params, "miehe", ost.U, ost.phi_tilde, ost.active,
+                       ost.dirichlet)
+        st.refresh_cache()
+        src = torch.from_numpy(part.scatter(x, r, 3)).cuda()
+        rl = torch.from_numpy(part.scatter(rhs, r, 3)).cuda()
+        c0, c1 = part.cells(r)
+        for fused in (None, rl):
+            want = st.empty(3)
+            st.apply_into(0, src, want, fused, exchange=False)
+            got = st.empty(3)
+            h = st.handle()
+            for a, b in ((c0 + 1, c1 - 1), (c0, c0 + 1), (c1 - 1, c1)):
+                call("pff_apply_rows", h, 0, ptr(src), ptr(got), ptr(fused), a, b, stream_handle())
+            own = torch.from_numpy(np.tile(part.owned_mask(r), 3)).cuda()
+            assert torch.equal(got[own], want[own])
