@@ -329,21 +329,36 @@ def newton_step_ours(args, P, torch):
         t_setup = time.perf_counter() - t0
         t1 = time.perf_counter()
         rhs_d = rhs_h.to("cuda", non_blocking=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         res = P.gmres_solve(P.JacobianOperator(st), rhs_d,
                             P.KrylovConfig(relative_tolerance=1e-8, restart=50),
                             preconditioner=gmg.apply)
+        e1.record()
         sol_h.copy_(res.solution)             # D2H into pinned memory
         torch.cuda.synchronize()
-        return res, t_setup, time.perf_counter() - t1
+        return res, t_setup, time.perf_counter() - t1, e0.elapsed_time(e1) / 1e3
 
-    _, c_setup, c_gmres = one()
-    res, t_setup, t_gmres = one()
+    _, c_setup, c_gmres, _ = one()
+    res, t_setup, t_gmres, t_dev = one()
+    # HBM floor of the solve: per fine scalar node and GMRES
+    # iteration j, 2.53 kB for the V-cycle over all levels (sweeps=3), 81 B for
+    # the operator and 72 (j+2) B for orthogonalisation + normalisation
+    n = h.dof_map(level).n_scalar
+    floor_b = n * sum(2530 + 81 + 72 * (j % 50 + 2) for j in range(res.iterations))
+    peak, peak_src = peaks()
+    floor_s = floor_b / (peak * 1e9)
     return {"config": f"configs[3]: {2 ** level}^2 Q2 notch, levels 2..{level}, sweeps=3, "
                       "restart 50, rtol 1e-8",
             "split": args.split, "iterations": res.iterations, "converged": res.converged,
             "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
             "total_s": round(t_setup + t_gmres, 4),
             "cold_setup_s": round(c_setup, 4), "cold_gmres_s": round(c_gmres, 4),
+            "gmres_device_s": round(t_dev, 4),
+            "roofline": {"bound": "hbm", "floor_s": round(floor_s, 4),
+                         "frac": round(floor_s / t_dev, 3), "peak_gbs": peak,
+                         "model": "SURVEY.md 8(d) fused-minimum dataflow: per fine node and "
+                                  "iteration 2.53 kB V-cycle + 81 B operator + 72(j+2) B MGS"},
             "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
             "note": "second solve in the process (fresh state + preconditioner); gmres_s "
                     "includes the rhs H2D and solution D2H"}

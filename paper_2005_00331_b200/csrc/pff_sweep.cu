@@ -69,12 +69,12 @@ struct Use {
     static constexpr int NF = slot(NFIELDS);
 };
 
-template <int NF, int NQ, int NRHS, int NCH = 0>
+template <int NF, int NQ, int NRHS>
 struct __align__(16) WarpSmem {
     double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
-    double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];   // fused rhs of this lane's output nodes
-    double ib[6][NCH > 0 ? NCH : 1][SW_LANES];     // fused Chebyshev: D^-1 and acc of them
-    double ab[6][NCH > 0 ? NCH : 1][SW_LANES];
+    // fused form: rhs of this lane's output nodes [0, NC); with a fused
+    // Chebyshev step also D^-1 [NC, 2 NC) and acc [2 NC, 3 NC)
+    double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];
     double v[RING][NF][RW];                  // node-row ring
     uint8_t f[RING][FW];                     // flag rows
     int voff[RING][NF];                      // element offset of staged column 0
@@ -307,7 +307,7 @@ k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
-    using Smem = WarpSmem<NF, NQ, FUSED ? NC : 0, CHEB ? NC : 0>;
+    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -401,8 +401,8 @@ k_sweep_q2(const SweepArgs A) {
                 if (FUSED) x = (rbi >= 0 ? W.rb[rbi][c][lane] : A.rhs[c][gid]) - x;
                 A.dst[c][gid] = x;
                 if (CHEB) {
-                    const double iv = rbi >= 0 ? W.ib[rbi][c][lane] : A.invd[c][gid];
-                    const double av = rbi >= 0 ? W.ab[rbi][c][lane] : A.acc[c][gid];
+                    const double iv = rbi >= 0 ? W.rb[rbi][NC + c][lane] : A.invd[c][gid];
+                    const double av = rbi >= 0 ? W.rb[rbi][2 * NC + c][lane] : A.acc[c][gid];
                     const double dn = cheb_update(A.c1, sv, A.c2, iv, x);
                     A.dout[c][gid] = dn;
                     A.acc[c][gid] = av + dn;
@@ -444,8 +444,8 @@ k_sweep_q2(const SweepArgs A) {
                             const int64_t gi = (jb + b) * np1 + 2 * (int64_t)cx + a;
                             cp_async8(&W.rb[b * 3 + a][c][lane], A.rhs[c] + gi);
                             if (CHEB) {
-                                cp_async8(&W.ib[b * 3 + a][c][lane], A.invd[c] + gi);
-                                cp_async8(&W.ab[b * 3 + a][c][lane], A.acc[c] + gi);
+                                cp_async8(&W.rb[b * 3 + a][NC + c][lane], A.invd[c] + gi);
+                                cp_async8(&W.rb[b * 3 + a][2 * NC + c][lane], A.acc[c] + gi);
                             }
                         }
             }
@@ -710,7 +710,7 @@ template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? NC : 0, CHEB ? NC : 0>);
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0>);
     auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB>;
     static LaunchCfg cfg;
     static int n_sm = 0;
