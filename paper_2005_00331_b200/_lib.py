@@ -126,7 +126,14 @@ def require_cuda():
                            "there is no CPU fallback")
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle() -> int:
+    """cudaStream_t of torch's current stream on the current device (the
+    stream every entry point is ordered on)."""
+    if _raw_stream is not None:   # the same query without torch's Python device plumbing
+        return _raw_stream(torch._C._cuda_getDevice())
     return torch.cuda.current_stream().cuda_stream
 
 

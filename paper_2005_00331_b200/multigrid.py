@@ -324,6 +324,22 @@ def start_vector(seed: int, n: int) -> np.ndarray:
     return _START[(seed, n)].result()
 
 
+_START_DEV: dict = {}
+
+
+def start_vector_device(seed: int, n: int, device) -> torch.Tensor:
+    """The seeded start vector (numpy's generator, as the reference) kept on
+    the device across setups; callers get their own copy."""
+    key = (seed, n, str(device))
+    t = _START_DEV.get(key)
+    if t is None:
+        t = torch.from_numpy(start_vector(seed, n)).pin_memory().to(device, non_blocking=True)
+        _START_DEV[key] = t
+        while len(_START_DEV) > 64:
+            _START_DEV.pop(next(iter(_START_DEV)))
+    return t.clone()
+
+
 class _LanczosRun:
     """One estimate_lambda_range run split at its two reductions."""
 
@@ -331,8 +347,7 @@ class _LanczosRun:
         self.level, self.block, self.fn = level, block, fn
         self.n = diag.numel()
         self.dhalf = 1.0 / torch.sqrt(diag)
-        v_h = start_vector(seed, self.n)
-        self.v = torch.from_numpy(v_h).to(diag.device)
+        self.v = start_vector_device(seed, self.n, diag.device)
         self.v_prev = torch.zeros_like(self.v)
         self.tmp = torch.empty_like(self.v)
         self.w = None
@@ -350,12 +365,14 @@ class _LanczosRun:
         call("pff_mul", self.n, ptr(self.dhalf), ptr(self.w), ptr(self.w), st)
         _axpby(-self.beta, self.v_prev, 1.0, self.w)
 
-    def step_b(self, alpha):
+    def step_b(self, alpha, ritz=True):
         _axpby(-alpha, self.v, 1.0, self.w)
         self.alphas.append(alpha)
-        ritz = (scipy.linalg.eigvalsh_tridiagonal(self.alphas, self.betas) if self.betas
-                else np.array([alpha]))
-        self.lo, self.hi = float(ritz[0]), float(ritz[-1])
+        if ritz:
+            r = (scipy.linalg.eigvalsh_tridiagonal(self.alphas, self.betas) if self.betas
+                 else np.array([alpha]))
+            self.lo, self.hi = float(r[0]), float(r[-1])
+
 
     def step_c(self, beta):
         self.beta = beta
@@ -372,6 +389,26 @@ class _LanczosRun:
         call("pff_div", self.n, ptr(self.v), None, beta, ptr(self.v), stream_handle())
         if self.left <= 0:
             self.done = True
+
+
+def _ritz_batched(runs):
+    """Extreme Ritz values of several Lanczos tridiagonals at once (runs in
+    lockstep have equal sizes): one batched dense eigvalsh per size instead of
+    one tridiagonal solve per run."""
+    by_k: dict = {}
+    for r in runs:
+        by_k.setdefault(len(r.alphas), []).append(r)
+    for k, group in by_k.items():
+        T = np.zeros((len(group), k, k))
+        idx = np.arange(k)
+        for g, r in enumerate(group):
+            T[g, idx, idx] = r.alphas
+            if k > 1:
+                T[g, idx[1:], idx[:-1]] = r.betas
+                T[g, idx[:-1], idx[1:]] = r.betas
+        ev = np.linalg.eigvalsh(T)
+        for g, r in enumerate(group):
+            r.lo, r.hi = float(ev[g, 0]), float(ev[g, -1])
 
 
 class _LevelWork:
@@ -512,9 +549,10 @@ class GmgPreconditioner:
                 call("pff_dot", r.n, ptr(r.v), ptr(r.w), ptr(partials[i * plen:]), ptr(out[i:]), st)
             alphas = out.cpu().numpy()
             for i in act:
-                runs[i].step_b(float(alphas[i]))
+                runs[i].step_b(float(alphas[i]), ritz=False)
                 r = runs[i]
                 call("pff_dot", r.n, ptr(r.w), ptr(r.w), ptr(partials[i * plen:]), ptr(out[i:]), st)
+            _ritz_batched([runs[i] for i in act])
             norms2 = out.cpu().numpy()
             for i in act:
                 runs[i].step_c(float(np.sqrt(norms2[i])))

@@ -75,24 +75,43 @@ class _Dual:
     it in place, as the reference's own code does), so the next device use
     re-uploads; device writes mark the host side stale."""
 
-    def __init__(self, n: int, dtype, fill):
-        self._h = np.full(n, fill, dtype=dtype)
+    def __init__(self, n: int, dtype, fill, tail=None):
+        self._n, self._dtype, self._fill = n, dtype, fill
+        self._tail = tail       # (start, value): entries [start:] start as value
+        self._h = None          # host array, made on first host access
         self._d = None
         self._host_new = True
         self._dev_new = False
         self.stamp = 0   # bumped on every (possible) modification
 
+    def _tdtype(self):
+        return torch.bool if self._dtype is bool else torch.from_numpy(
+            np.empty(0, dtype=self._dtype)).dtype
+
+    def _host_array(self) -> np.ndarray:
+        if self._h is None:
+            self._h = np.full(self._n, self._fill, dtype=self._dtype)
+            if self._tail is not None:
+                self._h[self._tail[0]:] = self._tail[1]
+        return self._h
+
     def host(self) -> np.ndarray:
         if self._dev_new:
             self._h = self._d.cpu().numpy().copy()
             self._dev_new = False
+        self._host_array()
         self._host_new = True
         self.stamp += 1
         return self._h
 
     def device(self) -> torch.Tensor:
         if self._d is None:
-            self._d = torch.from_numpy(self._h).to(_dev())
+            if self._h is None:     # never touched on the host: fill on the device
+                self._d = torch.full((self._n,), self._fill, dtype=self._tdtype(), device=_dev())
+                if self._tail is not None:
+                    self._d[self._tail[0]:] = self._tail[1]
+            else:
+                self._d = torch.from_numpy(self._h).to(_dev())
             self._host_new = False
         elif self._host_new:
             self._d.copy_(torch.from_numpy(self._h))
@@ -101,7 +120,9 @@ class _Dual:
 
     def set(self, value, index=None):
         if isinstance(value, torch.Tensor) and value.is_cuda and index is None:
-            d = self.device() if self._d is None else self._d
+            if self._d is None:
+                self._d = torch.empty(self._n, dtype=self._tdtype(), device=value.device)
+            d = self._d
             d.copy_(value.reshape(-1).to(d.dtype))
             self._host_new, self._dev_new = False, True
             self.stamp += 1
@@ -141,8 +162,7 @@ class LinearizationState:
         self.mesh = hierarchy.level(level)
         self.shape: ShapeData = shape_data(hierarchy.degree)
         n = self.dof_map.n_scalar
-        self._U = _Dual(3 * n, np.float64, 0.0)
-        self._U.host()[2 * n:] = 1.0
+        self._U = _Dual(3 * n, np.float64, 0.0, tail=(2 * n, 1.0))   # u = 0, phi = 1
         self._pt = _Dual(n, np.float64, 1.0)
         self._po = _Dual(n, np.float64, 1.0)
         self._act = _Dual(n, bool, False)
