@@ -87,7 +87,9 @@ struct Level {
     // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
     // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
-    bool sweep_ok() const { return mesh.p == 2 && mesh.nside >= 64 && q2_struct; }
+    bool sweep_ok() const {   // the sweep kernel stages with 32-bit node indices
+        return mesh.p == 2 && mesh.nside >= 64 && q2_struct && mesh.n < (int64_t(1) << 31);
+    }
     int n_strips() const { return (mesh.nside + 30) / 31; }
     int tile_nq() const { return miehe ? 10 : 5; }   // tangent (6 | 1) + coupling (3) + pc
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }

@@ -324,6 +324,13 @@ k_sweep_q2(const SweepArgs A) {
     }
     __syncwarp();
     unsigned phase = 0u;   // bit s: parity of the next completion of mbarrier s
+    // staging arithmetic in 32-bit elements (n < 2^31 is checked on the host):
+    // 16-byte misalignment of each staged field's base, in elements / bytes
+    const int np1i = (int)np1;
+    int fmis[NFIELDS];
+#pragma unroll
+    for (int f = 0; f < NFIELDS; ++f) fmis[f] = (int)(((uintptr_t)A.fld[f] >> 3) & 1);
+    const int flmis = (int)((uintptr_t)A.flags & 15);
 
     for (int item = blockIdx.x; item < A.n_items; item += gridDim.x) {
         const int strip = item % A.n_strips, chunk = item / A.n_strips;
@@ -335,29 +342,30 @@ k_sweep_q2(const SweepArgs A) {
         const bool active = cx >= 0 && cx < ns;
         const bool owner = lane > 0 && active;
         const int64_t gcol0 = 2 * (int64_t)(x0 - 1);
+        const int gc0 = 2 * (x0 - 1);                              // staged column 0
+        const int lo_c = gc0 < 0 ? 0 : gc0, hi_c = min(np1i, gc0 + SW_COLS);
 
-        // lane 0: stage node row j into ring slot `slot` (all used fields + flags)
-        auto issue_row = [&](int64_t j, unsigned long long* bar) -> unsigned {
-            const int slot = (int)(j % RING);
-            const int64_t lo = j * np1 + (gcol0 < 0 ? 0 : gcol0);
-            const int64_t hi = j * np1 + min((int64_t)np1, gcol0 + SW_COLS);
+        // lane 0: stage node row j into ring slot j % RING (all used fields +
+        // flags), 16-byte aligned bulk copies
+        auto issue_row = [&](int j, unsigned long long* bar) -> unsigned {
+            const int slot = j % RING;
+            const int rowb = j * np1i;
+            const int lo = rowb + lo_c, hi = rowb + hi_c;
             unsigned bytes = 0;
 #pragma unroll
             for (int f = 0; f < NFIELDS; ++f) {
                 if (!U::used(f)) continue;
-                const uintptr_t base = (uintptr_t)A.fld[f];
-                const uintptr_t a = (base + 8 * lo) & ~(uintptr_t)15;
-                const uintptr_t b = (base + 8 * hi + 15) & ~(uintptr_t)15;
-                bulk_g2s(W.v[slot][U::slot(f)], (const void*)a, (unsigned)(b - a), bar);
-                W.voff[slot][U::slot(f)] = (int)(((intptr_t)(base + 8 * (j * np1 + gcol0)) - (intptr_t)a) / 8);
-                bytes += (unsigned)(b - a);
+                const int ae = lo - ((lo + fmis[f]) & 1);
+                const int be = hi + ((hi + fmis[f]) & 1);
+                bulk_g2s(W.v[slot][U::slot(f)], A.fld[f] + ae, (unsigned)(8 * (be - ae)), bar);
+                W.voff[slot][U::slot(f)] = rowb + gc0 - ae;
+                bytes += (unsigned)(8 * (be - ae));
             }
-            const uintptr_t fb = (uintptr_t)A.flags;
-            const uintptr_t a = (fb + lo) & ~(uintptr_t)15;
-            const uintptr_t b = (fb + hi + 15) & ~(uintptr_t)15;
-            bulk_g2s(W.f[slot], (const void*)a, (unsigned)(b - a), bar);
-            W.foff[slot] = (int)((intptr_t)(fb + j * np1 + gcol0) - (intptr_t)a);
-            return bytes + (unsigned)(b - a);
+            const int ab = lo - ((lo + flmis) & 15);
+            const int bb = hi + ((16 - ((hi + flmis) & 15)) & 15);
+            bulk_g2s(W.f[slot], A.flags + ab, (unsigned)(bb - ab), bar);
+            W.foff[slot] = rowb + gc0 - ab;
+            return bytes + (unsigned)(bb - ab);
         };
         auto issue_qblock = [&](int cy, int stage) -> unsigned {
             const double* src =
@@ -421,7 +429,7 @@ k_sweep_q2(const SweepArgs A) {
             if (more && lane == 0) {
                 fence_proxy_async();
                 const bool first = cy < cstart;
-                const int64_t j0 = first ? jb + 2 : jb + 3;
+                const int j0 = first ? 2 * cy + 2 : 2 * cy + 3;
                 unsigned bytes = 0;
 #pragma unroll 1
                 for (int t = 0; t < (first ? 3 : 2); ++t) bytes += issue_row(j0 + t, &W.bar[nstage]);
@@ -452,7 +460,7 @@ k_sweep_q2(const SweepArgs A) {
             cp_async_commit();
             mbar_wait(&W.bar[stage], (phase >> stage) & 1u);
             phase ^= 1u << stage;
-            const int s0 = (int)(jb % RING), s1 = (int)((jb + 1) % RING), s2 = (int)((jb + 2) % RING);
+            const int s0 = (2 * cy) % RING, s1 = (2 * cy + 1) % RING, s2 = (2 * cy + 2) % RING;
             const bool slit_row = m.level >= 1 && cy == half;
             if (slit_row) {
                 __syncwarp();
