@@ -251,4 +251,56 @@ __device__ __forceinline__ void bwd_x_add(const double (&M)[NMAX][NMAX],
         }
 }
 
+// Miehe tangent with the state eigensystem given as (m, +-r, c, s):
+// ev1 = m + r, ev2 = m - r, tr e = 2m (bit-identical to src/_kernels.py:28-33),
+// the gap test of _dpos2s (line 66) is the sign of the stored r.
+struct MieheQ {
+    Eig e;
+    double tre;
+    bool gap_ok;
+};
+__device__ __forceinline__ MieheQ miehe_q(double m, double rs, double c, double s) {
+    MieheQ q;
+    const double r = fabs(rs);
+    q.e.ev1 = m + r;
+    q.e.ev2 = m - r;
+    q.e.c = c;
+    q.e.s = s;
+    q.tre = 2.0 * m;
+    q.gap_ok = rs > 0.0;
+    return q;
+}
+
+__device__ __forceinline__ void miehe_dsig(const Material& M, double g, const MieheQ& q,
+                                           double d11, double d22, double d12, double& s11,
+                                           double& s22, double& s12, double& spde) {
+    const double c = q.e.c, s = q.e.s, lam = M.lam, mu = M.mu;
+    const double t0 = d11 * c + d12 * s;
+    const double t1 = d12 * c + d22 * s;
+    const double dl1 = c * t0 + s * t1;
+    const double dl2 = s * s * d11 - 2.0 * s * c * d12 + c * c * d22;
+    const double dl1p = q.e.ev1 >= 0.0 ? dl1 : 0.0;
+    const double dl2p = q.e.ev2 >= 0.0 ? dl2 : 0.0;
+    const double l1p = posp(q.e.ev1), l2p = posp(q.e.ev2);
+    const double alpha = q.gap_ok ? (c * t1 - s * t0) / (q.e.ev1 - q.e.ev2) : 0.0;
+    const double rot = alpha * (l1p - l2p);
+    const double o11 = dl1p * c * c + dl2p * s * s - 2.0 * rot * s * c;
+    const double o22 = dl1p * s * s + dl2p * c * c + 2.0 * rot * s * c;
+    const double o12 = (dl1p - dl2p) * c * s + rot * (c * c - s * s);
+    const double trde = d11 + d22;
+    const double tt = q.tre < 0.0 ? 0.0 : trde;
+    const double dp11 = lam * tt + 2.0 * mu * o11;
+    const double dp22 = lam * tt + 2.0 * mu * o22;
+    const double dp12 = 2.0 * mu * o12;
+    const double f11 = lam * trde + 2.0 * mu * d11;
+    const double f22 = lam * trde + 2.0 * mu * d22;
+    const double f12 = 2.0 * mu * d12;
+    double sp11, sp22, sp12;
+    sigplus2(lam, mu, q.tre, q.e, sp11, sp22, sp12);
+    spde = sp11 * d11 + sp22 * d22 + 2.0 * sp12 * d12;
+    s11 = g * dp11 + (f11 - dp11);
+    s22 = g * dp22 + (f22 - dp22);
+    s12 = g * dp12 + (f12 - dp12);
+}
+
 }  // namespace pff

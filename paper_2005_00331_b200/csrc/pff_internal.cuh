@@ -97,9 +97,15 @@ struct Level {
     // element-vector scratch of the generic application and of the restriction
     // into this level: [component][cell][local node], 3 x cells x (p+1)^2
     int64_t ev_len() const { return 3 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells(); }
-    int64_t qcache_len() const { return generic_len() + tile_len() + ev_len(); }
+    // weighted tangent cache of the generic application (Miehe levels without
+    // the sweep kernel): [T00 T01 T02 T11 T12 T22 cw0 cw1 cw2 pc][k][cell]
+    int64_t gtan_len() const {
+        return miehe && !sweep_ok() ? 10 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells() : 0;
+    }
+    int64_t qcache_len() const { return generic_len() + tile_len() + gtan_len() + ev_len(); }
     double* qtile() const { return qcache + generic_len(); }
-    double* ev() const { return qcache + generic_len() + tile_len(); }
+    double* gtan() const { return qcache + generic_len() + tile_len(); }
+    double* ev() const { return qcache + generic_len() + tile_len() + gtan_len(); }
 };
 
 // Cells containing scalar node g (global id) in increasing cell index, with

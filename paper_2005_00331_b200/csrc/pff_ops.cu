@@ -121,6 +121,47 @@ k_refresh(Mesh m, Win w, Shape S, Material M, const double* __restrict__ U,
         }
 }
 
+// Weighted tangent cache of the generic path (Miehe): the reference's
+// cache_tensors quantities (src/_kernels.py:517-548) per (q-point, cell) from
+// the q-point cache, weight w_jq w_iq h^2 folded in; symmetric form
+// (ds11, ds22, 2 ds12) = T (d11, d22, d12) as in the Q2 tiles (pff_sweep.cu)
+template <int P>
+__global__ void k_refresh_gtan(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc,
+                               double* __restrict__ gt) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t nc = w.ncell, fs = (int64_t)QQ * nc;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= fs) return;
+    const int k = (int)(t / nc);
+    const int jq = k / N1, iq = k - jq * N1;
+    const double h = m.h, wv = S.w[jq] * S.w[iq] * h * h;
+    const double* q = qc + t;
+    const double e11 = q[0], e22 = q[fs], e12 = q[2 * fs], g = q[3 * fs], dg = q[4 * fs];
+    const double tre = e11 + e22;
+    const double mm = 0.5 * (e11 + e22), dh = 0.5 * (e11 - e22);
+    const double r = sqrt(dh * dh + e12 * e12);
+    const Eig e = eig2(e11, e22, e12);
+    const bool gap_ok = (e.ev1 - e.ev2) > 1e-12 * scale2(e11, e22, e12);
+    const MieheQ mq = miehe_q(mm, gap_ok ? r : -r, e.c, e.s);
+    double Mc[3][3], sp;
+    miehe_dsig(M, g, mq, 1.0, 0.0, 0.0, Mc[0][0], Mc[1][0], Mc[2][0], sp);
+    miehe_dsig(M, g, mq, 0.0, 1.0, 0.0, Mc[0][1], Mc[1][1], Mc[2][1], sp);
+    miehe_dsig(M, g, mq, 0.0, 0.0, 1.0, Mc[0][2], Mc[1][2], Mc[2][2], sp);
+    double q11, q22, q12;
+    sigplus2(M.lam, M.mu, tre, e, q11, q22, q12);
+    double* o = gt + t;
+    o[0] = wv * Mc[0][0];
+    o[fs] = wv * 0.5 * (Mc[0][1] + Mc[1][0]);
+    o[2 * fs] = wv * 0.5 * (Mc[0][2] + 2.0 * Mc[2][0]);
+    o[3 * fs] = wv * Mc[1][1];
+    o[4 * fs] = wv * 0.5 * (Mc[1][2] + 2.0 * Mc[2][1]);
+    o[5 * fs] = wv * 2.0 * Mc[2][2];
+    o[6 * fs] = wv * dg * q11;
+    o[7 * fs] = wv * dg * q22;
+    o[8 * fs] = wv * dg * 2.0 * q12;
+    o[9 * fs] = wv * q[5 * fs];
+}
+
 // ----------------------------------------------------- Jacobian (generic)
 template <int MODE>
 struct ModeTraits {
@@ -185,12 +226,12 @@ constexpr int COOP_WARPS = 4;
 #define COOP_MIN_BLOCKS 3
 #endif
 
-template <int P, bool MIEHE, int MODE>
+template <int P, bool MIEHE, int MODE, bool TC = false>
 __global__ void __launch_bounds__(32 * COOP_WARPS, COOP_MIN_BLOCKS)
 k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
              const uint8_t* __restrict__ flags, const double* __restrict__ sx,
              const double* __restrict__ sy, const double* __restrict__ sp,
-             double* __restrict__ ev) {
+             double* __restrict__ ev, const double* __restrict__ gt) {
     using T = ModeTraits<MODE>;
     constexpr int N1 = P + 1, QQ = N1 * N1, CPW = 32 / N1;
     constexpr int NA = 6;   // staged arrays per cell
@@ -276,10 +317,22 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
             const double wg = wq * h, wv = wq * h * h;
             const double* q = qc + (int64_t)(jq * N1 + iq) * nc + cell;
             double s11 = 0.0, s22 = 0.0, s12 = 0.0, coup = 0.0;
-            if (T::NEED_U) {
-                const double d11 = yn[1] * inv_h;                 // N_y (D_x u)
-                const double d22 = yd[2] * inv_h;                 // D_y (N_x v)
-                const double d12 = 0.5 * (yd[0] + yn[3]) * inv_h;
+            const double d11 = yn[1] * inv_h;                 // N_y (D_x u)
+            const double d22 = yd[2] * inv_h;                 // D_y (N_x v)
+            const double d12 = 0.5 * (yd[0] + yn[3]) * inv_h;
+            const double* g = TC ? gt + (int64_t)(jq * N1 + iq) * nc + cell : nullptr;
+            if (T::NEED_U && TC) {
+                // cached weighted tangent (x wv); the backward passes expect x wg = wv / h
+                if (T::DO_UU) {
+                    const double t00 = g[0], t01 = g[fs], t02 = g[2 * fs];
+                    const double t11 = g[3 * fs], t12 = g[4 * fs], t22 = g[5 * fs];
+                    s11 = fma(t00, d11, fma(t01, d22, t02 * d12)) * inv_h;
+                    s22 = fma(t01, d11, fma(t11, d22, t12 * d12)) * inv_h;
+                    s12 = 0.5 * fma(t02, d11, fma(t12, d22, t22 * d12)) * inv_h;
+                }
+                if (T::DO_COUP)
+                    coup = fma(g[6 * fs], d11, fma(g[7 * fs], d22, g[8 * fs] * d12));   // x wv
+            } else if (T::NEED_U) {
                 double ds11, ds22, ds12, spde;
                 dsig<MIEHE>(M.lam, M.mu, q[3 * fs], q[0], q[fs], q[2 * fs], d11, d22, d12, ds11,
                             ds22, ds12, spde);
@@ -290,9 +343,14 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
             }
             double fv = 0.0, fgx = 0.0, fgy = 0.0;
             if (T::DO_PP) {
-                double pval = q[5 * fs] * yn[4];
-                if (T::DO_COUP) pval += coup;
-                fv = pval * wv;
+                if (TC) {
+                    fv = g[9 * fs] * yn[4];
+                    if (T::DO_COUP) fv += coup;
+                } else {
+                    double pval = q[5 * fs] * yn[4];
+                    if (T::DO_COUP) pval += coup;
+                    fv = pval * wv;
+                }
                 fgx = M.gc * M.eps * yn[5] * inv_h * wg;
                 fgy = M.gc * M.eps * yd[4] * inv_h * wg;
             }
@@ -566,6 +624,12 @@ struct RefreshL {
         k_refresh<P, MIEHE><<<grid_for(w.ncell, CELL_THREADS), CELL_THREADS, 0, s>>>(
             m, w, L->shape, L->mat, L->U, L->phi_tilde, L->qcache);
         count_launches(1);
+        if (L->gtan_len() > 0) {
+            const int64_t nq = (int64_t)(P + 1) * (P + 1) * w.ncell;
+            k_refresh_gtan<P><<<grid_for(nq, 256), 256, 0, s>>>(m, w, L->shape, L->mat, L->qcache,
+                                                               L->gtan());
+            count_launches(1);
+        }
         return cudaGetLastError();
     }
 };
@@ -584,25 +648,27 @@ struct ApplyL {
         const double* q = L->qcache;
         const uint8_t* f = L->flags;
         double* ev = L->ev();
+        const bool tc = MIEHE && L->gtan_len() > 0;
+        const double* gt = tc ? L->gtan() : nullptr;
         switch (mode) {
             case MODE_FULL:
-                k_apply_coop<P, MIEHE, MODE_FULL><<<gc, 32 * COOP_WARPS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
+                (tc ? k_apply_coop<P, MIEHE, MODE_FULL, true> : k_apply_coop<P, MIEHE, MODE_FULL, false>)<<<gc, 32 * COOP_WARPS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev, gt);
                 k_apply_gather<P, MODE_FULL><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             case MODE_UU:
-                k_apply_coop<P, MIEHE, MODE_UU><<<gc, 32 * COOP_WARPS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, src, src + n, nullptr, ev);
+                (tc ? k_apply_coop<P, MIEHE, MODE_UU, true> : k_apply_coop<P, MIEHE, MODE_UU, false>)<<<gc, 32 * COOP_WARPS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, nullptr, ev, gt);
                 k_apply_gather<P, MODE_UU><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             case MODE_PHIPHI:
-                k_apply_coop<P, MIEHE, MODE_PHIPHI><<<gc, 32 * COOP_WARPS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, nullptr, nullptr, src, ev);
+                (tc ? k_apply_coop<P, MIEHE, MODE_PHIPHI, true> : k_apply_coop<P, MIEHE, MODE_PHIPHI, false>)<<<gc, 32 * COOP_WARPS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, nullptr, nullptr, src, ev, gt);
                 k_apply_gather<P, MODE_PHIPHI><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             case MODE_PHIROW:
-                k_apply_coop<P, MIEHE, MODE_PHIROW><<<gc, 32 * COOP_WARPS, 0, s>>>(
-                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev);
+                (tc ? k_apply_coop<P, MIEHE, MODE_PHIROW, true> : k_apply_coop<P, MIEHE, MODE_PHIROW, false>)<<<gc, 32 * COOP_WARPS, 0, s>>>(
+                    m, L->shape, L->mat, q, f, src, src + n, src + 2 * n, ev, gt);
                 k_apply_gather<P, MODE_PHIROW><<<gi, 256, 0, s>>>(m, f, src, rhs, ev, dst, cb);
                 break;
             default:
