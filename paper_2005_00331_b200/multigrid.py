@@ -419,7 +419,6 @@ class _LevelWork:
         self.resphi = _empty(n)
         self.d = _empty(2 * n)
         self.d2 = _empty(2 * n)     # ping-pong partner of d (fused Chebyshev steps)
-        self.acc = _empty(2 * n)
         self.cr = _empty(2 * n)
 
 
@@ -608,11 +607,14 @@ class GmgPreconditioner:
         nb = rhs.numel()
         inv = self._inv[l][0 if mode == _lib.MODE_UU else 1]
         d, cr = W.d[:nb], W.cr[:nb]
-        acc = out if assign else W.acc[:nb]
+        # the smoothing increments accumulate straight into `out` (z += sum of the
+        # Chebyshev updates; assign: z = sum) -- no separate accumulator pass
+        acc = out
         theta, delta = 0.5 * (b + a), 0.5 * (b - a)
         sigma1 = theta / delta
         st = stream_handle()
-        call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0, st)
+        call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0 if assign else 1,
+             st)
         if sweeps > 1 and FUSE_CHEB:
             # each step: cr = (rhs | cr) - G d, d' = c1 d + c2 D^-1 cr, acc += d' in ONE
             # pass over the level (d ping-pongs between two buffers)
@@ -637,8 +639,6 @@ class GmgPreconditioner:
                 rho_old = rho
                 if k < sweeps - 1:
                     s.apply_into(mode, d, cr, cr)
-        if not assign:
-            _axpby(1.0, acc, 1.0, out)
 
     def _smooth(self, l, z, r, first=False):
         s = self.states[l]
