@@ -166,6 +166,43 @@ __global__ void __launch_bounds__(RT) upd_u4(long n, int k, const double* V, lon
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// update U5: rows in chunks of 8 with independent partial sums, 2 elements per thread
+__global__ void __launch_bounds__(RT) upd_u5(long n, int k, const double* V, long ldv, const double* h, double* w, double* part) {
+    __shared__ double hs[1024];
+    for (int i = threadIdx.x; i < k; i += RT) hs[i] = h[i];
+    __syncthreads();
+    double v = 0.0;
+    const long stride = (long)gridDim.x * RT;
+    for (long e = (long)blockIdx.x * RT + threadIdx.x; e < n; e += 2 * stride) {
+        const long e2 = e + stride;
+        const bool two = e2 < n;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        int i = 0;
+        for (; i + 1 < k; i += 2) {
+            const double h0 = hs[i], h1 = hs[i + 1];
+            const double* r0 = V + (long)i * ldv;
+            const double* r1 = r0 + ldv;
+            a0 = fma(h0, r0[e], a0);
+            a1 = fma(h1, r1[e], a1);
+            if (two) { b0 = fma(h0, r0[e2], b0); b1 = fma(h1, r1[e2], b1); }
+        }
+        if (i < k) {
+            a0 = fma(hs[i], V[(long)i * ldv + e], a0);
+            if (two) b0 = fma(hs[i], V[(long)i * ldv + e2], b0);
+        }
+        const double we = w[e] - (a0 + a1);
+        w[e] = we;
+        v = fma(we, we, v);
+        if (two) {
+            const double we2 = w[e2] - (b0 + b1);
+            w[e2] = we2;
+            v = fma(we2, we2, v);
+        }
+    }
+    const double s = block_sum(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 int main() {
     const long n = 12598275, ldv = (n + 63) / 64 * 64, n2 = ldv / 2;
     const int m = 31;
@@ -195,6 +232,8 @@ int main() {
         const double dv = k + 2, uv = k + 2;
         timeit("dots v1 R=4", k, dv, [&] { dots_v1<4><<<RB, RT>>>(n, k, V, ldv, w, V, part); });
         timeit("upd u1", k, uv, [&] { upd_u1<<<RB, RT>>>(n, k, V, ldv, h, w, part); });
+        timeit("upd u5 (2 elem, 2 chains)", k, uv, [&] { upd_u5<<<RB, RT>>>(n, k, V, ldv, h, w, part); });
+        timeit("upd u5 x2 grid", k, uv, [&] { upd_u5<<<2 * RB, RT>>>(n, k, V, ldv, h, w, part); });
         timeit("upd u3 R=4", k, uv, [&] { upd_u3<4><<<RB, RT>>>(n, k, V, ldv, h, w, part); });
         timeit("upd u3 R=2", k, uv, [&] { upd_u3<2><<<RB, RT>>>(n, k, V, ldv, h, w, part); });
         timeit("upd u3 R=4 x2 grid", k, uv, [&] { upd_u3<4><<<2 * RB, RT>>>(n, k, V, ldv, h, w, part); });
