@@ -196,6 +196,20 @@ int pff_div(int64_t n, const double* x, const double* sdev, double sval, double*
             void* stream);
 int pff_mul(int64_t n, const double* a, const double* x, double* y, void* stream);
 
+/* Lanczos range estimates of several block operators at once
+ * (src/multigrid.py:123-162 for every level and block of GmgPreconditioner,
+ * 259-275): run r applies mode modes[r] (PFF_MODE_UU or PFF_MODE_PHIPHI) of
+ * levels[r] scaled by dhalf[r] = diag^-1/2 (ns[r] entries) for at most
+ * max_iterations steps; work[r] holds 4 ns[r] doubles whose first ns[r] are the
+ * start vector on entry.  The runs advance in lockstep (two host
+ * synchronisations per round); lo_hi (host, 2 nruns) receives the extreme Ritz
+ * values; partials: nruns * pff_reduce_scratch_len() doubles, dots: nruns
+ * doubles (device).  Synchronises the stream. */
+int pff_lanczos_ranges(int nruns, const pff_level* const* levels, const int* modes,
+                       const int64_t* ns, const double* const* dhalf, double* const* work,
+                       int max_iterations, double* lo_hi, double* partials, double* dots,
+                       void* stream);
+
 /* deterministic dot: partials = pff_reduce_scratch_len() doubles, out = 1 double */
 int64_t pff_reduce_scratch_len(void);
 int pff_dot(int64_t n, const double* x, const double* y, double* partials, double* out,

@@ -296,6 +296,25 @@ int pff_mul(int64_t n, const double* a, const double* x, double* y, void* stream
     return check(pff::launch_lanczos_scale(n, a, x, y, S(stream)), "pff_mul");
 }
 
+int pff_lanczos_ranges(int nruns, const pff_level* const* levels, const int* modes,
+                       const int64_t* ns, const double* const* dhalf, double* const* work,
+                       int max_iterations, double* lo_hi, double* partials, double* dots,
+                       void* stream) {
+    if (nruns < 0 || (nruns > 0 && (!levels || !modes || !ns || !dhalf || !work || !lo_hi ||
+                                    !partials || !dots)))
+        return fail(PFF_E_ARG, "%s", "pff_lanczos_ranges: bad argument");
+    for (int r = 0; r < nruns; ++r) {
+        const Level* L = reinterpret_cast<const Level*>(levels[r]);
+        if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_lanczos_ranges: state not bound");
+        if ((modes[r] != 1 && modes[r] != 2) || !dhalf[r] || !work[r] || ns[r] <= 0)
+            return fail(PFF_E_ARG, "%s", "pff_lanczos_ranges: bad run");
+    }
+    return check(pff::lanczos_ranges(nruns, reinterpret_cast<const Level* const*>(levels), modes,
+                                     ns, dhalf, work, max_iterations, lo_hi, partials, dots,
+                                     S(stream)),
+                 "pff_lanczos_ranges");
+}
+
 int64_t pff_reduce_scratch_len(void) { return 2 * pff::RED_BLOCKS; }
 
 int pff_dot(int64_t n, const double* x, const double* y, double* partials, double* out,

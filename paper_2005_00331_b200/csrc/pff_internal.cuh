@@ -218,4 +218,10 @@ cudaError_t launch_combine(int64_t n, int k, const double* V, int64_t ldv, const
 cudaError_t launch_lanczos_scale(int64_t n, const double* dhalf, const double* v, double* out,
                                  cudaStream_t s);
 
+// batched Lanczos range estimates (pff_lanczos.cu)
+cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* modes,
+                           const int64_t* ns, const double* const* dhalf, double* const* work,
+                           int max_it, double* lo_hi, double* partials, double* dots,
+                           cudaStream_t s);
+
 }  // namespace pff

@@ -32,6 +32,7 @@ from .mesh import MeshHierarchy
 logger = logging.getLogger(__name__)
 
 FUSE_CHEB = True   # Chebyshev steps fused into the block applications (pff_apply_cheb)
+NATIVE_LANCZOS = True   # setup's batched Lanczos driven by pff_lanczos_ranges (C++)
 
 
 @dataclass
@@ -522,6 +523,8 @@ class GmgPreconditioner:
         independent, so each round launches the work of all active runs and
         synchronises once per reduction instead of once per run (identical
         per-run algebra: src/multigrid.py:123-162, 259-275)."""
+        if NATIVE_LANCZOS:
+            return self._estimate_ranges_native(levels)
         cfg = self.cheb
         runs = []
         for l in levels:
@@ -560,6 +563,39 @@ class GmgPreconditioner:
             hi = max(r.hi, 1e-30)
             lo = max(r.lo, cfg.lambda_min_floor * hi)
             res.setdefault(r.level, {})[r.block] = (lo, hi)
+        return res
+
+    def _estimate_ranges_native(self, levels):
+        """Same runs as the Python path, the loop inside libpff_b200."""
+        cfg = self.cheb
+        descs = []
+        for l in levels:
+            s = self.states[l]
+            s._check_cache()
+            n = s.n_scalar
+            for blk, mode, nb in (("uu", _lib.MODE_UU, 2 * n), ("phiphi", _lib.MODE_PHIPHI, n)):
+                diag = self.diags[l][blk]
+                work = torch.empty(4 * nb, dtype=torch.float64, device=diag.device)
+                work[:nb].copy_(start_vector_device(cfg.seed + 101 * l + (0 if blk == "uu" else 1),
+                                                    nb, diag.device))
+                descs.append((l, blk, s.bind(), mode, nb, 1.0 / torch.sqrt(diag), work))
+        R = len(descs)
+        dev = descs[0][6].device
+        plen = _lib.load().pff_reduce_scratch_len()
+        partials = torch.empty(R * plen, dtype=torch.float64, device=dev)
+        dots = torch.empty(R, dtype=torch.float64, device=dev)
+        lo_hi = np.zeros(2 * R)
+        arr = lambda ctype, vals: (ctype * R)(*vals)  # noqa: E731
+        call("pff_lanczos_ranges", R, arr(ctypes.c_void_p, [d[2].value for d in descs]),
+             arr(ctypes.c_int, [d[3] for d in descs]), arr(ctypes.c_int64, [d[4] for d in descs]),
+             arr(ctypes.c_void_p, [d[5].data_ptr() for d in descs]),
+             arr(ctypes.c_void_p, [d[6].data_ptr() for d in descs]), cfg.lanczos_iterations,
+             lo_hi.ctypes.data, ptr(partials), ptr(dots), stream_handle())
+        res = {}
+        for r, d in enumerate(descs):
+            hi = max(float(lo_hi[2 * r + 1]), 1e-30)
+            lo = max(float(lo_hi[2 * r]), cfg.lambda_min_floor * hi)
+            res.setdefault(d[0], {})[d[1]] = (lo, hi)
         return res
 
     # -- linear operator ---------------------------------------------------------

@@ -97,3 +97,24 @@ def test_fused_chebyshev_vcycle_bitwise_equal(level, split):
         finally:
             MG.FUSE_CHEB = True
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("level,split", [(7, "miehe"), (6, "none")])
+def test_native_lanczos_matches_python_loop(level, split):
+    """pff_lanczos_ranges (C++ loop, Sturm bisection) gives the ranges of the
+    Python lockstep loop (scipy/numpy tridiagonal eigenvalues)."""
+    from paper_2005_00331_b200 import multigrid as MG
+    h, st, x, _ = state(2, level, split)
+    out = []
+    for native in (False, True):
+        MG.NATIVE_LANCZOS = native
+        try:
+            gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+            gmg.setup(st)
+            out.append(gmg.ranges)
+        finally:
+            MG.NATIVE_LANCZOS = True
+    for l, blocks in out[0].items():
+        for blk, (lo, hi) in blocks.items():
+            lo2, hi2 = out[1][l][blk]
+            assert hi2 == pytest.approx(hi, rel=1e-12) and lo2 == pytest.approx(lo, rel=1e-11), (l, blk)
