@@ -33,6 +33,7 @@ logger = logging.getLogger(__name__)
 
 FUSE_CHEB = True   # Chebyshev steps fused into the block applications (pff_apply_cheb)
 NATIVE_LANCZOS = True   # setup's batched Lanczos driven by pff_lanczos_ranges (C++)
+_EAGER_DONE: set = set()
 
 
 @dataclass
@@ -628,8 +629,19 @@ class GmgPreconditioner:
 
     def _capture(self):
         top = self._work[self.finest]
-        # one eager pass first: validates every launch outside capture
-        self._vcycle(self.finest, top.r, top.z)
+        # one eager pass before the first capture of this hierarchy shape in the
+        # process: validates every launch and does the kernels' one-time setup
+        # (shared-memory attributes, occupancy queries) outside capture
+        key = (self.hierarchy.degree, self.finest, self.coarse_level,
+               self.states[self.finest].split)
+        if key not in _EAGER_DONE:
+            self._vcycle(self.finest, top.r, top.z)
+            _EAGER_DONE.add(key)
+        else:
+            # later captures: only flush pending host->device syncs of the level
+            # states (a host read of a state marks its mirror possibly modified)
+            for s in self.states.values():
+                s.bind()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
