@@ -210,6 +210,12 @@ int pff_lanczos_ranges(int nruns, const pff_level* const* levels, const int* mod
                        int max_iterations, double* lo_hi, double* partials, double* dots,
                        void* stream);
 
+/* Copy `count` entries of each of `ncomp` components spaced `stride` entries
+ * apart (component-major vectors; host<->device or device<->device, UVA) in
+ * one strided copy -- the chunk transfers of the pipelined host path. */
+int pff_copy_components(double* dst, const double* src, int64_t count, int ncomp,
+                        int64_t stride, void* stream);
+
 /* deterministic dot: partials = pff_reduce_scratch_len() doubles, out = 1 double */
 int64_t pff_reduce_scratch_len(void);
 int pff_dot(int64_t n, const double* x, const double* y, double* partials, double* out,

@@ -54,6 +54,7 @@ SIGNATURES = {
     "pff_div": (_i, [_i64, _c_dp, _c_dp, _d, _c_dp, ctypes.c_void_p]),
     "pff_mul": (_i, [_i64, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_reduce_scratch_len": (_i64, []),
+    "pff_copy_components": (_i, [_c_dp, _c_dp, _i64, _i, _i64, ctypes.c_void_p]),
     "pff_lanczos_ranges": (_i, [_i, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_void_p, _i, ctypes.c_void_p, _c_dp, _c_dp,
                                 ctypes.c_void_p]),

@@ -315,6 +315,17 @@ int pff_lanczos_ranges(int nruns, const pff_level* const* levels, const int* mod
                  "pff_lanczos_ranges");
 }
 
+int pff_copy_components(double* dst, const double* src, int64_t count, int ncomp,
+                        int64_t stride, void* stream) {
+    if (!dst || !src || count < 0 || ncomp < 1 || stride < count)
+        return fail(PFF_E_ARG, "%s", "pff_copy_components: bad argument");
+    if (count == 0) return 0;
+    const size_t pitch = (size_t)stride * sizeof(double);
+    return check(cudaMemcpy2DAsync(dst, pitch, src, pitch, (size_t)count * sizeof(double),
+                                   (size_t)ncomp, cudaMemcpyDefault, S(stream)),
+                 "pff_copy_components");
+}
+
 int64_t pff_reduce_scratch_len(void) { return 2 * pff::RED_BLOCKS; }
 
 int pff_dot(int64_t n, const double* x, const double* y, double* partials, double* out,

@@ -352,7 +352,7 @@ class LinearizationState:
         return dst
 
 
-_PIPE_CHUNKS = 4
+_PIPE_CHUNKS = 8
 _NC_IN = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 3}
 _NC_OUT = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 1}
 
@@ -383,14 +383,14 @@ def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor) -> torch.
         c0, c1 = cuts[k], cuts[k + 1]
         hi = min(p * c1 + (1 if c1 < ns else 0), np1 - 1)
         with torch.cuda.stream(s_in):
-            if hi > loaded:
+            if hi > loaded:   # all components of the new node rows: one strided copy
                 a, b = (loaded + 1) * np1, (hi + 1) * np1
-                for c in range(cin):
-                    xd[c * n + a:c * n + b].copy_(xh[c * n + a:c * n + b], non_blocking=True)
+                call("pff_copy_components", xd.data_ptr() + 8 * a, xh.data_ptr() + 8 * a, b - a,
+                     cin, n, s_in.cuda_stream)
                 loaded = hi
             if not dups_in and c1 > ns // 2:
-                for c in range(cin):
-                    xd[c * n + ng:(c + 1) * n].copy_(xh[c * n + ng:(c + 1) * n], non_blocking=True)
+                call("pff_copy_components", xd.data_ptr() + 8 * ng, xh.data_ptr() + 8 * ng, nd,
+                     cin, n, s_in.cuda_stream)
                 dups_in = True
             ev = torch.cuda.Event()
             ev.record(s_in)
@@ -401,11 +401,11 @@ def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor) -> torch.
         with torch.cuda.stream(s_out):
             s_out.wait_event(evc)
             a, b = p * c0 * np1, (p * c1 + (1 if c1 == ns else 0)) * np1
-            for c in range(cout):
-                yh[c * n + a:c * n + b].copy_(yd[c * n + a:c * n + b], non_blocking=True)
+            call("pff_copy_components", yh.data_ptr() + 8 * a, yd.data_ptr() + 8 * a, b - a, cout,
+                 n, s_out.cuda_stream)
             if nd and p * c0 <= im < p * c1 + (1 if c1 == ns else 0):
-                for c in range(cout):
-                    yh[c * n + ng:(c + 1) * n].copy_(yd[c * n + ng:(c + 1) * n], non_blocking=True)
+                call("pff_copy_components", yh.data_ptr() + 8 * ng, yd.data_ptr() + 8 * ng, nd,
+                     cout, n, s_out.cuda_stream)
             e = torch.cuda.Event()
             e.record(s_out)
             ev_out.append(e)
