@@ -65,12 +65,8 @@ int64_t pff_launch_counter(void);
 /* tuning / testing knobs (process-wide):
  *   PFF_OPT_GENERIC_APPLY: 1 = route pff_apply through the generic per-cell
  *     atomic kernel for every degree (the Q2 sweep kernel is the default)
- *   PFF_OPT_SWEEP_ROWS: cell rows per warp chunk of the Q2 sweep (0 = auto)
- *   PFF_OPT_SWEEP_CACHE: q-point cache form of the Q2 sweep for levels
- *     created afterwards (it sizes pff_level_qcache_len): 0 = auto, 1 = full
- *     weighted tangent (10 | 5 doubles per q-point, miehe | none), 2 = lean
- *     state strain / eigen-frame (5 | 4), tangent rebuilt per application */
-enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2, PFF_OPT_SWEEP_CACHE = 3 };
+ *   PFF_OPT_SWEEP_ROWS: cell rows per warp chunk of the Q2 sweep (0 = auto) */
+enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2 };
 int pff_set_option(int key, int value);
 
 /* One mesh level (replaces DofMap + LinearizationState's static data,

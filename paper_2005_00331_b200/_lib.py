@@ -70,7 +70,7 @@ MODE_FULL, MODE_UU, MODE_PHIPHI, MODE_PHIROW = 0, 1, 2, 3
 FLAG_DIRICHLET, FLAG_ACTIVE = 1, 2
 LAYOUT_FULL, LAYOUT_UU, LAYOUT_PHI = 0, 1, 2
 CONS_SELECT, CONS_ZERO, CONS_COPY, CONS_EXCLUDE = 0, 1, 2, 3
-OPT_GENERIC_APPLY, OPT_SWEEP_ROWS, OPT_SWEEP_CACHE = 1, 2, 3
+OPT_GENERIC_APPLY, OPT_SWEEP_ROWS = 1, 2
 
 
 def set_option(key: int, value: int):

@@ -47,10 +47,6 @@ int pff_set_option(int key, int value) {
     switch (key) {
         case PFF_OPT_GENERIC_APPLY: pff::set_generic_apply(value != 0); return 0;
         case PFF_OPT_SWEEP_ROWS: pff::set_sweep_rows_per_chunk(value); return 0;
-        case PFF_OPT_SWEEP_CACHE:
-            if (value < 0 || value > 2) return fail(PFF_E_ARG, "%s", "pff_set_option: sweep cache must be 0, 1 or 2");
-            pff::set_sweep_cache(value);
-            return 0;
     }
     return fail(PFF_E_ARG, "%s", "pff_set_option: unknown key");
 }
@@ -91,7 +87,6 @@ int pff_level_create(pff_level** out, int degree, int level, int split, const pf
         L->q2_struct = ok;
     }
     L->miehe = split;
-    L->lean = pff::sweep_cache_lean(split);
     *out = reinterpret_cast<pff_level*>(L);
     return 0;
 }

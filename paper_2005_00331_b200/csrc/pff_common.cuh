@@ -82,17 +82,6 @@ struct Eig {
 
 __device__ __forceinline__ double posp(double x) { return x > 0.0 ? x : 0.0; }
 
-// 1/x to full double precision: MUFU.RCP64H seed + two Newton steps
-// (no IEEE slow path; x is a positive normal number where the result is used)
-__device__ __forceinline__ double drcp(double x) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
-}
-
 __device__ __forceinline__ Eig eig2(double a11, double a22, double a12) {
     Eig e;
     double m = 0.5 * (a11 + a22);

@@ -91,9 +91,7 @@ struct Level {
         return mesh.p == 2 && mesh.nside >= 64 && q2_struct && mesh.n < (int64_t(1) << 31);
     }
     int n_strips() const { return (mesh.nside + 30) / 31; }
-    // full: weighted tangent (6 | 1) + coupling (3) + pc; lean: pc + (m, +-r, cos 2t, sin 2t) | e
-    bool lean = false;
-    int tile_nq() const { return lean ? (miehe ? 5 : 4) : (miehe ? 10 : 5); }
+    int tile_nq() const { return miehe ? 10 : 5; }   // tangent (6 | 1) + coupling (3) + pc
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
     int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
     // element-vector scratch of the generic application and of the restriction
@@ -155,8 +153,6 @@ struct ChebArgs {
 // options (pff_set_option)
 void set_generic_apply(bool on);
 void set_sweep_rows_per_chunk(int rows);
-void set_sweep_cache(int form);        // 0 auto, 1 full tangent, 2 lean
-bool sweep_cache_lean(int miehe);      // the form a level created now uses
 
 // Q2 sweep kernel (pff_sweep.cu)
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s);

@@ -42,37 +42,25 @@ constexpr int RING = 5;                       // node-row ring (3 in use + 2 in 
 constexpr int QK = 9;                         // q-points per Q2 cell
 constexpr int QARR = QK * SW_LANES;           // doubles per q-point array of a block
 
-// staged node fields: the direction (ux uy phi) and, for the lean cache, the
-// nodal phase fields of the linearisation point (phi0 for g', phi~ for g)
-enum Field { FX = 0, FY, FP, F0, FT, NFIELDS };
+enum Field { FX = 0, FY, FP, NFIELDS };
 
-// Q-point cache block of one (strip, cell row), per form:
-//  full: [T (NT arrays)][cw0 cw1 cw2][pc]   weighted tangent (cache_tensors form)
-//  lean: [pc][m, +-r, cos 2t, sin 2t]       Miehe: eigen-frame of the state strain
-//        [pc][e11 e22 e12]                  none: the state strain
-// (pc = w (2(1-kappa) E+ + Gc/eps) weighted); each mode stages a contiguous
-// sub-range [Q0, Q0 + NQ) of it.
-template <int MODE, bool MIEHE, bool LEAN>
+// tangent-cache block: [T (NT arrays)][cw0 cw1 cw2][pc]; the modes read a
+// contiguous sub-range of it
+template <int MODE, bool MIEHE>
 struct Use {
     static constexpr bool ux = MODE != MODE_PHIPHI;
     static constexpr bool ph = MODE != MODE_UU;
     static constexpr bool DO_UU = MODE == MODE_FULL || MODE == MODE_UU;
     static constexpr bool DO_PP = MODE != MODE_UU;
     static constexpr bool DO_COUP = MODE == MODE_FULL || MODE == MODE_PHIROW;
-    static constexpr bool need_t = LEAN && DO_UU;     // g(phi~) from nodal phi~
-    static constexpr bool need_0 = LEAN && DO_COUP;   // g'(phi0) from nodal phi0
-    static constexpr int NT = MIEHE ? 6 : 1;            // tangent arrays (full form)
-    static constexpr int NQT = LEAN ? (MIEHE ? 5 : 4) : NT + 4;   // arrays of a block
-    static constexpr int Q0 = LEAN ? (MODE == MODE_PHIPHI ? 0 : 1)
-                                   : MODE == MODE_PHIROW ? NT : MODE == MODE_PHIPHI ? NT + 3 : 0;
-    static constexpr int NQ = LEAN ? (MODE == MODE_PHIPHI ? 1 : (!MIEHE && MODE == MODE_UU) ? 0 : NQT - 1)
-                                   : MODE == MODE_FULL ? NQT : MODE == MODE_UU ? NT
-                                   : MODE == MODE_PHIROW ? 4 : 1;
-    static constexpr int QCW = DO_UU ? NT : 0;          // local index of cw0 (full form)
-    static constexpr int QPC = NQ - 1;                  // local index of pc (full form, lean PHIPHI)
-    static constexpr bool used(int f) {
-        return (f == FX || f == FY) ? ux : f == FP ? ph : f == F0 ? need_0 : need_t;
-    }
+    static constexpr int NT = MIEHE ? 6 : 1;            // tangent arrays
+    static constexpr int NQT = NT + 4;                  // arrays of a block
+    static constexpr int Q0 = MODE == MODE_PHIROW ? NT : MODE == MODE_PHIPHI ? NT + 3 : 0;
+    static constexpr int NQ = MODE == MODE_FULL ? NQT : MODE == MODE_UU ? NT
+                              : MODE == MODE_PHIROW ? 4 : 1;
+    static constexpr int QCW = DO_UU ? NT : 0;          // local index of cw0
+    static constexpr int QPC = NQ - 1;                  // local index of pc
+    static constexpr bool used(int f) { return (f == FX || f == FY) ? ux : ph; }
     static constexpr int slot(int f) {
         int s = 0;
         for (int g = 0; g < f; ++g) s += used(g) ? 1 : 0;
@@ -81,11 +69,9 @@ struct Use {
     static constexpr int NF = slot(NFIELDS);
 };
 
-template <int NF, int NQ, int NRHS, int NW = 1>
+template <int NF, int NQ, int NRHS>
 struct __align__(16) WarpSmem {
-    // NW > 1: column contributions of warps 1..NW-1 handed to warp 0
-    double red[NW > 1 ? NW - 1 : 1][NW > 1 ? 27 : 1][SW_LANES];
-    double q[2][NQ > 0 ? NQ * QARR : 2];     // q-point cache blocks, two stages
+    double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
     // fused form: rhs of this lane's output nodes [0, NC); with a fused
     // Chebyshev step also D^-1 [NC, 2 NC) and acc [2 NC, 3 NC)
     double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];
@@ -102,20 +88,13 @@ struct SweepConst {
     double Dh[3][3];   // shape derivatives / h (row 1 is (-1,0,1)/h)
     double ih;         // 1/h
     double cgw[9];     // gc eps w_jq w_iq h^2
-    double lam, mu, mu2;
-    // lean form: per q-point weight W = w_jq w_iq h^2 folded into the constants
-    double wl[9];      // W lambda
-    double wm2[9];     // W 2 mu
-    double wgd[9];     // W 2 (1 - kappa)
-    double wgce[9];    // W gc / eps
-    double wv[9];      // W
-    double k1, kappa;  // 1 - kappa, kappa
+    double lam, mu2;
 };
 
 struct SweepArgs {
     SweepConst K;
     Mesh m;
-    const double* fld[NFIELDS];   // ux uy phi of the direction, phi0 phi~ of the state
+    const double* fld[NFIELDS];   // ux uy phi of the direction
     const uint8_t* flags;
     const double* qtile;          // strip-tiled tangent cache
     int64_t qblock;               // doubles per (strip, row) block
@@ -163,14 +142,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
 }
 
-// named barriers of the NW-warp variant (id 0 is __syncthreads)
-__device__ __forceinline__ void bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
-
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
@@ -180,7 +151,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // ------------------------------------------------------------- tiled refresh
-template <bool MIEHE, bool LEAN>
+template <bool MIEHE>
 __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __restrict__ U,
                                 const double* __restrict__ PT, double* __restrict__ qt,
                                 int n_strips, int64_t qblock, int q_row0, int q_rows,
@@ -193,7 +164,7 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
     const int strip = (int)(blk / q_rows), cy = q_row0 + (int)(blk % q_rows);
     const int cx = strip * SW_OWN - 1 + lane;
     double* out = qt + blk * qblock + lane;
-    constexpr int NT = MIEHE ? 6 : 1, NQT = LEAN ? (MIEHE ? 5 : 4) : NT + 4;
+    constexpr int NT = MIEHE ? 6 : 1, NQT = NT + 4;
     auto put = [&](int arr, int k, double x) { out[(arr * QK + k) * SW_LANES] = x; };
     if (cx < 0 || cx >= m.nside) {
         for (int a = 0; a < NQT; ++a)
@@ -240,30 +211,6 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
             const double tre = e11 + e22;
             const double g = (1.0 - M.kappa) * pt[jq][iq] * pt[jq][iq] + M.kappa;
             const double dg = gdd * p0[jq][iq];
-            if (LEAN) {
-                // [pc][m, +-r, cos 2t, sin 2t] (Miehe) | [pc][e11 e22 e12] (none); the
-                // application rebuilds the tangent, g and g' per q-point
-                double esp;
-                if (MIEHE) {
-                    const double mm = 0.5 * (e11 + e22);
-                    const double dh = 0.5 * (e11 - e22);
-                    const double r = sqrt(dh * dh + e12 * e12);   // = eig2's r
-                    const Eig e = eig2(e11, e22, e12);
-                    const bool gap_ok = (e.ev1 - e.ev2) > 1e-12 * scale2(e11, e22, e12);
-                    put(1, k, mm);
-                    put(2, k, gap_ok ? r : -r);
-                    put(3, k, e.c * e.c - e.s * e.s);
-                    put(4, k, 2.0 * e.c * e.s);
-                    esp = esplus2(lam, mu, tre, e);
-                } else {
-                    put(1, k, e11);
-                    put(2, k, e22);
-                    put(3, k, e12);
-                    esp = 0.5 * lam * tre * tre + mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
-                }
-                put(0, k, wv * (gdd * esp + gce));
-                continue;
-            }
             double esp, q11, q22, q12;
             if (MIEHE) {
                 // the reference's tangent columns for unit directions (src/_kernels.py:519-523)
@@ -302,41 +249,28 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
 }
 
 // ------------------------------------------------------------------ the kernel
-// NW = 1: one warp computes all three Gauss columns of its cells.  NW = 3:
-// three warps share the CTA's staged rows, warp w computing Gauss column
-// (mid, left, right)[w]; warps 1, 2 hand their contributions to warp 0
-// through W.red (named barriers: 1 = red full, 2 = red free), which adds
-// them in the single-warp order (bitwise identical) and stores.  Three
-// times the warps per SM for the same staging buffers.
-template <int MODE, bool MIEHE, bool LEAN, bool FUSED, bool CHEB = false, int NW = 1>
-__global__ void __launch_bounds__(SW_LANES * NW)
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
+__global__ void __launch_bounds__(SW_LANES)
 k_sweep_q2(const SweepArgs A) {
-    using U = Use<MODE, MIEHE, LEAN>;
+    using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
-    constexpr int NTHR = SW_LANES * NW;
-    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0, NW>;
+    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
-    const int lane = threadIdx.x & (SW_LANES - 1);
-    const int warp = NW > 1 ? (int)(threadIdx.x >> 5) : 0;
+    const int lane = threadIdx.x;
 
     const Mesh& m = A.m;
     const int ns = m.nside;
     const int64_t np1 = m.np1;
     const int half = ns >> 1;
 
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         mbar_init(&W.bar[0]);
         mbar_init(&W.bar[1]);
         fence_mbar_init();
     }
-    if (NW > 1) {
-        __syncthreads();
-        if (warp == 0) bar_arrive(2, NTHR);   // W.red starts free
-    } else {
-        __syncwarp();
-    }
+    __syncwarp();
     unsigned phase = 0u;   // bit s: parity of the next completion of mbarrier s
     // staging arithmetic in 32-bit elements (n < 2^31 is checked on the host):
     // 16-byte misalignment of each staged field's base, in elements / bytes
@@ -382,7 +316,6 @@ k_sweep_q2(const SweepArgs A) {
             return bytes + (unsigned)(bb - ab);
         };
         auto issue_qblock = [&](int cy, int stage) -> unsigned {
-            if (NQ == 0) return 0u;
             const double* src =
                 A.qtile + ((int64_t)strip * A.q_rows + (cy - A.q_row0)) * A.qblock + U::Q0 * QARR;
             bulk_g2s(W.q[stage], src, (unsigned)(NQ * QARR * 8), &W.bar[stage]);
@@ -441,7 +374,7 @@ k_sweep_q2(const SweepArgs A) {
             const int64_t jb = 2 * (int64_t)cy;
             const bool more = cy + 1 < c1;
             const int nstage = stage ^ 1;
-            if (more && threadIdx.x == 0) {
+            if (more && lane == 0) {
                 fence_proxy_async();
                 const bool first = cy < cstart;
                 const int j0 = first ? 2 * cy + 2 : 2 * cy + 3;
@@ -458,7 +391,7 @@ k_sweep_q2(const SweepArgs A) {
             const bool own_row = cy >= c0;
             const bool last_cell = cx == ns - 1;
             const int na_out = last_cell ? 3 : 2;
-            if (FUSED && own_row && owner && warp == 0) {   // prefetch rhs of this lane's output nodes
+            if (FUSED && own_row && owner) {   // prefetch rhs of this lane's output nodes
 #pragma unroll
                 for (int b = 0; b < 2; ++b)
                     for (int a = 0; a < na_out; ++a)
@@ -478,13 +411,8 @@ k_sweep_q2(const SweepArgs A) {
             const int s0 = (2 * cy) % RING, s1 = (2 * cy + 1) % RING, s2 = (2 * cy + 2) % RING;
             const bool slit_row = m.level >= 1 && cy == half;
             if (slit_row) {
-                if (NW > 1) {   // warp 0 patches, every warp waits for it
-                    if (warp == 0) patch_slit(s0);
-                    bar_sync(3, NTHR);
-                } else {
-                    __syncwarp();
-                    patch_slit(s0);
-                }
+                __syncwarp();
+                patch_slit(s0);
             }
             __syncwarp();
             const int sl[3] = {s0, s1, s2};
@@ -545,7 +473,7 @@ k_sweep_q2(const SweepArgs A) {
                     return sD * fma(K.Dh[0][2], g(f, b, 2),
                                     fma(K.Dh[0][1], g(f, b, 1), K.Dh[0][0] * g(f, b, 0)));
                 };
-                double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3], X0N[3], XtN[3];
+                double XxN[3], XxD[3], XyN[3], XyD[3], XpN[3], XpD[3];
 #pragma unroll
                 for (int b = 0; b < 3; ++b) {
                     if (U::ux) {
@@ -553,8 +481,6 @@ k_sweep_q2(const SweepArgs A) {
                         XyN[b] = xN(FY, b); XyD[b] = xD(FY, b);
                     }
                     if (U::ph) { XpN[b] = xN(FP, b); XpD[b] = xD(FP, b); }
-                    if (U::need_0) X0N[b] = xN(F0, b);
-                    if (U::need_t) XtN[b] = xN(FT, b);
                 }
                 double Tu1[3] = {}, Tu2[3] = {}, Tv1[3] = {}, Tv2[3] = {}, Tp1[3] = {}, Tp2[3] = {};
 #pragma unroll
@@ -576,72 +502,6 @@ k_sweep_q2(const SweepArgs A) {
                         d22 = yD(XyN);
                         d12 = 0.5 * (yD(XxN) + yN(XyD));
                     }
-                    double fv = 0.0, fgx = 0.0, fgy = 0.0;
-                    if (LEAN && MODE != MODE_PHIPHI) {
-                        // lean form: the tangent of src/_kernels.py:102-123 rebuilt from
-                        // the cached eigen-frame (Miehe) or strain (none), g and g' from
-                        // the nodal phase fields; same algebra in the eigen-basis:
-                        // dl_i = v_i.de.v_i, rot = rho (v1.de.v2) with rho = (l1+ - l2+)/gap
-                        const int wk = jq * 3 + ic;
-                        const double trde = d11 + d22;
-                        double gw = 0.0;   // W g'(phi0)
-                        if (U::need_0) gw = K.wgd[wk] * yN(X0N);
-                        if (MIEHE) {
-                            const double mq = qv(0, k), rs = qv(1, k);
-                            const double c2 = qv(2, k), s2 = qv(3, k);
-                            const double r = fabs(rs);
-                            const double ev1 = mq + r, ev2 = mq - r, tre = 2.0 * mq;
-                            const bool h1 = ev1 >= 0.0, h2 = ev2 >= 0.0;
-                            const double l1p = posp(ev1), l2p = posp(ev2), trp = posp(tre);
-                            const double md = 0.5 * trde, ad = 0.5 * (d11 - d22);
-                            const double P = fma(c2, ad, s2 * d12);
-                            const double dl1 = md + P, dl2 = md - P;
-                            if (U::DO_UU) {
-                                const double rho = h2 ? 1.0 : l1p * drcp(ev1 - ev2);
-                                const double Bp = (rs > 0.0 ? rho : 0.0) * fma(c2, d12, -(s2 * ad));
-                                const double dl1p = h1 ? dl1 : 0.0, dl2p = h2 ? dl2 : 0.0;
-                                const double Mp = 0.5 * (dl1p + dl2p), Ap = 0.5 * (dl1p - dl2p);
-                                const double oa = fma(c2, Ap, -(s2 * Bp));
-                                const double o12 = fma(s2, Ap, c2 * Bp);
-                                const double tt = tre < 0.0 ? 0.0 : trde;
-                                const double pt = yN(XtN);
-                                const double G = K.wv[wk] * fma(K.k1 * pt, pt, K.kappa - 1.0);
-                                const double Gm = G * K.mu2;
-                                const double iso = fma(K.wl[wk], trde, (G * K.lam) * tt);
-                                s11 = fma(K.wm2[wk], d11, fma(Gm, Mp + oa, iso));
-                                s22 = fma(K.wm2[wk], d22, fma(Gm, Mp - oa, iso));
-                                s12 = fma(K.wm2[wk], d12, Gm * o12);
-                            }
-                            if (U::DO_PP) {
-                                const double ep = fma(0.5 * K.lam * trp, trp, K.mu * fma(l1p, l1p, l2p * l2p));
-                                fv = fma(K.wgd[wk], ep, K.wgce[wk]) * yN(XpN);
-                                if (U::DO_COUP)
-                                    fv = fma(gw, fma(K.lam * trp, trde, K.mu2 * fma(l1p, dl1, l2p * dl2)), fv);
-                            }
-                        } else {
-                            if (U::DO_UU) {
-                                const double pt = yN(XtN);
-                                const double gq = K.wv[wk] * fma(K.k1 * pt, pt, K.kappa);
-                                const double lt = K.lam * trde;
-                                s11 = gq * fma(K.mu2, d11, lt);
-                                s22 = gq * fma(K.mu2, d22, lt);
-                                s12 = (gq * K.mu2) * d12;
-                            }
-                            if (U::DO_PP) {
-                                const double e11 = qv(0, k), e22 = qv(1, k), e12 = qv(2, k);
-                                const double tre = e11 + e22;
-                                const double ep = fma(0.5 * K.lam * tre, tre,
-                                                      K.mu * fma(e11, e11, fma(e22, e22, 2.0 * e12 * e12)));
-                                fv = fma(K.wgd[wk], ep, K.wgce[wk]) * yN(XpN);
-                                if (U::DO_COUP) {
-                                    const double lte = K.lam * tre;
-                                    const double sp = fma(fma(K.mu2, e11, lte), d11,
-                                                          fma(fma(K.mu2, e22, lte), d22, (2.0 * K.mu2 * e12) * d12));
-                                    fv = fma(gw, sp, fv);
-                                }
-                            }
-                        }
-                    } else {
                     if (U::DO_UU) {
                         if (MIEHE) {
                             const double t00 = qv(0, k), t01 = qv(1, k), t02 = qv(2, k);
@@ -657,14 +517,12 @@ k_sweep_q2(const SweepArgs A) {
                             s12 = (gw * K.mu2) * d12;
                         }
                     }
+                    double fv = 0.0, fgx = 0.0, fgy = 0.0;
                     if (U::DO_PP) {
                         fv = qv(U::QPC, k) * yN(XpN);
                         if (U::DO_COUP)
                             fv = fma(qv(U::QCW, k), d11,
                                      fma(qv(U::QCW + 1, k), d22, fma(qv(U::QCW + 2, k), d12, fv)));
-                    }
-                    }
-                    if (U::DO_PP) {
                         fgx = K.cgw[jq * 3 + ic] * yN(XpD);
                         fgy = K.cgw[jq * 3 + ic] * yD(XpN);
                     }
@@ -735,40 +593,9 @@ k_sweep_q2(const SweepArgs A) {
             };
             using I0 = std::integral_constant<int, 0>;
             using I1 = std::integral_constant<int, 1>;
-            if (NW == 1) {
-                column(std::true_type{}, I0{});
-                column(std::false_type{}, I0{});
-                column(std::false_type{}, I1{});
-            } else if (warp == 0) {
-                column(std::true_type{}, I0{});
-            } else {
-                column(std::false_type{}, warp - 1);
-            }
-            if (NW > 1) {
-                if (warp > 0) {   // hand the column over to warp 0; nothing else to do this row
-                    bar_sync(2, NTHR);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-#pragma unroll
-                        for (int b = 0; b < 3; ++b)
-#pragma unroll
-                            for (int a = 0; a < 3; ++a) W.red[warp - 1][(c * 3 + b) * 3 + a][lane] = r[c][b][a];
-                    fence_proxy_async();
-                    bar_arrive(1, NTHR);
-                    stage = nstage;
-                    continue;
-                }
-                bar_sync(1, NTHR);
-#pragma unroll
-                for (int w = 0; w < NW - 1; ++w)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-#pragma unroll
-                        for (int b = 0; b < 3; ++b)
-#pragma unroll
-                            for (int a = 0; a < 3; ++a) r[c][b][a] += W.red[w][(c * 3 + b) * 3 + a][lane];
-                bar_arrive(2, NTHR);
-            }
+            column(std::true_type{}, I0{});
+            column(std::false_type{}, I0{});
+            column(std::false_type{}, I1{});
             if (!active) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
@@ -828,7 +655,6 @@ k_sweep_q2(const SweepArgs A) {
         }
         __syncwarp();
     }
-    if (NW > 1 && warp > 0) bar_sync(2, NTHR);   // matches warp 0's last "red free"
 }
 
 struct LaunchCfg {
@@ -836,19 +662,18 @@ struct LaunchCfg {
     int blocks_per_sm = 0;
 };
 
-template <int MODE, bool MIEHE, bool LEAN, bool FUSED, bool CHEB = false>
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
-    using U = Use<MODE, MIEHE, LEAN>;
+    using U = Use<MODE, MIEHE>;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-    constexpr int NW = LEAN ? 3 : 1;
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0, NW>);
-    auto k = k_sweep_q2<MODE, MIEHE, LEAN, FUSED, CHEB, NW>;
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0>);
+    auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB>;
     static LaunchCfg cfg;
     static int n_sm = 0;
     if (!cfg.init) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.blocks_per_sm, k, SW_LANES * NW, shm);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.blocks_per_sm, k, SW_LANES, shm);
         if (e != cudaSuccess) return e;
         int dev = 0;
         cudaGetDevice(&dev);
@@ -871,64 +696,49 @@ cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     a.rows_per_chunk = rows;
     a.n_items = a.n_strips * ((ns + rows - 1) / rows);
     const int grid = a.n_items < slots ? a.n_items : slots;
-    k<<<grid, SW_LANES * NW, shm, s>>>(a);
+    k<<<grid, SW_LANES, shm, s>>>(a);
     count_launches(1);
     return cudaGetLastError();
 }
 
-template <bool MIEHE, bool LEAN, bool FUSED>
+template <bool MIEHE, bool FUSED>
 cudaError_t launch_split(int mode, SweepArgs& a, cudaStream_t s, int rows) {
     switch (mode) {
-        case MODE_FULL: return launch_mode<MODE_FULL, MIEHE, LEAN, FUSED>(a, s, rows);
-        case MODE_UU: return launch_mode<MODE_UU, MIEHE, LEAN, FUSED>(a, s, rows);
-        case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, LEAN, FUSED>(a, s, rows);
-        case MODE_PHIROW: return launch_mode<MODE_PHIROW, MIEHE, LEAN, FUSED>(a, s, rows);
+        case MODE_FULL: return launch_mode<MODE_FULL, MIEHE, FUSED>(a, s, rows);
+        case MODE_UU: return launch_mode<MODE_UU, MIEHE, FUSED>(a, s, rows);
+        case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, FUSED>(a, s, rows);
+        case MODE_PHIROW: return launch_mode<MODE_PHIROW, MIEHE, FUSED>(a, s, rows);
     }
     return cudaErrorInvalidValue;
 }
 
-template <bool MIEHE, bool LEAN>
+template <bool MIEHE>
 cudaError_t launch_cheb(int mode, SweepArgs& a, cudaStream_t s, int rows) {
     switch (mode) {
-        case MODE_UU: return launch_mode<MODE_UU, MIEHE, LEAN, true, true>(a, s, rows);
-        case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, LEAN, true, true>(a, s, rows);
+        case MODE_UU: return launch_mode<MODE_UU, MIEHE, true, true>(a, s, rows);
+        case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, true, true>(a, s, rows);
     }
     return cudaErrorInvalidValue;
-}
-
-template <bool MIEHE, bool LEAN>
-cudaError_t launch_any(int mode, SweepArgs& a, cudaStream_t s, int rows, bool fused, bool cheb) {
-    if (cheb) return launch_cheb<MIEHE, LEAN>(mode, a, s, rows);
-    return fused ? launch_split<MIEHE, LEAN, true>(mode, a, s, rows)
-                 : launch_split<MIEHE, LEAN, false>(mode, a, s, rows);
 }
 
 int g_rows_override = 0;
-int g_cache_form = -1;   // -1: not set (PFF_SWEEP_CACHE env or auto)
 
 }  // namespace
 
 void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
-void set_sweep_cache(int form) { g_cache_form = form; }
-bool sweep_cache_lean(int miehe) {
-    int form = g_cache_form;
-    if (form < 0) {
-        const char* e = getenv("PFF_SWEEP_CACHE");
-        form = e ? (e[0] == 'l' ? 2 : e[0] == 'f' ? 1 : atoi(e)) : 0;
-    }
-    if (form == 1) return false;
-    if (form == 2) return true;
-    return true;   // auto
-}
 
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
     const Mesh& m = L.mesh;
     const int64_t total = (int64_t)L.n_strips() * L.q_rows() * SW_LANES;
     const unsigned grid = (unsigned)((total + 127) / 128);
-    auto k = L.miehe ? (L.lean ? k_refresh_tiled<true, true> : k_refresh_tiled<true, false>)
-                     : (L.lean ? k_refresh_tiled<false, true> : k_refresh_tiled<false, false>);
-    k<<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.phi_tilde, L.qtile(), L.n_strips(), L.tile_block(),
-                           L.q_row0(), L.q_rows(), L.local_n(), L.row_shift(), L.dupoff());
+    if (L.miehe)
+        k_refresh_tiled<true><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.phi_tilde, L.qtile(), L.n_strips(),
+                                                   L.tile_block(), L.q_row0(), L.q_rows(),
+                                                   L.local_n(), L.row_shift(), L.dupoff());
+    else
+        k_refresh_tiled<false><<<grid, 128, 0, s>>>(m, L.shape, L.mat, L.U, L.phi_tilde, L.qtile(), L.n_strips(),
+                                                    L.tile_block(), L.q_row0(), L.q_rows(),
+                                                    L.local_n(), L.row_shift(), L.dupoff());
     count_launches(1);
     return cudaGetLastError();
 }
@@ -975,20 +785,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
                 K.cgw[jq * 3 + iq] = L.mat.gc * L.mat.eps * (wq * h * h);
             }
         K.lam = L.mat.lam;
-        K.mu = L.mat.mu;
         K.mu2 = 2.0 * L.mat.mu;
-        K.k1 = 1.0 - L.mat.kappa;
-        K.kappa = L.mat.kappa;
-        for (int jq = 0; jq < 3; ++jq)
-            for (int iq = 0; iq < 3; ++iq) {
-                const double W = L.shape.w[jq] * L.shape.w[iq] * h * h;
-                const int k = jq * 3 + iq;
-                K.wv[k] = W;
-                K.wl[k] = W * L.mat.lam;
-                K.wm2[k] = W * (2.0 * L.mat.mu);
-                K.wgd[k] = W * (2.0 * (1.0 - L.mat.kappa));
-                K.wgce[k] = W * (L.mat.gc / L.mat.eps);
-            }
     }
     for (int f = 0; f < NFIELDS; ++f) a.fld[f] = nullptr;
     switch (mode) {
@@ -1001,8 +798,6 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
             a.fld[FP] = src - sh; break;
         default: return cudaErrorInvalidValue;
     }
-    a.fld[F0] = L.U + 2 * n - sh;   // nodal phase fields of the state (lean form)
-    a.fld[FT] = L.phi_tilde - sh;
     a.flags = L.flags - sh;
     a.qtile = L.qtile();
     a.qblock = L.tile_block();
@@ -1043,12 +838,12 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         rows = env_rows;
     }
     *handled = true;
-    const bool fused = rhs != nullptr, ch = cheb != nullptr;
+    if (cheb) return L.miehe ? launch_cheb<true>(mode, a, s, rows) : launch_cheb<false>(mode, a, s, rows);
     if (L.miehe)
-        return L.lean ? launch_any<true, true>(mode, a, s, rows, fused, ch)
-                      : launch_any<true, false>(mode, a, s, rows, fused, ch);
-    return L.lean ? launch_any<false, true>(mode, a, s, rows, fused, ch)
-                  : launch_any<false, false>(mode, a, s, rows, fused, ch);
+        return rhs ? launch_split<true, true>(mode, a, s, rows)
+                   : launch_split<true, false>(mode, a, s, rows);
+    return rhs ? launch_split<false, true>(mode, a, s, rows)
+               : launch_split<false, false>(mode, a, s, rows);
 }
 
 }  // namespace pff
