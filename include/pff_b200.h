@@ -238,6 +238,15 @@ int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* p
 int pff_mgs_lowsync(int64_t n, int j, const double* V, int64_t ldv, double* w, double* gram,
                     int64_t ldg, double* partials, double* h, void* stream);
 
+/* Coarse-level solve of the V-cycle (replaces the coarse Chebyshev passes of
+ * src/multigrid.py:311-328 on a coarse level of n <= 256 scalar nodes):
+ * z_u = Cu r_u, t = r_phi - Gpu z_u, z_phi = Cp t, then z = r on the rows
+ * with cmask != 0.  Cu (2n x 2n), Gpu (n x 2n), Cp (n x n): row-major device
+ * matrices formed at setup (Cu, Cp: the fixed Chebyshev polynomials of the
+ * masked diagonal blocks; Gpu: the masked phi-row's u columns); r, z: 3n. */
+int pff_coarse_dense(int64_t n, const double* Cu, const double* Gpu, const double* Cp,
+                     const uint8_t* cmask, const double* r, double* z, void* stream);
+
 /* multi-dot out[i] = V[i] . w for i < k (CGS2 orthogonalisation of the
  * distributed GMRES); partials = k * pff_reduce_scratch_len() / 2 doubles */
 int pff_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* partials,

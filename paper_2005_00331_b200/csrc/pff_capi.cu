@@ -361,4 +361,12 @@ int pff_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y,
     return check(pff::launch_combine(n, k, V, ldv, y, out, accumulate, S(stream)), "pff_combine");
 }
 
+int pff_coarse_dense(int64_t n, const double* Cu, const double* Gpu, const double* Cp,
+                     const uint8_t* cmask, const double* r, double* z, void* stream) {
+    if (n < 1 || n > pff::coarse_dense_nmax() || !Cu || !Gpu || !Cp || !cmask || !r || !z)
+        return fail(PFF_E_ARG, "%s", "pff_coarse_dense: bad argument (n must be in 1..256)");
+    return check(pff::launch_coarse_dense((int)n, Cu, Gpu, Cp, cmask, r, z, S(stream)),
+                 "pff_coarse_dense");
+}
+
 }  // extern "C"

@@ -172,6 +172,12 @@ cudaError_t launch_diagonal(const Level& L, double* dx, double* dy, double* dp, 
 cudaError_t launch_residual(const Level& L, double* out, int mask_dirichlet, int mask_active,
                             cudaStream_t s);
 
+// coarse-level solve as dense linear maps (pff_coarse.cu)
+int coarse_dense_nmax();
+cudaError_t launch_coarse_dense(int n, const double* Cu, const double* Gpu, const double* Cp,
+                                const uint8_t* cmask, const double* r, double* z,
+                                cudaStream_t s);
+
 // dense per-cell matrices (pff_assemble.cu)
 cudaError_t launch_cell_matrices(const Level& L, double* gk, cudaStream_t s);
 

@@ -246,18 +246,55 @@ k_lsmgs_solve(int j, const double* __restrict__ part, double* __restrict__ gram,
     }
 }
 
-// w -= sum_i h[i] V[i]; part = per-block |w|^2
+// w -= sum_i h[i] V[i]; part = per-block |w|^2.  Bandwidth form: h in shared
+// memory, two elements per thread and the basis rows loaded in independent
+// batches of 4 ahead of their FMAs (the per-element sum keeps the order
+// i = 0..j); one pass over the j+1 rows.
+constexpr int LSU_HMAX = 512;
 __global__ void __launch_bounds__(RED_THREADS)
 k_lsmgs_update(int64_t n, int j, const double* __restrict__ V, int64_t ldv,
                const double* __restrict__ h, double* __restrict__ w, double* __restrict__ part) {
+    __shared__ double hs[LSU_HMAX];
+    const bool sm = j < LSU_HMAX;
+    if (sm)
+        for (int i = threadIdx.x; i <= j; i += RED_THREADS) hs[i] = h[i];
+    __syncthreads();
+    const double* hp = sm ? hs : h;
     double v = 0.0;
-    for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < n;
-         e += (int64_t)RED_BLOCKS * RED_THREADS) {
-        double acc = 0.0;
-        for (int i = 0; i <= j; ++i) acc = fma(h[i], V[(int64_t)i * ldv + e], acc);
-        const double we = w[e] - acc;
-        w[e] = we;
-        v = fma(we, we, v);
+    const int64_t stride = (int64_t)RED_BLOCKS * RED_THREADS * 2;
+    for (int64_t e0 = (int64_t)blockIdx.x * RED_THREADS * 2 + threadIdx.x; e0 < n; e0 += stride) {
+        const int64_t e1 = e0 + RED_THREADS;
+        const bool two = e1 < n;
+        const double w0 = w[e0], w1 = two ? w[e1] : 0.0;
+        double a0 = 0.0, a1 = 0.0;
+        int i = 0;
+        for (; i + 4 <= j + 1; i += 4) {
+            double x0[4], x1[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double* vr = V + (int64_t)(i + r) * ldv;
+                x0[r] = vr[e0];
+                x1[r] = two ? vr[e1] : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                a0 = fma(hp[i + r], x0[r], a0);
+                a1 = fma(hp[i + r], x1[r], a1);
+            }
+        }
+        for (; i <= j; ++i) {
+            const double* vr = V + (int64_t)i * ldv;
+            a0 = fma(hp[i], vr[e0], a0);
+            if (two) a1 = fma(hp[i], vr[e1], a1);
+        }
+        const double we0 = w0 - a0;
+        w[e0] = we0;
+        v = fma(we0, we0, v);
+        if (two) {
+            const double we1 = w1 - a1;
+            w[e1] = we1;
+            v = fma(we1, we1, v);
+        }
     }
     const double s = block_sum(v);
     if (threadIdx.x == 0) part[blockIdx.x] = s;

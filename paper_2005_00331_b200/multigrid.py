@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -32,6 +33,10 @@ from .mesh import MeshHierarchy
 logger = logging.getLogger(__name__)
 
 FUSE_CHEB = True   # Chebyshev steps fused into the block applications (pff_apply_cheb)
+# coarse solve as precomputed dense linear maps (pff_coarse_dense) on coarse
+# levels of at most COARSE_DENSE_NMAX scalar nodes (Q2 level 2: 85)
+DENSE_COARSE = os.environ.get("PFF_DENSE_COARSE", "1") != "0"
+COARSE_DENSE_NMAX = 256
 NATIVE_LANCZOS = True   # setup's batched Lanczos driven by pff_lanczos_ranges (C++)
 _EAGER_DONE: set = set()
 
@@ -461,6 +466,7 @@ class GmgPreconditioner:
         self.use_graph = use_graph
         self._inv: dict[int, tuple] = {}
         self._work: dict[int, _LevelWork] = {}
+        self._dense = None
         self._graph = None
         self._scratch = None
 
@@ -499,10 +505,53 @@ class GmgPreconditioner:
                 todo.append(l)
         if todo:
             self.ranges.update(self._estimate_ranges_batched(todo))
+        self._build_dense_coarse()
         self._graph = None
         if logger.isEnabledFor(logging.DEBUG):
             logger.debug("gmg setup: levels %d..%d, ranges %s", self.coarse_level, state.level,
                          {l: (r["uu"][1], r["phiphi"][1]) for l, r in self.ranges.items()})
+
+    def _build_dense_coarse(self):
+        """Coarse solve (src/multigrid.py:311-328) as fixed linear maps: the
+        coarse_sweeps-step Jacobi-Chebyshev pass on a block is the matrix
+        polynomial obtained by running the reference recurrence (cheb_init, then
+        cr -= G d, d = c1 d + c2 D^-1 cr, z += d) on the identity.  The blocks come
+        from the assembled masked Jacobian of the coarse level (identity
+        constrained rows/columns, as pff_apply's modes)."""
+        self._dense = None
+        l = self.coarse_level
+        s = self.states[l]
+        n = s.n_scalar
+        if not DENSE_COARSE or n > COARSE_DENSE_NMAX:
+            return
+        G = op.assemble_oracle(s).device.to_dense()
+        inv_u, inv_p = self._inv[l]
+        cfg = self.cheb
+
+        def poly(A, invd, a, b, sweeps):
+            nb = A.shape[0]
+            theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+            sigma1 = theta / delta
+            eye = torch.eye(nb, dtype=torch.float64, device=A.device)
+            d = invd[:, None] * eye / theta
+            acc = d.clone()
+            cr = eye
+            rho_old = 1.0 / sigma1
+            for _ in range(1, sweeps):
+                rho = 1.0 / (2.0 * sigma1 - rho_old)
+                cr = cr - A @ d
+                d = (rho * rho_old) * d + (2.0 * rho / delta) * (invd[:, None] * cr)
+                acc = acc + d
+                rho_old = rho
+            return acc.contiguous()
+
+        lo, hi = self.ranges[l]["uu"]
+        Cu = poly(G[:2 * n, :2 * n], inv_u, lo, cfg.C * hi, cfg.coarse_sweeps)
+        lo, hi = self.ranges[l]["phiphi"]
+        Cp = poly(G[2 * n:, 2 * n:], inv_p, lo, cfg.C * hi, cfg.coarse_sweeps)
+        Gpu = G[2 * n:, :2 * n].contiguous()
+        cmask = torch.from_numpy(s.constrained_mask().astype(np.uint8)).to(G.device)
+        self._dense = (n, Cu, Gpu, Cp, cmask)
 
     def _estimate_ranges(self, level: int):
         s = self.states[level]
@@ -724,7 +773,12 @@ class GmgPreconditioner:
 
     def _vcycle(self, l, r, z):
         if l == self.coarse_level:
-            self._coarse(l, r, z)
+            if self._dense is not None:
+                n, Cu, Gpu, Cp, cmask = self._dense
+                call("pff_coarse_dense", n, ptr(Cu), ptr(Gpu), ptr(Cp), ptr(cmask), ptr(r), ptr(z),
+                     stream_handle())
+            else:
+                self._coarse(l, r, z)
             return
         s, sc = self.states[l], self.states[l - 1]
         W, Wc = self._work[l], self._work[l - 1]
