@@ -238,6 +238,27 @@ int pff_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* p
 int pff_mgs_lowsync(int64_t n, int j, const double* V, int64_t ldv, double* w, double* gram,
                     int64_t ldg, double* partials, double* h, void* stream);
 
+/* pff_apply_cheb with the accumulator update acc += d + d' instead of
+ * acc += d': the first fused step after a producer emitted d = d0 (the
+ * separate pff_cheb_init pass's `acc += d0`, same rounding). */
+int pff_apply_cheb_first(const pff_level* L, int mode, const double* d, double* d_out,
+                         const double* rhs, double* cr, const double* invd, double* acc,
+                         double c1, double c2, void* stream);
+
+/* Fused residual dst = rhs - G src (mode FULL or PHIROW) that also emits the
+ * next smoothing block's Chebyshev start d0 = invd * dst / theta (FULL: the
+ * two u components, invd/d0 of length 2n; PHIROW: the phi output, length n)
+ * -- pff_cheb_init folded into the residual's store. */
+int pff_apply_emit(const pff_level* L, int mode, const double* src, double* dst,
+                   const double* rhs, const double* invd, double* d0, double theta,
+                   void* stream);
+
+/* First smoothing of a V-cycle level: z = r on constrained rows, 0 elsewhere
+ * (3n); res_u = r[:2n] with constrained rows zeroed; d_u = invd_u res_u / theta
+ * (pff_cons SELECT + EXCLUDE + pff_cheb_init in one pass). */
+int pff_smooth_init(const pff_level* L, const double* r, double* z, double* res_u,
+                    const double* invd_u, double* d_u, double theta, void* stream);
+
 /* Coarse-level solve of the V-cycle (replaces the coarse Chebyshev passes of
  * src/multigrid.py:311-328 on a coarse level of n <= 256 scalar nodes):
  * z_u = Cu r_u, t = r_phi - Gpu z_u, z_phi = Cp t, then z = r on the rows

@@ -175,6 +175,44 @@ int pff_apply_cheb(const pff_level* h, int mode, const double* d, double* d_out,
     return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb");
 }
 
+int pff_apply_cheb_first(const pff_level* h, int mode, const double* d, double* d_out,
+                         const double* rhs, double* cr, const double* invd, double* acc,
+                         double c1, double c2, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
+        return fail(PFF_E_UNBOUND, "%s", "pff_apply_cheb_first: state not bound");
+    if ((mode != 1 && mode != 2) || !d || !d_out || !rhs || !cr || !invd || !acc || d_out == d)
+        return fail(PFF_E_ARG, "%s", "pff_apply_cheb_first: mode must be UU or PHIPHI, d_out != d");
+    pff::ChebArgs cb{invd, d_out, acc, c1, c2};
+    cb.acc_src = 1;
+    return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb_first");
+}
+
+int pff_apply_emit(const pff_level* h, int mode, const double* src, double* dst,
+                   const double* rhs, const double* invd, double* d0, double theta,
+                   void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
+        return fail(PFF_E_UNBOUND, "%s", "pff_apply_emit: state not bound");
+    if ((mode != 0 && mode != 3) || !src || !dst || !rhs || !invd || !d0 || !(theta != 0.0))
+        return fail(PFF_E_ARG, "%s", "pff_apply_emit: mode must be FULL or PHIROW, fused, theta != 0");
+    pff::ChebArgs cb{invd, nullptr, nullptr, 0.0, 0.0};
+    cb.emit = d0;
+    cb.theta = theta;
+    cb.emit_nc = mode == 0 ? 2 : 1;
+    return check(pff::launch_apply(*L, mode, src, dst, rhs, S(stream), &cb), "pff_apply_emit");
+}
+
+int pff_smooth_init(const pff_level* h, const double* r, double* z, double* res_u,
+                    const double* invd_u, double* d_u, double theta, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!L || !L->flags) return fail(PFF_E_UNBOUND, "%s", "pff_smooth_init: flags not bound");
+    if (!r || !z || !res_u || !invd_u || !d_u || !(theta != 0.0))
+        return fail(PFF_E_ARG, "%s", "pff_smooth_init: bad argument");
+    return check(pff::launch_smooth_init(*L, r, z, res_u, invd_u, d_u, theta, S(stream)),
+                 "pff_smooth_init");
+}
+
 int pff_apply_rows(const pff_level* h, int mode, const double* src, double* dst,
                    const double* rhs, int cy_begin, int cy_end, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);

@@ -148,6 +148,14 @@ struct ChebArgs {
     double* dout;
     double* acc;
     double c1, c2;
+    // acc_src: acc += d + d' (the first step after a producer emitted d0 = d;
+    // (acc + d) + d' rounds exactly like the separate pff_cheb_init pass)
+    int acc_src = 0;
+    // residual producers (fused form, no dout): d0 = invd * dst / theta on the
+    // first emit_nc output components (pff_cheb_init's d, same rounding)
+    double* emit = nullptr;
+    double theta = 1.0;
+    int emit_nc = 0;
 };
 
 // options (pff_set_option)
@@ -203,6 +211,8 @@ constexpr int RED_BLOCKS = 592;   // 4 x 148 SMs: fixed, so reductions are deter
 constexpr int RED_THREADS = 256;
 cudaError_t launch_cons(const Level& L, int layout, int op, const double* r, double* z,
                         cudaStream_t s);
+cudaError_t launch_smooth_init(const Level& L, const double* r, double* z, double* res_u,
+                               const double* invd_u, double* d_u, double theta, cudaStream_t s);
 cudaError_t launch_cheb_init(int64_t n, const double* invd, const double* rhs, double theta,
                              double* d, double* acc, int acc_mode, cudaStream_t s);
 cudaError_t launch_cheb_step(int64_t n, const double* invd, const double* r, double c1,

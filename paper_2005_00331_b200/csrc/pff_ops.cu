@@ -209,7 +209,10 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
         if (cheb.dout) {   // fused Chebyshev step on the residual just formed
             const double dn = cheb_update(cheb.c1, sv, cheb.c2, cheb.invd[c * n + i], x);
             cheb.dout[c * n + i] = dn;
-            cheb.acc[c * n + i] += dn;
+            const double av = cheb.acc[c * n + i];
+            cheb.acc[c * n + i] = (cheb.acc_src ? av + sv : av) + dn;
+        } else if (c < cheb.emit_nc) {   // the next block's Chebyshev d0
+            cheb.emit[c * n + i] = cheb.invd[c * n + i] * x / cheb.theta;
         }
     }
 }
@@ -735,7 +738,11 @@ void set_generic_apply(bool on) { g_generic_apply = on; }
 cudaError_t launch_apply(const Level& L, int mode, const double* src, double* dst,
                          const double* rhs, cudaStream_t s, const ChebArgs* cheb) {
     bool handled = false;
-    if (cheb && (!rhs || (mode != MODE_UU && mode != MODE_PHIPHI) || cheb->dout == src))
+    if (cheb && cheb->dout && (!rhs || (mode != MODE_UU && mode != MODE_PHIPHI) || cheb->dout == src))
+        return cudaErrorInvalidValue;
+    if (cheb && !cheb->dout &&
+        (!rhs || !cheb->emit || !cheb->invd || (mode != MODE_FULL && mode != MODE_PHIROW) ||
+         cheb->emit_nc != (mode == MODE_FULL ? 2 : 1)))
         return cudaErrorInvalidValue;
     if (L.windowed()) {   // slabs run the write-once sweep kernel only
         cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled, cheb);

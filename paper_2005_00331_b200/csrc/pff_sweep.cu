@@ -106,6 +106,11 @@ struct SweepArgs {
     double* dout[3];
     double* acc[3];
     double c1, c2;
+    int acc_src;                  // first Chebyshev step: acc += d + d'
+    // EMIT: d0 = invd * dst / theta on the first emit_nc components (reuses invd)
+    double* emit[2];
+    double theta;
+    int emit_nc;
     int n_strips, rows_per_chunk, n_items;
     int cy_begin, cy_end;         // owned cell rows (window)
     int q_row0, q_rows;           // cell rows held by the tiled q-point cache
@@ -249,13 +254,13 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false>
 __global__ void __launch_bounds__(SW_LANES)
 k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
-    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0>;
+    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : NC) : 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -356,12 +361,16 @@ k_sweep_q2(const SweepArgs A) {
                 if (cons) x = sv;
                 if (FUSED) x = (rbi >= 0 ? W.rb[rbi][c][lane] : A.rhs[c][gid]) - x;
                 A.dst[c][gid] = x;
+                if (EMIT && c < A.emit_nc) {   // the next block's Chebyshev d0
+                    const double iv = rbi >= 0 ? W.rb[rbi][NC + c][lane] : A.invd[c][gid];
+                    A.emit[c][gid] = iv * x / A.theta;
+                }
                 if (CHEB) {
                     const double iv = rbi >= 0 ? W.rb[rbi][NC + c][lane] : A.invd[c][gid];
                     const double av = rbi >= 0 ? W.rb[rbi][2 * NC + c][lane] : A.acc[c][gid];
                     const double dn = cheb_update(A.c1, sv, A.c2, iv, x);
                     A.dout[c][gid] = dn;
-                    A.acc[c][gid] = av + dn;
+                    A.acc[c][gid] = (A.acc_src ? av + sv : av) + dn;
                 }
             }
         };
@@ -399,6 +408,7 @@ k_sweep_q2(const SweepArgs A) {
                         for (int c = 0; c < NC; ++c) {
                             const int64_t gi = (jb + b) * np1 + 2 * (int64_t)cx + a;
                             cp_async8(&W.rb[b * 3 + a][c][lane], A.rhs[c] + gi);
+                            if (EMIT && c < A.emit_nc) cp_async8(&W.rb[b * 3 + a][NC + c][lane], A.invd[c] + gi);
                             if (CHEB) {
                                 cp_async8(&W.rb[b * 3 + a][NC + c][lane], A.invd[c] + gi);
                                 cp_async8(&W.rb[b * 3 + a][2 * NC + c][lane], A.acc[c] + gi);
@@ -662,12 +672,12 @@ struct LaunchCfg {
     int blocks_per_sm = 0;
 };
 
-template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false>
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false>
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : NC) : 0>);
-    auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB>;
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : NC) : 0>);
+    auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB, EMIT>;
     static LaunchCfg cfg;
     static int n_sm = 0;
     if (!cfg.init) {
@@ -708,6 +718,15 @@ cudaError_t launch_split(int mode, SweepArgs& a, cudaStream_t s, int rows) {
         case MODE_UU: return launch_mode<MODE_UU, MIEHE, FUSED>(a, s, rows);
         case MODE_PHIPHI: return launch_mode<MODE_PHIPHI, MIEHE, FUSED>(a, s, rows);
         case MODE_PHIROW: return launch_mode<MODE_PHIROW, MIEHE, FUSED>(a, s, rows);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <bool MIEHE>
+cudaError_t launch_emit(int mode, SweepArgs& a, cudaStream_t s, int rows) {
+    switch (mode) {
+        case MODE_FULL: return launch_mode<MODE_FULL, MIEHE, true, false, true>(a, s, rows);
+        case MODE_PHIROW: return launch_mode<MODE_PHIROW, MIEHE, true, false, true>(a, s, rows);
     }
     return cudaErrorInvalidValue;
 }
@@ -816,7 +835,21 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
     }
     for (int c = 0; c < 3; ++c) { a.invd[c] = nullptr; a.dout[c] = nullptr; a.acc[c] = nullptr; }
     a.c1 = a.c2 = 0.0;
-    if (cheb) {
+    a.acc_src = 0;
+    a.emit[0] = a.emit[1] = nullptr;
+    a.theta = 1.0;
+    a.emit_nc = 0;
+    const bool emit = cheb && !cheb->dout;
+    if (emit) {   // residual producer emitting the next block's Chebyshev d0
+        if (!rhs || !cheb->emit || !cheb->invd || (mode != MODE_FULL && mode != MODE_PHIROW))
+            return cudaErrorInvalidValue;
+        a.emit_nc = mode == MODE_FULL ? 2 : 1;
+        for (int c = 0; c < a.emit_nc; ++c) {
+            a.invd[c] = cheb->invd + c * n - sh;
+            a.emit[c] = cheb->emit + c * n - sh;
+        }
+        a.theta = cheb->theta;
+    } else if (cheb) {
         if (!rhs || (mode != MODE_UU && mode != MODE_PHIPHI)) return cudaErrorInvalidValue;
         const int nc = mode == MODE_UU ? 2 : 1;
         for (int c = 0; c < nc; ++c) {
@@ -826,6 +859,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         }
         a.c1 = cheb->c1;
         a.c2 = cheb->c2;
+        a.acc_src = cheb->acc_src;
     }
     a.n_strips = L.n_strips();
     int rows = g_rows_override;
@@ -838,6 +872,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         rows = env_rows;
     }
     *handled = true;
+    if (emit) return L.miehe ? launch_emit<true>(mode, a, s, rows) : launch_emit<false>(mode, a, s, rows);
     if (cheb) return L.miehe ? launch_cheb<true>(mode, a, s, rows) : launch_cheb<false>(mode, a, s, rows);
     if (L.miehe)
         return rhs ? launch_split<true, true>(mode, a, s, rows)

@@ -38,6 +38,32 @@ __global__ void k_cons(int64_t n, const uint8_t* __restrict__ flags, int layout,
     }
 }
 
+// first smoothing of a V-cycle level (z = 0 on entry): z = SELECT(r) (3n),
+// res_u = EXCLUDE(r) on the u rows and the u block's Chebyshev
+// d0 = invd_u res_u / theta -- the cons SELECT, cons EXCLUDE and cheb_init
+// passes in one (same values bit for bit; z += d0 is left to the first
+// fused step, pff_apply_cheb_first)
+__global__ void k_smooth_init(int64_t n, const uint8_t* __restrict__ flags,
+                              const double* __restrict__ r, double* __restrict__ z,
+                              double* __restrict__ res_u, const double* __restrict__ invd_u,
+                              double* __restrict__ d_u, double theta) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t f = flags[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int64_t k = c * n + i;
+        const bool cons = is_cons(f, 0, c);
+        const double rv = r[k];
+        z[k] = cons ? rv : 0.0;
+        if (c < 2) {
+            const double rr = cons ? 0.0 : rv;
+            res_u[k] = rr;
+            d_u[k] = invd_u[k] * rr / theta;
+        }
+    }
+}
+
 __global__ void k_cheb_init(int64_t n, const double* __restrict__ invd,
                             const double* __restrict__ rhs, double theta, double* __restrict__ d,
                             double* __restrict__ acc, int acc_mode) {
@@ -316,6 +342,14 @@ cudaError_t launch_cons(const Level& L, int layout, int op, const double* r, dou
                         cudaStream_t s) {
     const int64_t n = L.local_n();
     k_cons<<<blocks(n), 256, 0, s>>>(n, L.flags, layout, op, r, z);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_smooth_init(const Level& L, const double* r, double* z, double* res_u,
+                               const double* invd_u, double* d_u, double theta, cudaStream_t s) {
+    const int64_t n = L.local_n();
+    k_smooth_init<<<blocks(n), 256, 0, s>>>(n, L.flags, r, z, res_u, invd_u, d_u, theta);
     count_launches(1);
     return cudaGetLastError();
 }

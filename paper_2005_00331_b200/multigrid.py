@@ -35,6 +35,11 @@ logger = logging.getLogger(__name__)
 FUSE_CHEB = True   # Chebyshev steps fused into the block applications (pff_apply_cheb)
 # coarse solve as precomputed dense linear maps (pff_coarse_dense) on coarse
 # levels of at most COARSE_DENSE_NMAX scalar nodes (Q2 level 2: 85)
+# pff_cheb_init folded into the residual producers (pff_apply_emit, pff_smooth_init)
+FUSE_INIT = os.environ.get("PFF_FUSE_INIT", "1") != "0"
+# the FULL residual emitting the u block's d0 measured slower (+4.5 ms per Newton
+# solve at 1024^2) than the separate pff_cheb_init pass it replaces: off
+EMIT_FULL = os.environ.get("PFF_EMIT_FULL", "0") != "0"
 DENSE_COARSE = os.environ.get("PFF_DENSE_COARSE", "1") != "0"
 COARSE_DENSE_NMAX = 256
 NATIVE_LANCZOS = True   # setup's batched Lanczos driven by pff_lanczos_ranges (C++)
@@ -698,7 +703,7 @@ class GmgPreconditioner:
         self._graph = g
 
     # -- device V-cycle (src/multigrid.py:295-344) ---------------------------------
-    def _cheb(self, l, mode, rhs, a, b, sweeps, out, assign):
+    def _cheb(self, l, mode, rhs, a, b, sweeps, out, assign, pre_d=False):
         s = self.states[l]
         W = self._work[l]
         nb = rhs.numel()
@@ -710,6 +715,23 @@ class GmgPreconditioner:
         theta, delta = 0.5 * (b + a), 0.5 * (b - a)
         sigma1 = theta / delta
         st = stream_handle()
+        if pre_d:
+            # the residual's producer already wrote d = D^-1 rhs / theta (pff_apply_emit,
+            # pff_smooth_init); the first fused step adds it to acc ((acc + d) + d')
+            assert sweeps > 1 and FUSE_CHEB and not assign
+            h = s.bind()
+            d_in, d_out = d, W.d2[:nb]
+            src = rhs
+            rho_old = 1.0 / sigma1
+            for k in range(1, sweeps):
+                rho = 1.0 / (2.0 * sigma1 - rho_old)
+                call("pff_apply_cheb_first" if k == 1 else "pff_apply_cheb", h, mode, ptr(d_in),
+                     ptr(d_out), ptr(src), ptr(cr), ptr(inv), ptr(acc), rho * rho_old,
+                     2.0 * rho / delta, st)
+                rho_old = rho
+                src = cr
+                d_in, d_out = d_out, d_in
+            return
         call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0 if assign else 1,
              st)
         if sweeps > 1 and FUSE_CHEB:
@@ -737,10 +759,39 @@ class GmgPreconditioner:
                 if k < sweeps - 1:
                     s.apply_into(mode, d, cr, cr)
 
+    def _fused_init(self):
+        return FUSE_CHEB and FUSE_INIT and self.cheb.sweeps > 1
+
     def _smooth(self, l, z, r, first=False):
         s = self.states[l]
         n = s.n_scalar
         W = self._work[l]
+        if self._fused_init():
+            # pff_cheb_init folded into the residual producers: d0 of the u block by
+            # pff_smooth_init (first smoothing, z = 0 on entry) or the FULL residual,
+            # d0 of the phi block by the phi-row residual (bitwise the same cycle)
+            c, C = self.cheb.c, self.cheb.C
+            hu = self.ranges[l]["uu"][1]
+            hp = self.ranges[l]["phiphi"][1]
+            th_u = 0.5 * (C * hu + c * hu)
+            th_p = 0.5 * (C * hp + c * hp)
+            inv_u, inv_p = self._inv[l]
+            st = stream_handle()
+            h = s.bind()
+            if first:
+                call("pff_smooth_init", h, ptr(r), ptr(z), ptr(W.res), ptr(inv_u), ptr(W.d), th_u, st)
+            elif EMIT_FULL:
+                call("pff_apply_emit", h, _lib.MODE_FULL, ptr(z), ptr(W.res), ptr(r), ptr(inv_u),
+                     ptr(W.d), th_u, st)
+            else:
+                s.apply_into(_lib.MODE_FULL, z, W.res, r)
+            self._cheb(l, _lib.MODE_UU, W.res[:2 * n], c * hu, C * hu, self.cheb.sweeps, z[:2 * n],
+                       False, pre_d=first or EMIT_FULL)
+            call("pff_apply_emit", h, _lib.MODE_PHIROW, ptr(z), ptr(W.resphi), ptr(r[2 * n:]),
+                 ptr(inv_p), ptr(W.d), th_p, st)
+            self._cheb(l, _lib.MODE_PHIPHI, W.resphi, c * hp, C * hp, self.cheb.sweeps, z[2 * n:],
+                       False, pre_d=True)
+            return
         if first:
             # z = SELECT(r): r - G z is r with the constrained rows zeroed, exactly
             # (identity rows/columns), so no operator application is needed
@@ -783,7 +834,8 @@ class GmgPreconditioner:
         s, sc = self.states[l], self.states[l - 1]
         W, Wc = self._work[l], self._work[l - 1]
         st = stream_handle()
-        call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
+        if not self._fused_init():   # pff_smooth_init writes z = SELECT(r) itself
+            call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
         self._smooth(l, z, r, first=True)
         s.apply_into(_lib.MODE_FULL, z, W.res, r)
         call("pff_restrict", s.bind(), sc.bind(), ptr(W.res), ptr(Wc.r), 1, st)

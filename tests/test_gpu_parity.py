@@ -165,6 +165,21 @@ def test_solver_stack_vs_golden(name):
     gmg.use_graph = False
     assert max(block_rel(gmg.apply(d["x"]), z, n)) <= 1e-14
     gmg.use_graph = True
+    # the matrix-free coarse solve (the reference's Chebyshev passes) agrees
+    # with the dense-map coarse solve (pff_coarse_dense) and with the golden
+    from paper_2005_00331_b200 import multigrid as MG
+    assert gmg._dense is not None
+    MG.DENSE_COARSE = False
+    try:
+        gmg2 = P.GmgPreconditioner(st.hierarchy, coarse_level=2,
+                                   cheb=P.ChebyshevConfig(sweeps=sweeps))
+        gmg2.setup(st)
+        assert gmg2._dense is None
+        z2 = gmg2.apply(d["x"])
+    finally:
+        MG.DENSE_COARSE = True
+    assert max(block_rel(z2, d["vcycle"], n)) <= TOL
+    assert max(block_rel(z2, z, n)) <= 1e-13
     hi = gmg.ranges[level]["uu"][1]
     cheb = P.chebyshev_apply(lambda v: P.apply_block_uu(st, v), gmg.diags[level]["uu"].cpu().numpy(),
                              d["x"][:2 * n], 0.24 * hi, 1.2 * hi, 5)
@@ -316,3 +331,32 @@ def test_pipelined_host_path_matches_device_path(split, level):
         assert not got.is_cuda
         want = fn(st, xd[sl].contiguous())
         assert torch.equal(got, want.cpu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_vcycle_fused_chebyshev_start_bitwise(split):
+    """pff_smooth_init / pff_apply_emit / pff_apply_cheb_first (the Chebyshev
+    start folded into the residual producers) give the V-cycle of the separate
+    pff_cons + pff_cheb_init passes bit for bit, on sweep (>= 64^2) and generic
+    levels."""
+    import bench
+    from paper_2005_00331_b200 import multigrid as MG
+    level = 7
+    h, params, U, pt, act, dirn, x = bench.baseline_inputs(2, level, split, seed=1, notch=True)
+    st = P.LinearizationState(h, level, params, split=split)
+    st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    st.refresh_cache()
+    out = []
+    saved = (MG.FUSE_INIT, MG.EMIT_FULL)
+    try:
+        for fuse, emit in ((False, False), (True, False), (True, True)):
+            MG.FUSE_INIT, MG.EMIT_FULL = fuse, emit
+            g = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+            g.setup(st)
+            out.append(g.apply(x))
+    finally:
+        MG.FUSE_INIT, MG.EMIT_FULL = saved
+    assert np.array_equal(out[0], out[1])
+    assert np.array_equal(out[0], out[2])
