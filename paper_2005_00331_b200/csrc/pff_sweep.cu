@@ -74,9 +74,9 @@ struct __align__(16) WarpSmem {
     double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
     // fused form: rhs of this lane's output nodes [0, NC); with a fused
     // Chebyshev step also D^-1 [NC, 2 NC) and acc [2 NC, 3 NC)
-    double rb[6][NRHS > 0 ? NRHS : 1][SW_LANES];
-    double v[RING][NF][RW];                  // node-row ring
-    uint8_t f[RING][FW];                     // flag rows
+    double rb[NRHS > 0 ? 6 : 1][NRHS > 0 ? NRHS : 1][NRHS > 0 ? SW_LANES : 1];
+    alignas(16) double v[RING][NF][RW];      // node-row ring (TMA destinations: 16-B aligned)
+    alignas(16) uint8_t f[RING][FW];         // flag rows
     int voff[RING][NF];                      // element offset of staged column 0
     int foff[RING];
     unsigned long long bar[2];
@@ -260,7 +260,11 @@ k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
-    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : NC) : 0>;
+    // the fused Chebyshev / emit forms stage rhs, D^-1 (and acc) in shared memory
+    // by cp.async; the plain fused residual prefetches its rhs into registers
+    // (keeps the FULL residual at the plain kernel's 4 CTAs per SM)
+    constexpr bool RB_SMEM = FUSED && (CHEB || EMIT);
+    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : 0) : 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -348,7 +352,9 @@ k_sweep_q2(const SweepArgs A) {
         // stores: identity rows take the raw staged src value (slot/column) or,
         // on the rare paths (slot < 0), a global load; the fused rhs comes from
         // the per-lane cp.async buffer (rbi >= 0) or a global load
-        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int slot, int k, int rbi) {
+        // rh: this row's fused rhs value per component (unused unless FUSED)
+        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int slot, int k, int rbi,
+                         const double (&rh)[3]) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const int pc = U::DO_UU ? c : 2;
@@ -359,7 +365,7 @@ k_sweep_q2(const SweepArgs A) {
                 if (cons || CHEB)
                     sv = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k) : A.src_out[c][gid];
                 if (cons) x = sv;
-                if (FUSED) x = (rbi >= 0 ? W.rb[rbi][c][lane] : A.rhs[c][gid]) - x;
+                if (FUSED) x = rh[c] - x;
                 A.dst[c][gid] = x;
                 if (EMIT && c < A.emit_nc) {   // the next block's Chebyshev d0
                     const double iv = rbi >= 0 ? W.rb[rbi][NC + c][lane] : A.invd[c][gid];
@@ -400,13 +406,20 @@ k_sweep_q2(const SweepArgs A) {
             const bool own_row = cy >= c0;
             const bool last_cell = cx == ns - 1;
             const int na_out = last_cell ? 3 : 2;
+            double rr[2][3][3];   // register-prefetched rhs (plain fused form)
             if (FUSED && own_row && owner) {   // prefetch rhs of this lane's output nodes
 #pragma unroll
                 for (int b = 0; b < 2; ++b)
-                    for (int a = 0; a < na_out; ++a)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        if (a >= na_out) break;
 #pragma unroll
                         for (int c = 0; c < NC; ++c) {
                             const int64_t gi = (jb + b) * np1 + 2 * (int64_t)cx + a;
+                            if (!RB_SMEM) {
+                                rr[b][a][c] = A.rhs[c][gi];
+                                continue;
+                            }
                             cp_async8(&W.rb[b * 3 + a][c][lane], A.rhs[c] + gi);
                             if (EMIT && c < A.emit_nc) cp_async8(&W.rb[b * 3 + a][NC + c][lane], A.invd[c] + gi);
                             if (CHEB) {
@@ -414,6 +427,7 @@ k_sweep_q2(const SweepArgs A) {
                                 cp_async8(&W.rb[b * 3 + a][2 * NC + c][lane], A.acc[c] + gi);
                             }
                         }
+                    }
             }
             cp_async_commit();
             mbar_wait(&W.bar[stage], (phase >> stage) & 1u);
@@ -621,29 +635,44 @@ k_sweep_q2(const SweepArgs A) {
             for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int b = 0; b < 3; ++b) left[c][b] = __shfl_up_sync(0xffffffffu, r[c][b][2], 1);
-            if (FUSED) cp_async_wait_all();
+            if (RB_SMEM) cp_async_wait_all();
+            // rhs of a store: prefetched (rbi >= 0) or a global load (rare paths)
+            auto rhs_of = [&](int64_t gid, int rbi, double (&rh)[3]) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    if (!FUSED) { rh[c] = 0.0; continue; }
+                    if (rbi < 0) rh[c] = A.rhs[c][gid];
+                    else if (RB_SMEM) rh[c] = W.rb[rbi][c][lane];
+                    else rh[c] = rr[rbi / 3][rbi % 3][c];
+                }
+            };
             if (own_row && owner) {
                 const int na = na_out;
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                     const int64_t j = jb + b;
-                    for (int a = 0; a < na; ++a) {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        if (a >= na) break;
                         const int64_t gc = 2 * (int64_t)cx + a;
-                        double v[3];
+                        double v[3], rh[3];
                         if (b == 0 && slit_row && gc < m.i_mid) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = carry[c][a];
-                            store(j * np1 + gc, v, A.flags[j * np1 + gc], -1, 0, -1);
+                            rhs_of(j * np1 + gc, -1, rh);
+                            store(j * np1 + gc, v, A.flags[j * np1 + gc], -1, 0, -1, rh);
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = r[c][0][a] + (a == 0 ? left[c][0] : 0.0);
-                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], s0, 2 * lane + a, -1);
+                            rhs_of(A.dupoff + gc, -1, rh);
+                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], s0, 2 * lane + a, -1, rh);
                             continue;
                         }
 #pragma unroll
                         for (int c = 0; c < 3; ++c)
                             v[c] = r[c][b][a] + (a == 0 ? left[c][b] : 0.0) +
                                    (b == 0 ? carry[c][a] : 0.0);
-                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a), sl[b], 2 * lane + a, b * 3 + a);
+                        rhs_of(j * np1 + gc, b * 3 + a, rh);
+                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a), sl[b], 2 * lane + a, b * 3 + a, rh);
                     }
                 }
             }
@@ -653,10 +682,13 @@ k_sweep_q2(const SweepArgs A) {
                 for (int a = 0; a < 3; ++a) carry[c][a] = r[c][2][a] + (a == 0 ? left[c][2] : 0.0);
             if (cy == ns - 1 && own_row && owner) {   // top boundary row 2*ns
                 const int64_t j = jb + 2;
-                for (int a = 0; a < na_out; ++a) {
-                    double v[3] = {carry[0][a], carry[1][a], carry[2][a]};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    if (a >= na_out) break;
+                    double v[3] = {carry[0][a], carry[1][a], carry[2][a]}, rh[3];
+                    rhs_of(j * np1 + 2 * (int64_t)cx + a, -1, rh);
                     store(j * np1 + 2 * (int64_t)cx + a, v, flag(s2, 2 * lane + a), s2,
-                          2 * lane + a, -1);
+                          2 * lane + a, -1, rh);
                 }
             }
             fence_proxy_async();   // our generic smem accesses before the next TMA writes
@@ -676,7 +708,8 @@ template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : NC) : 0>);
+    // must match k_sweep_q2's Smem (the plain fused form keeps its rhs in registers)
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : 0) : 0>);
     auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB, EMIT>;
     static LaunchCfg cfg;
     static int n_sm = 0;
@@ -742,6 +775,17 @@ cudaError_t launch_cheb(int mode, SweepArgs& a, cudaStream_t s, int rows) {
 
 int g_rows_override = 0;
 
+// smallest mesh (cells per side) routed to the sweep kernel; below it the
+// generic cooperative kernel is faster (latency-bound levels)
+int sweep_min_nside() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PFF_SWEEP_MIN_NSIDE");
+        v = e ? atoi(e) : 64;
+    }
+    return v;
+}
+
 }  // namespace
 
 void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
@@ -773,6 +817,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
                                     bool* handled, const ChebArgs* cheb) {
     *handled = false;
     if (!L.sweep_ok()) return cudaSuccess;
+    if (!L.windowed() && cy_begin < 0 && L.mesh.nside < sweep_min_nside()) return cudaSuccess;
     const Mesh& m = L.mesh;
     const int64_t n = L.local_n();
     const int64_t sh = L.row_shift();   // global node j*np1+i lives at local index - sh

@@ -20,6 +20,7 @@ ap.add_argument("--level", type=int, default=10)
 ap.add_argument("--generic", type=int, default=0)
 ap.add_argument("--rows", type=int, default=0)
 ap.add_argument("--degree", type=int, default=2)
+ap.add_argument("--fused", type=int, default=0, help="fused residual form dst = rhs - G src")
 a = ap.parse_args()
 _lib.set_option(_lib.OPT_GENERIC_APPLY, a.generic)
 _lib.set_option(_lib.OPT_SWEEP_ROWS, a.rows)
@@ -36,13 +37,14 @@ nin = {0: 3 * n, 1: 2 * n, 2: n, 3: 3 * n}[a.mode]
 nout = {0: 3 * n, 1: 2 * n, 2: n, 3: n}[a.mode]
 xd = torch.from_numpy(x[:nin]).cuda()
 y = torch.empty(nout, dtype=torch.float64, device="cuda")
+rhs = torch.rand(nout, dtype=torch.float64, device="cuda") if a.fused else None
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(a.reps):
-    st.apply_into(a.mode, xd, y)
+    st.apply_into(a.mode, xd, y, rhs)
 torch.cuda.synchronize()
 ev[0].record()
 for i in range(a.reps):
-    st.apply_into(a.mode, xd, y)
+    st.apply_into(a.mode, xd, y, rhs)
 ev[1].record()
 torch.cuda.synchronize()
 print(f"mode {a.mode} split {a.split}: {ev[0].elapsed_time(ev[1]) / a.reps:.4f} ms/apply")
