@@ -21,7 +21,10 @@
 //  * a cell's right node column goes to lane+1 by shuffle, its top node row
 //    is carried in registers; every dst entry is written exactly once
 //    (deterministic) with the identity rows and the optional fused
-//    rhs - G src applied at the store;
+//    rhs - G src applied at the store (rhs, and the fused Chebyshev step's
+//    D^-1 / accumulator, prefetched into registers at the top of the row step:
+//    no shared-memory staging, so the fused forms keep the plain form's CTAs
+//    per SM);
 //  * the slit (src/mesh_hierarchy.py:156-189): the upper cell row reads the
 //    upper copies (n_grid + i) and lower/upper copies are stored apart.
 #include <cstdlib>
@@ -147,13 +150,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
 
 // ------------------------------------------------------------- tiled refresh
 template <bool MIEHE>
@@ -260,11 +256,10 @@ k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
     constexpr int NF = U::NF, NQ = U::NQ;
     constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;   // output components
-    // the fused Chebyshev / emit forms stage rhs, D^-1 (and acc) in shared memory
-    // by cp.async; the plain fused residual prefetches its rhs into registers
-    // (keeps the FULL residual at the plain kernel's 4 CTAs per SM)
-    constexpr bool RB_SMEM = FUSED && (CHEB || EMIT);
-    using Smem = WarpSmem<NF, NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : 0) : 0>;
+    // the fused forms prefetch rhs (and D^-1, acc) of the lane's output nodes
+    // into registers at the top of the row step: no staging buffer in shared
+    // memory, so they run at the plain kernel's CTAs per SM
+    using Smem = WarpSmem<NF, NQ, 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -350,11 +345,10 @@ k_sweep_q2(const SweepArgs A) {
             }
         };
         // stores: identity rows take the raw staged src value (slot/column) or,
-        // on the rare paths (slot < 0), a global load; the fused rhs comes from
-        // the per-lane cp.async buffer (rbi >= 0) or a global load
-        // rh: this row's fused rhs value per component (unused unless FUSED)
-        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int slot, int k, int rbi,
-                         const double (&rh)[3]) {
+        // on the rare paths (slot < 0), a global load; rh[0|1|2][c] = this row's
+        // fused rhs, D^-1, acc per component (register prefetch, FUSED only)
+        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int slot, int k,
+                         const double (&rh)[3][3]) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const int pc = U::DO_UU ? c : 2;
@@ -365,15 +359,12 @@ k_sweep_q2(const SweepArgs A) {
                 if (cons || CHEB)
                     sv = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k) : A.src_out[c][gid];
                 if (cons) x = sv;
-                if (FUSED) x = rh[c] - x;
+                if (FUSED) x = rh[0][c] - x;
                 A.dst[c][gid] = x;
-                if (EMIT && c < A.emit_nc) {   // the next block's Chebyshev d0
-                    const double iv = rbi >= 0 ? W.rb[rbi][NC + c][lane] : A.invd[c][gid];
-                    A.emit[c][gid] = iv * x / A.theta;
-                }
+                if (EMIT && c < A.emit_nc) A.emit[c][gid] = rh[1][c] * x / A.theta;   // next block's d0
                 if (CHEB) {
-                    const double iv = rbi >= 0 ? W.rb[rbi][NC + c][lane] : A.invd[c][gid];
-                    const double av = rbi >= 0 ? W.rb[rbi][2 * NC + c][lane] : A.acc[c][gid];
+                    const double iv = rh[1][c];
+                    const double av = rh[2][c];
                     const double dn = cheb_update(A.c1, sv, A.c2, iv, x);
                     A.dout[c][gid] = dn;
                     A.acc[c][gid] = (A.acc_src ? av + sv : av) + dn;
@@ -406,8 +397,9 @@ k_sweep_q2(const SweepArgs A) {
             const bool own_row = cy >= c0;
             const bool last_cell = cx == ns - 1;
             const int na_out = last_cell ? 3 : 2;
-            double rr[2][3][3];   // register-prefetched rhs (plain fused form)
-            if (FUSED && own_row && owner) {   // prefetch rhs of this lane's output nodes
+            // register-prefetched rhs, D^-1 and acc of the lane's output nodes
+            double rr[2][3][3], ri[2][3][3], ra[2][3][3];
+            if (FUSED && own_row && owner) {
 #pragma unroll
                 for (int b = 0; b < 2; ++b)
 #pragma unroll
@@ -416,20 +408,12 @@ k_sweep_q2(const SweepArgs A) {
 #pragma unroll
                         for (int c = 0; c < NC; ++c) {
                             const int64_t gi = (jb + b) * np1 + 2 * (int64_t)cx + a;
-                            if (!RB_SMEM) {
-                                rr[b][a][c] = A.rhs[c][gi];
-                                continue;
-                            }
-                            cp_async8(&W.rb[b * 3 + a][c][lane], A.rhs[c] + gi);
-                            if (EMIT && c < A.emit_nc) cp_async8(&W.rb[b * 3 + a][NC + c][lane], A.invd[c] + gi);
-                            if (CHEB) {
-                                cp_async8(&W.rb[b * 3 + a][NC + c][lane], A.invd[c] + gi);
-                                cp_async8(&W.rb[b * 3 + a][2 * NC + c][lane], A.acc[c] + gi);
-                            }
+                            rr[b][a][c] = A.rhs[c][gi];
+                            if (CHEB || (EMIT && c < A.emit_nc)) ri[b][a][c] = A.invd[c][gi];
+                            if (CHEB) ra[b][a][c] = A.acc[c][gi];
                         }
                     }
             }
-            cp_async_commit();
             mbar_wait(&W.bar[stage], (phase >> stage) & 1u);
             phase ^= 1u << stage;
             const int s0 = (2 * cy) % RING, s1 = (2 * cy + 1) % RING, s2 = (2 * cy + 2) % RING;
@@ -635,15 +619,23 @@ k_sweep_q2(const SweepArgs A) {
             for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int b = 0; b < 3; ++b) left[c][b] = __shfl_up_sync(0xffffffffu, r[c][b][2], 1);
-            if (RB_SMEM) cp_async_wait_all();
-            // rhs of a store: prefetched (rbi >= 0) or a global load (rare paths)
-            auto rhs_of = [&](int64_t gid, int rbi, double (&rh)[3]) {
+            // rhs (and D^-1, acc) of a store: prefetched (rbi >= 0) or global
+            // loads (rare paths: slit copies, top boundary row)
+            auto rhs_of = [&](int64_t gid, int rbi, double (&rh)[3][3]) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    if (!FUSED) { rh[c] = 0.0; continue; }
-                    if (rbi < 0) rh[c] = A.rhs[c][gid];
-                    else if (RB_SMEM) rh[c] = W.rb[rbi][c][lane];
-                    else rh[c] = rr[rbi / 3][rbi % 3][c];
+                    rh[0][c] = rh[1][c] = rh[2][c] = 0.0;
+                    if (!FUSED) continue;
+                    const bool wi = CHEB || (EMIT && c < A.emit_nc);
+                    if (rbi < 0) {
+                        rh[0][c] = A.rhs[c][gid];
+                        if (wi) rh[1][c] = A.invd[c][gid];
+                        if (CHEB) rh[2][c] = A.acc[c][gid];
+                    } else {
+                        rh[0][c] = rr[rbi / 3][rbi % 3][c];
+                        if (wi) rh[1][c] = ri[rbi / 3][rbi % 3][c];
+                        if (CHEB) rh[2][c] = ra[rbi / 3][rbi % 3][c];
+                    }
                 }
             };
             if (own_row && owner) {
@@ -655,16 +647,16 @@ k_sweep_q2(const SweepArgs A) {
                     for (int a = 0; a < 3; ++a) {
                         if (a >= na) break;
                         const int64_t gc = 2 * (int64_t)cx + a;
-                        double v[3], rh[3];
+                        double v[3], rh[3][3];
                         if (b == 0 && slit_row && gc < m.i_mid) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = carry[c][a];
                             rhs_of(j * np1 + gc, -1, rh);
-                            store(j * np1 + gc, v, A.flags[j * np1 + gc], -1, 0, -1, rh);
+                            store(j * np1 + gc, v, A.flags[j * np1 + gc], -1, 0, rh);
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = r[c][0][a] + (a == 0 ? left[c][0] : 0.0);
                             rhs_of(A.dupoff + gc, -1, rh);
-                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], s0, 2 * lane + a, -1, rh);
+                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], s0, 2 * lane + a, rh);
                             continue;
                         }
 #pragma unroll
@@ -672,7 +664,7 @@ k_sweep_q2(const SweepArgs A) {
                             v[c] = r[c][b][a] + (a == 0 ? left[c][b] : 0.0) +
                                    (b == 0 ? carry[c][a] : 0.0);
                         rhs_of(j * np1 + gc, b * 3 + a, rh);
-                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a), sl[b], 2 * lane + a, b * 3 + a, rh);
+                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a), sl[b], 2 * lane + a, rh);
                     }
                 }
             }
@@ -685,10 +677,10 @@ k_sweep_q2(const SweepArgs A) {
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     if (a >= na_out) break;
-                    double v[3] = {carry[0][a], carry[1][a], carry[2][a]}, rh[3];
+                    double v[3] = {carry[0][a], carry[1][a], carry[2][a]}, rh[3][3];
                     rhs_of(j * np1 + 2 * (int64_t)cx + a, -1, rh);
                     store(j * np1 + 2 * (int64_t)cx + a, v, flag(s2, 2 * lane + a), s2,
-                          2 * lane + a, -1, rh);
+                          2 * lane + a, rh);
                 }
             }
             fence_proxy_async();   // our generic smem accesses before the next TMA writes
@@ -707,9 +699,8 @@ struct LaunchCfg {
 template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false>
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
-    constexpr int NC = U::DO_UU ? (U::DO_PP ? 3 : 2) : 1;
-    // must match k_sweep_q2's Smem (the plain fused form keeps its rhs in registers)
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, FUSED ? (CHEB ? 3 * NC : EMIT ? 2 * NC : 0) : 0>);
+    // must match k_sweep_q2's Smem (the fused forms keep rhs / D^-1 / acc in registers)
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, 0>);
     auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB, EMIT>;
     static LaunchCfg cfg;
     static int n_sm = 0;
