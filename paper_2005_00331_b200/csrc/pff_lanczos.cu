@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "pff_internal.cuh"
@@ -51,6 +53,97 @@ double tridiag_eig(const std::vector<double>& a, const std::vector<double>& b, i
         else lo = mid;
     }
     return 0.5 * (lo + hi);
+}
+
+// ---- batched vector kernels: one launch per phase for all active runs ----------
+// Each run keeps the exact per-run arithmetic and reduction structure of the
+// single-run kernels (k_mul, k_div, k_axpby, k_dot_partials / k_reduce_final:
+// RED_BLOCKS x RED_THREADS grid-stride partials, fixed-order final sum), so a
+// run's alphas and betas do not depend on how many runs share a launch.
+constexpr int LZ_MAX = 32;
+struct LzBatch {
+    int nr;
+    int slot[LZ_MAX];            // run index: partials / dots slot
+    int64_t n[LZ_MAX];
+    const double* dhalf[LZ_MAX];
+    double* v[LZ_MAX];
+    double* vp[LZ_MAX];
+    double* w[LZ_MAX];
+    double* tmp[LZ_MAX];
+    double s[LZ_MAX];            // beta (post, pre: divisor) or alpha
+    int div[LZ_MAX];             // pre: v = v / s first
+};
+
+__device__ __forceinline__ double lz_block_sum(double v) {
+    __shared__ double sh[RED_THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (wid == 0) {
+        t = lane < RED_THREADS / 32 ? sh[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    }
+    return t;
+}
+
+// (v = v / s;) tmp = dhalf v
+__global__ void __launch_bounds__(RED_THREADS) k_lz_pre(const LzBatch B) {
+    const int r = blockIdx.y;
+    const int64_t n = B.n[r];
+    const double* dh = B.dhalf[r];
+    double* v = B.v[r];
+    double* t = B.tmp[r];
+    const bool dv = B.div[r] != 0;
+    const double sv = B.s[r];
+    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        double x = v[i];
+        if (dv) {
+            x = x / sv;
+            v[i] = x;
+        }
+        t[i] = dh[i] * x;
+    }
+}
+
+// post-apply: w = dhalf w; w = (-beta) vp + w; partials of v.w
+// alpha step: w = (-alpha) v + w; partials of w.w
+template <bool POST>
+__global__ void __launch_bounds__(RED_THREADS) k_lz_update(const LzBatch B, double* part) {
+    const int r = blockIdx.y;
+    const int64_t n = B.n[r];
+    const double a = -B.s[r];
+    const double* dh = B.dhalf[r];
+    const double* v = B.v[r];
+    const double* x = POST ? B.vp[r] : B.v[r];
+    double* w = B.w[r];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+         i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        double wi = w[i];
+        if (POST) wi = dh[i] * wi;
+        wi = fma(a, x[i], wi);
+        w[i] = wi;
+        acc = POST ? fma(v[i], wi, acc) : fma(wi, wi, acc);
+    }
+    const double t = lz_block_sum(acc);
+    if (threadIdx.x == 0) part[(int64_t)B.slot[r] * 2 * RED_BLOCKS + blockIdx.x] = t;
+}
+
+// dots[slot] = fixed-order sum of the run's RED_BLOCKS partials
+__global__ void __launch_bounds__(RED_THREADS) k_lz_final(const LzBatch B, const double* part,
+                                                          double* dots) {
+    const int slot = B.slot[blockIdx.x];
+    const double* p = part + (int64_t)slot * 2 * RED_BLOCKS;
+    double v = 0.0;
+    for (int k = threadIdx.x; k < RED_BLOCKS; k += RED_THREADS) v += p[k];
+    const double t = lz_block_sum(v);
+    if (threadIdx.x == 0) dots[slot] = t;
 }
 
 struct Run {
@@ -95,38 +188,98 @@ cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* mod
         return e;
     };
     cudaError_t e = cudaSuccess;
+    // the active runs in batches of LZ_MAX; per phase one launch per batch
+    auto batches = [&](auto&& fill, auto&& launch) -> cudaError_t {
+        LzBatch B;
+        B.nr = 0;
+        for (int r = 0; r < nruns; ++r) {
+            if (runs[r].done) continue;
+            fill(B, B.nr, r);
+            B.slot[B.nr] = r;
+            if (++B.nr == LZ_MAX) {
+                cudaError_t x = launch(B);
+                if (x != cudaSuccess) return x;
+                B.nr = 0;
+            }
+        }
+        return B.nr ? launch(B) : cudaSuccess;
+    };
+    auto base = [&](LzBatch& B, int k, int r) {
+        const Run& R = runs[r];
+        B.n[k] = R.n;
+        B.dhalf[k] = R.dhalf;
+        B.v[k] = R.v;
+        B.vp[k] = R.vp;
+        B.w[k] = R.w;
+        B.tmp[k] = R.tmp;
+        B.div[k] = 0;
+        B.s[k] = 0.0;
+    };
+    auto final_dots = [&](const LzBatch& B) -> cudaError_t {
+        k_lz_final<<<B.nr, RED_THREADS, 0, s>>>(B, partials, dots);
+        count_launches(1);
+        return cudaGetLastError();
+    };
+    std::vector<double> pending_div(nruns, 0.0);   // v = v / beta at the next round's start
     for (;;) {
         bool any = false;
-        for (int r = 0; r < nruns; ++r) {
-            Run& R = runs[r];
-            if (R.done) continue;
-            any = true;
-            if ((e = launch_lanczos_scale(R.n, R.dhalf, R.v, R.tmp, s)) != cudaSuccess) return e;
-            if ((e = launch_apply(*R.L, R.mode, R.tmp, R.w, nullptr, s)) != cudaSuccess) return e;
-            if ((e = launch_lanczos_scale(R.n, R.dhalf, R.w, R.w, s)) != cudaSuccess) return e;
-            if ((e = launch_axpby(R.n, -R.beta, R.vp, 1.0, R.w, s)) != cudaSuccess) return e;
-            if ((e = launch_dot(R.n, R.v, R.w, partials + (int64_t)r * 2 * RED_BLOCKS, dots + r, s)) !=
-                cudaSuccess)
-                return e;
-        }
+        for (int r = 0; r < nruns; ++r) any = any || !runs[r].done;
         if (!any) break;
+        // (v = v / beta;) tmp = D^-1/2 v
+        e = batches([&](LzBatch& B, int k, int r) {
+                        base(B, k, r);
+                        B.div[k] = pending_div[r] != 0.0;
+                        B.s[k] = pending_div[r];
+                    },
+                    [&](const LzBatch& B) -> cudaError_t {
+                        k_lz_pre<<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B);
+                        count_launches(1);
+                        return cudaGetLastError();
+                    });
+        if (e != cudaSuccess) return e;
+        for (int r = 0; r < nruns; ++r) {
+            pending_div[r] = 0.0;
+            Run& R = runs[r];
+            if (R.done) continue;
+            if ((e = launch_apply(*R.L, R.mode, R.tmp, R.w, nullptr, s)) != cudaSuccess) return e;
+        }
+        // w = D^-1/2 w - beta v_prev;  alpha = v.w
+        e = batches([&](LzBatch& B, int k, int r) {
+                        base(B, k, r);
+                        B.s[k] = runs[r].beta;
+                    },
+                    [&](const LzBatch& B) -> cudaError_t {
+                        k_lz_update<true><<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B, partials);
+                        count_launches(1);
+                        cudaError_t x = cudaGetLastError();
+                        return x != cudaSuccess ? x : final_dots(B);
+                    });
+        if (e != cudaSuccess) return e;
         if ((e = fetch()) != cudaSuccess) return e;
+        // largest Ritz value of every active run (it drives the stopping test;
+        // the smallest is needed only once a run stops): independent
+        // bisections, spread over the host cores
+        for (int r = 0; r < nruns; ++r)
+            if (!runs[r].done) runs[r].alphas.push_back(host[r]);
+#pragma omp parallel for schedule(dynamic, 1)
         for (int r = 0; r < nruns; ++r) {
             Run& R = runs[r];
             if (R.done) continue;
-            const double alpha = host[r];
-            if ((e = launch_axpby(R.n, -alpha, R.v, 1.0, R.w, s)) != cudaSuccess) return e;
-            R.alphas.push_back(alpha);
-            if (R.betas.empty()) {
-                R.lo = R.hi = alpha;
-            } else {
-                R.lo = tridiag_eig(R.alphas, R.betas, 0);
-                R.hi = tridiag_eig(R.alphas, R.betas, (int)R.alphas.size() - 1);
-            }
-            if ((e = launch_dot(R.n, R.w, R.w, partials + (int64_t)r * 2 * RED_BLOCKS, dots + r, s)) !=
-                cudaSuccess)
-                return e;
+            if (R.betas.empty()) R.lo = R.hi = R.alphas.back();
+            else R.hi = tridiag_eig(R.alphas, R.betas, (int)R.alphas.size() - 1);
         }
+        // w -= alpha v;  beta^2 = w.w
+        e = batches([&](LzBatch& B, int k, int r) {
+                        base(B, k, r);
+                        B.s[k] = runs[r].alphas.back();
+                    },
+                    [&](const LzBatch& B) -> cudaError_t {
+                        k_lz_update<false><<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B, partials);
+                        count_launches(1);
+                        cudaError_t x = cudaGetLastError();
+                        return x != cudaSuccess ? x : final_dots(B);
+                    });
+        if (e != cudaSuccess) return e;
         if ((e = fetch()) != cudaSuccess) return e;
         for (int r = 0; r < nruns; ++r) {
             Run& R = runs[r];
@@ -139,6 +292,7 @@ cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* mod
                 R.done = true;
                 continue;
             }
+            // (the stopping run's smallest Ritz value is taken after the loop)
             R.prev = R.hi;
             R.has_prev = true;
             R.betas.push_back(beta);
@@ -146,14 +300,27 @@ cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* mod
             R.vp = R.v;
             R.v = R.w;
             R.w = old_vp;
-            if ((e = launch_div(R.n, R.v, nullptr, beta, R.v, s)) != cudaSuccess) return e;
+            pending_div[r] = beta;   // v = w / beta, fused into the next round's scaling
             if (R.left <= 0) R.done = true;
+        }
+    }
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < nruns; ++r) {
+        Run& R = runs[r];
+        if (!R.betas.empty() || R.alphas.size() > 1) {
+            // T of the final Ritz values: alphas[0..m), betas[0..m-1)
+            std::vector<double> b(R.betas.begin(), R.betas.begin() + (R.alphas.size() - 1));
+            R.lo = tridiag_eig(R.alphas, b, 0);
         }
     }
     for (int r = 0; r < nruns; ++r) {
         lo_hi[2 * r] = runs[r].lo;
         lo_hi[2 * r + 1] = runs[r].hi;
     }
+    if (getenv("PFF_LANCZOS_DEBUG"))
+        for (int r = 0; r < nruns; ++r)
+            fprintf(stderr, "lanczos run %d: n %lld mode %d, %zu iterations, [%.6g, %.6g]\n", r,
+                    (long long)runs[r].n, runs[r].mode, runs[r].alphas.size(), runs[r].lo, runs[r].hi);
     return cudaSuccess;
 }
 
