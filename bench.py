@@ -309,10 +309,11 @@ def release_device_memory(torch):
 
 
 def newton_step_ours(args, P, torch):
-    """configs[3]: one Newton step's GMRES+GMG solve on 1024^2 Q2.  Run twice
-    in the process -- a fresh state and preconditioner each time; the first
-    (cold: module loads, graph capture first use) is reported as cold_*, the
-    second is the steady-state figure a simulation sees every step."""
+    """configs[3]: one Newton step's GMRES+GMG solve on 1024^2 Q2.  A fresh
+    state and preconditioner each time: the first solve (cold: module loads,
+    graph capture first use) is reported as cold_*, then three warm solves,
+    of which the median (setup + GMRES) is the steady-state figure a
+    simulation sees every step."""
     level = args.newton_level
     h, params, U, pt, act, dirn, x = baseline_inputs(2, level, args.split, seed=0, notch=True)
     rhs = x.copy()
@@ -321,6 +322,8 @@ def newton_step_ours(args, P, torch):
     rhs[np.concatenate([dmask, dmask, act])] = 0.0
     rhs_h = torch.from_numpy(rhs).pin_memory()
     sol_h = torch.empty(rhs_h.numel(), dtype=torch.float64, pin_memory=True)
+
+    phases = {}
 
     def one():
         st = P.LinearizationState(h, level, params, split=args.split)
@@ -332,12 +335,19 @@ def newton_step_ours(args, P, torch):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st.refresh_cache()
+        torch.cuda.synchronize()
+        ta = time.perf_counter()
         gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
         gmg.setup(st)
+        torch.cuda.synchronize()
+        tb = time.perf_counter()
         gmg.io_buffers()[0].zero_()
         gmg.run_cycle()                       # CUDA-graph capture counted as setup
         torch.cuda.synchronize()
         t_setup = time.perf_counter() - t0
+        phases["refresh_s"] = round(ta - t0, 4)
+        phases["gmg_setup_s"] = round(tb - ta, 4)
+        phases["graph_capture_s"] = round(t0 + t_setup - tb, 4)
         t1 = time.perf_counter()
         rhs_d = rhs_h.to("cuda", non_blocking=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -357,9 +367,17 @@ def newton_step_ours(args, P, torch):
     t_setup, t_gmres = c_setup, c_gmres
     release_device_memory(torch)
     warm = 8 * n * (70 + 3 * 51) < 0.45 * torch.cuda.get_device_properties(0).total_memory
+    runs = []
     if warm:
-        res, t_setup, t_gmres, t_dev = one()
-        release_device_memory(torch)
+        # steady state: median of three warm solves (host-side timing noise on
+        # shared boxes is large; each run's numbers are kept below)
+        for _ in range(3):
+            runs.append(one() + (dict(phases),))
+            release_device_memory(torch)
+        runs.sort(key=lambda r: r[1] + r[2])
+        res, t_setup, t_gmres, t_dev, mid_phases = runs[len(runs) // 2]
+        phases.clear()
+        phases.update(mid_phases)
     # HBM floor of the solve: per fine scalar node and GMRES
     # iteration j, 2.53 kB for the V-cycle over all levels (sweeps=3), 81 B for
     # the operator and 72 (j+2) B for orthogonalisation + normalisation
@@ -370,7 +388,8 @@ def newton_step_ours(args, P, torch):
                       "restart 50, rtol 1e-8",
             "split": args.split, "iterations": res.iterations, "converged": res.converged,
             "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
-            "total_s": round(t_setup + t_gmres, 4),
+            "total_s": round(t_setup + t_gmres, 4), "setup_phases": dict(phases),
+            "warm_runs_total_s": [round(r[1] + r[2], 4) for r in runs],
             "cold_setup_s": round(c_setup, 4), "cold_gmres_s": round(c_gmres, 4),
             "gmres_device_s": round(t_dev, 4),
             "roofline": {"bound": "hbm", "floor_s": round(floor_s, 4),
@@ -378,7 +397,8 @@ def newton_step_ours(args, P, torch):
                          "model": "SURVEY.md 8(d) fused-minimum dataflow: per fine node and "
                                   "iteration 2.53 kB V-cycle + 81 B operator + 72(j+2) B MGS"},
             "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
-            "note": ("second solve in the process (fresh state + preconditioner)" if warm
+            "note": ("median of three warm solves (fresh state + preconditioner each) after a "
+                     "cold one" if warm
                      else "single (cold) solve: two hierarchies would not fit next to each other")
                     + "; gmres_s includes the rhs H2D and solution D2H"}
 

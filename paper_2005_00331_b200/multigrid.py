@@ -15,6 +15,7 @@ import ctypes
 import logging
 import os
 import threading
+import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from functools import cached_property
@@ -688,7 +689,10 @@ class GmgPreconditioner:
         # (shared-memory attributes, occupancy queries) outside capture
         key = (self.hierarchy.degree, self.finest, self.coarse_level,
                self.states[self.finest].split)
-        if key not in _EAGER_DONE:
+        dbg = os.environ.get("PFF_CAPTURE_DEBUG")
+        t0 = time.perf_counter()
+        eager = key not in _EAGER_DONE
+        if eager:
             self._vcycle(self.finest, top.r, top.z)
             _EAGER_DONE.add(key)
         else:
@@ -697,10 +701,16 @@ class GmgPreconditioner:
             for s in self.states.values():
                 s.bind()
         torch.cuda.synchronize()
+        t1 = time.perf_counter()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
             self._vcycle(self.finest, top.r, top.z)
         self._graph = g
+        if dbg:
+            torch.cuda.synchronize()
+            logger.warning("capture: %s %.1f ms, capture+instantiate %.1f ms",
+                           "eager pass" if eager else "bind", (t1 - t0) * 1e3,
+                           (time.perf_counter() - t1) * 1e3)
 
     # -- device V-cycle (src/multigrid.py:295-344) ---------------------------------
     def _cheb(self, l, mode, rhs, a, b, sweeps, out, assign, pre_d=False):

@@ -30,8 +30,16 @@ MG.op.restrict_state_to_level = timed("inject+coarse refresh", OP.restrict_state
 MG.op.block_diagonals = timed("diagonals", OP.block_diagonals)
 MG.GmgPreconditioner._estimate_ranges_batched = timed(
     "lanczos", MG.GmgPreconditioner._estimate_ranges_batched)
+MG.GmgPreconditioner._build_dense_coarse = timed(
+    "dense coarse", MG.GmgPreconditioner._build_dense_coarse)
+EMPTY = "--empty-cache" in sys.argv   # bench.py's pattern: release the cache between solves
 for rep in range(3):
     T.clear()
+    if EMPTY:
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
     st = P.LinearizationState(h, 10, params, split="miehe")
     st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
     st.set_dirichlet_nodes(dirn)
