@@ -691,6 +691,30 @@ k_sweep_q2(const SweepArgs A) {
     }
 }
 
+// smallest chunk (cell rows per warp item) of the auto chunking: every item
+// re-does one halo cell row, and each row step waits on its TMA stage, so
+// small meshes trade redundant work for fewer dependent steps per item
+int sweep_min_rows() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PFF_SWEEP_MIN_ROWS");
+        v = e ? atoi(e) : 1;   // measured: 1 beats 4 on the 64^2-256^2 levels (Newton -4.6 ms)
+        if (v < 1) v = 1;
+    }
+    return v;
+}
+
+// smallest mesh (cells per side) routed to the sweep kernel; below it the
+// generic cooperative kernel is faster (latency-bound levels)
+int sweep_min_nside() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PFF_SWEEP_MIN_NSIDE");
+        v = e ? atoi(e) : 64;
+    }
+    return v;
+}
+
 struct LaunchCfg {
     bool init = false;
     int blocks_per_sm = 0;
@@ -724,7 +748,8 @@ cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
         if (chunks < 1) chunks = 1;
         if (chunks > ns) chunks = ns;
         rows = (ns + chunks - 1) / chunks;
-        if (rows < 4) rows = ns < 4 ? ns : 4;
+        const int rmin = sweep_min_rows();
+        if (rows < rmin) rows = ns < rmin ? ns : rmin;
     }
     if (rows > ns) rows = ns;
     a.rows_per_chunk = rows;
@@ -766,16 +791,6 @@ cudaError_t launch_cheb(int mode, SweepArgs& a, cudaStream_t s, int rows) {
 
 int g_rows_override = 0;
 
-// smallest mesh (cells per side) routed to the sweep kernel; below it the
-// generic cooperative kernel is faster (latency-bound levels)
-int sweep_min_nside() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PFF_SWEEP_MIN_NSIDE");
-        v = e ? atoi(e) : 64;
-    }
-    return v;
-}
 
 }  // namespace
 
