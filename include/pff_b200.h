@@ -245,6 +245,14 @@ int pff_apply_cheb_first(const pff_level* L, int mode, const double* d, double* 
                          const double* rhs, double* cr, const double* invd, double* acc,
                          double c1, double c2, void* stream);
 
+/* pff_apply_cheb with options: PFF_CHEB_FIRST = pff_apply_cheb_first's
+ * acc += d + d'; PFF_CHEB_LAST = the last step of a pass: only acc is
+ * written (cr and d_out are not stored; nothing reads them afterwards). */
+enum { PFF_CHEB_FIRST = 1, PFF_CHEB_LAST = 2 };
+int pff_apply_cheb_ex(const pff_level* L, int mode, const double* d, double* d_out,
+                      const double* rhs, double* cr, const double* invd, double* acc, double c1,
+                      double c2, int flags, void* stream);
+
 /* Fused residual dst = rhs - G src (mode FULL or PHIROW) that also emits the
  * next smoothing block's Chebyshev start d0 = invd * dst / theta (FULL: the
  * two u components, invd/d0 of length 2n; PHIROW: the phi output, length n)

@@ -38,6 +38,8 @@ SIGNATURES = {
                             _d, ctypes.c_void_p]),
     "pff_apply_cheb_first": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp,
                                   _d, _d, ctypes.c_void_p]),
+    "pff_apply_cheb_ex": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp,
+                               _d, _d, _i, ctypes.c_void_p]),
     "pff_apply_emit": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _d,
                             ctypes.c_void_p]),
     "pff_smooth_init": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _d,
@@ -78,6 +80,7 @@ FLAG_DIRICHLET, FLAG_ACTIVE = 1, 2
 LAYOUT_FULL, LAYOUT_UU, LAYOUT_PHI = 0, 1, 2
 CONS_SELECT, CONS_ZERO, CONS_COPY, CONS_EXCLUDE = 0, 1, 2, 3
 OPT_GENERIC_APPLY, OPT_SWEEP_ROWS = 1, 2
+CHEB_FIRST, CHEB_LAST = 1, 2
 
 
 def set_option(key: int, value: int):

@@ -175,17 +175,25 @@ int pff_apply_cheb(const pff_level* h, int mode, const double* d, double* d_out,
     return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb");
 }
 
+int pff_apply_cheb_ex(const pff_level* h, int mode, const double* d, double* d_out,
+                      const double* rhs, double* cr, const double* invd, double* acc, double c1,
+                      double c2, int flags, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
+        return fail(PFF_E_UNBOUND, "%s", "pff_apply_cheb_ex: state not bound");
+    if ((mode != 1 && mode != 2) || !d || !d_out || !rhs || !cr || !invd || !acc || d_out == d ||
+        (flags & ~(PFF_CHEB_FIRST | PFF_CHEB_LAST)))
+        return fail(PFF_E_ARG, "%s", "pff_apply_cheb_ex: mode must be UU or PHIPHI, d_out != d, known flags");
+    pff::ChebArgs cb{invd, d_out, acc, c1, c2};
+    cb.acc_src = (flags & PFF_CHEB_FIRST) ? 1 : 0;
+    cb.last = (flags & PFF_CHEB_LAST) ? 1 : 0;
+    return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb_ex");
+}
+
 int pff_apply_cheb_first(const pff_level* h, int mode, const double* d, double* d_out,
                          const double* rhs, double* cr, const double* invd, double* acc,
                          double c1, double c2, void* stream) {
-    const Level* L = reinterpret_cast<const Level*>(h);
-    if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
-        return fail(PFF_E_UNBOUND, "%s", "pff_apply_cheb_first: state not bound");
-    if ((mode != 1 && mode != 2) || !d || !d_out || !rhs || !cr || !invd || !acc || d_out == d)
-        return fail(PFF_E_ARG, "%s", "pff_apply_cheb_first: mode must be UU or PHIPHI, d_out != d");
-    pff::ChebArgs cb{invd, d_out, acc, c1, c2};
-    cb.acc_src = 1;
-    return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb_first");
+    return pff_apply_cheb_ex(h, mode, d, d_out, rhs, cr, invd, acc, c1, c2, PFF_CHEB_FIRST, stream);
 }
 
 int pff_apply_emit(const pff_level* h, int mode, const double* src, double* dst,

@@ -151,6 +151,9 @@ struct ChebArgs {
     // acc_src: acc += d + d' (the first step after a producer emitted d0 = d;
     // (acc + d) + d' rounds exactly like the separate pff_cheb_init pass)
     int acc_src = 0;
+    // last: the final step of a pass -- only acc is consumed, so the residual
+    // (dst) and d' (dout) stores are skipped
+    int last = 0;
     // residual producers (fused form, no dout): d0 = invd * dst / theta on the
     // first emit_nc output components (pff_cheb_init's d, same rounding)
     double* emit = nullptr;

@@ -110,6 +110,7 @@ struct SweepArgs {
     double* acc[3];
     double c1, c2;
     int acc_src;                  // first Chebyshev step: acc += d + d'
+    int last;                     // last Chebyshev step: only acc is stored
     // EMIT: d0 = invd * dst / theta on the first emit_nc components (reuses invd)
     double* emit[2];
     double theta;
@@ -360,13 +361,13 @@ k_sweep_q2(const SweepArgs A) {
                     sv = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k) : A.src_out[c][gid];
                 if (cons) x = sv;
                 if (FUSED) x = rh[0][c] - x;
-                A.dst[c][gid] = x;
+                if (!CHEB || !A.last) A.dst[c][gid] = x;
                 if (EMIT && c < A.emit_nc) A.emit[c][gid] = rh[1][c] * x / A.theta;   // next block's d0
                 if (CHEB) {
                     const double iv = rh[1][c];
                     const double av = rh[2][c];
                     const double dn = cheb_update(A.c1, sv, A.c2, iv, x);
-                    A.dout[c][gid] = dn;
+                    if (!A.last) A.dout[c][gid] = dn;
                     A.acc[c][gid] = (A.acc_src ? av + sv : av) + dn;
                 }
             }
@@ -887,6 +888,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
     for (int c = 0; c < 3; ++c) { a.invd[c] = nullptr; a.dout[c] = nullptr; a.acc[c] = nullptr; }
     a.c1 = a.c2 = 0.0;
     a.acc_src = 0;
+    a.last = 0;
     a.emit[0] = a.emit[1] = nullptr;
     a.theta = 1.0;
     a.emit_nc = 0;
@@ -911,6 +913,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         a.c1 = cheb->c1;
         a.c2 = cheb->c2;
         a.acc_src = cheb->acc_src;
+        a.last = cheb->last;
     }
     a.n_strips = L.n_strips();
     int rows = g_rows_override;

@@ -18,62 +18,71 @@ namespace pff {
 
 namespace {
 
-struct Owner {
-    int ccx, ccy, chx, chy, a, b;
-};
-
-__device__ __forceinline__ Owner fine_owner(const Mesh& mf, int64_t gid) {
-    int64_t i, j;
-    bool dup = gid >= mf.n_grid;
-    if (dup) {
-        i = gid - mf.n_grid;
-        j = mf.i_mid;
-    } else {
-        i = gid % mf.np1;
-        j = gid / mf.np1;
-    }
-    const int p = mf.p;
-    auto lowest = [&](int64_t k) -> int {
-        int64_t c = (k % p == 0 && k > 0) ? k / p - 1 : k / p;
-        return (int)(c < mf.nside ? c : mf.nside - 1);
-    };
-    int fx = lowest(i);
-    int fy = dup ? (mf.nside >> 1) : lowest(j);
-    Owner o;
-    o.a = (int)(i - (int64_t)p * fx);
-    o.b = (int)(j - (int64_t)p * fy);
-    o.ccx = fx >> 1;
-    o.ccy = fy >> 1;
-    o.chx = fx & 1;
-    o.chy = fy & 1;
-    return o;
-}
-
-template <int P>
-__global__ void k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
-                          double* __restrict__ yf, const uint8_t* __restrict__ flags_f,
-                          int add_masked) {
+// One thread per owned fine node.  The embedding table sits in shared memory
+// (runtime-indexed), the owner cell comes from 32-bit index math when the
+// level has < 2^31 nodes, and the per-direction weights are read once; the
+// sums keep the (my, mx) order and the |w| > 1e-14 filter of the reference's
+// CSR rows, so the result is the same bit for bit.
+template <int P, bool SMALL>
+__global__ void __launch_bounds__(256)
+k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
+          double* __restrict__ yf, const uint8_t* __restrict__ flags_f, int add_masked) {
     constexpr int N1 = P + 1;
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ double Es[2][N1][N1];
+    for (int k = threadIdx.x; k < 2 * N1 * N1; k += blockDim.x) {
+        const int c = k / (N1 * N1), r = (k / N1) % N1, m = k % N1;
+        Es[c][r][m] = E.E[c][r][m];
+    }
+    __syncthreads();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= wf.n_owned(mf)) return;
     const int64_t gg = wf.owned_global(mf, t);
-    Owner o = fine_owner(mf, gg);
+    // fine grid position and owner (the lowest containing fine cell; the
+    // upper slit copies belong to the upper cell row)
+    int64_t i, j;
+    const bool dup = gg >= mf.n_grid;
+    if (dup) {
+        i = gg - mf.n_grid;
+        j = mf.i_mid;
+    } else if (SMALL) {
+        const uint32_t g32 = (uint32_t)gg, w32 = (uint32_t)mf.np1;
+        const uint32_t jj = g32 / w32;
+        j = jj;
+        i = g32 - jj * w32;
+    } else {
+        j = gg / mf.np1;
+        i = gg - j * mf.np1;
+    }
+    auto lowest = [&](int64_t k) -> int {
+        const int64_t c = k > 0 ? (k - 1) / P : 0;
+        return (int)(c < mf.nside ? c : mf.nside - 1);
+    };
+    const int fx = lowest(i);
+    const int fy = dup ? (mf.nside >> 1) : lowest(j);
+    const int a = (int)(i - (int64_t)P * fx), b = (int)(j - (int64_t)P * fy);
+    const int ccx = fx >> 1, ccy = fy >> 1, chx = fx & 1, chy = fy & 1;
     const int64_t g = wf.loc(mf, gg);     // local index of the fine node
+    double wx[N1], wy[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+        wx[m] = Es[chx][a][m];
+        wy[m] = Es[chy][b][m];
+    }
     double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int my = 0; my < N1; ++my)
 #pragma unroll
         for (int mx = 0; mx < N1; ++mx) {
-            double w = E.E[o.chy][o.b][my] * E.E[o.chx][o.a][mx];
+            const double w = wy[my] * wx[mx];
             if (fabs(w) > 1e-14) {
-                int64_t c = mc.node(o.ccx, o.ccy, mx, my);
+                const int64_t c = mc.node(ccx, ccy, mx, my);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) acc[k] = fma(w, xc[k * mc.n + c], acc[k]);
             }
         }
     if (add_masked) {
         // z += where(cons, 0, P zc)  (src/multigrid.py:340-342)
-        uint8_t f = flags_f[g];
+        const uint8_t f = flags_f[g];
         if (!(f & F_DIR)) {
             yf[g] += acc[0];
             yf[wf.n + g] += acc[1];
@@ -125,7 +134,7 @@ k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, dou
     // The fine nodes of the coarse cell's block, each once: rows 0..p of the
     // lower child, then rows 0..p of the upper child, whose row 0 repeats the
     // lower child's row p except where the slit splits it (coarse level 0).
-    // First-visit ownership (fine_owner) in closed form: the cell owns a
+    // First-visit ownership (as k_prolong's owner) in closed form: the cell owns a
     // block node unless it lies on the block's left column (ccx > 0) or
     // bottom row (ccy > 0) -- those belong to the neighbour -- except the
     // upper slit copies, owned by the upper cell row.  The owner's child and
@@ -182,6 +191,59 @@ k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, dou
 #pragma unroll
             for (int k = 0; k < 3; ++k) xc[k * mc.n + c] += acc[k][my][mx];
         }
+}
+
+// Element-vector form of the restriction, one thread per (coarse cell,
+// component k, coarse basis row my): the thread accumulates acc[mx] =
+// ev[k][cell][my][mx] over the cell's owned fine nodes in the same (fb, fa)
+// order as k_restrict's per-cell accumulator, so the element vectors are the
+// same bit for bit with 3 (p+1) times the parallelism (the small levels are
+// latency-bound on that per-thread chain).  Threads of a warp share (k, my):
+// uniform weights and branches.
+template <int P>
+__global__ void __launch_bounds__(128)
+k_restrict_ev(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, int cy0, int hy,
+              double* __restrict__ ev) {
+    constexpr int N1 = P + 1, QQ = N1 * N1;
+    const int64_t ncw = (int64_t)mc.nside * hy;          // coarse cells of the window rows
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncw * 3 * N1) return;
+    const int km = (int)(t / ncw);                         // k * N1 + my
+    const int64_t cw = t - (int64_t)km * ncw;
+    const int k = km / N1, my = km % N1;
+    const int ccx = (int)(cw % mc.nside), ccy = cy0 + (int)(cw / mc.nside);
+    const double* yk = yf + (int64_t)k * wf.n;
+    double acc[N1] = {};
+#pragma unroll
+    for (int fb = 0; fb <= 2 * P + 1; ++fb) {
+        const bool up = fb > P;
+        const int chy = up ? 1 : 0, lb = up ? fb - P - 1 : fb;
+        const int fcy = 2 * ccy + chy;
+        const int64_t j = (int64_t)P * fcy + lb;
+        const double ey = E.E[chy][lb][my];
+#pragma unroll
+        for (int fa = 0; fa <= 2 * P; ++fa) {
+            const int chx = fa > P ? 1 : 0, la = fa - P * chx;
+            const int fcx = 2 * ccx + chx;
+            const int64_t i = (int64_t)P * fcx + la;
+            const bool dup = mf.level >= 1 && fcy >= (mf.nside >> 1) && j == mf.i_mid && i < mf.i_mid;
+            if (up && lb == 0 && !dup) continue;
+            if (fa == 0 && ccx > 0) continue;
+            if (fb == 0 && ccy > 0 && !dup) continue;
+            if (dup ? !wf.owns_dup : (j < wf.own_lo || j >= wf.own_hi)) continue;
+            const int64_t gg = dup ? mf.n_grid + i : j * mf.np1 + i;
+            const double v = yk[wf.loc(mf, gg)];
+#pragma unroll
+            for (int mx = 0; mx < N1; ++mx) {
+                const double w = ey * E.E[chx][la][mx];
+                if (fabs(w) > 1e-14) acc[mx] += w * v;
+            }
+        }
+    }
+    const int64_t nc = mc.n_cells(), cell = (int64_t)ccy * mc.nside + ccx;
+    double* o = ev + ((int64_t)k * nc + cell) * QQ + my * N1;
+#pragma unroll
+    for (int mx = 0; mx < N1; ++mx) o[mx] = acc[mx];
 }
 
 // coarse node gather of the element vectors (cell rows [lo, hi)), zeroing the
@@ -252,13 +314,18 @@ cudaError_t launch_prolongate(const Level& F, const Level& C, const double* xc, 
     if (C.windowed()) return cudaErrorNotSupported;   // coarse side is always whole-mesh
     const Win wf = F.win();
     const int64_t nf = wf.n_owned(F.mesh);
+    const bool small = F.mesh.n < (int64_t(1) << 31);
+#define PFF_PROLONG(PP)                                                                          \
+    (small ? k_prolong<PP, true> : k_prolong<PP, false>)<<<blocks(nf), 256, 0, s>>>(             \
+        F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked)
     switch (F.mesh.p) {
-        case 1: k_prolong<1><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
-        case 2: k_prolong<2><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
-        case 3: k_prolong<3><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
-        case 4: k_prolong<4><<<blocks(nf), 256, 0, s>>>(F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked); break;
+        case 1: PFF_PROLONG(1); break;
+        case 2: PFF_PROLONG(2); break;
+        case 3: PFF_PROLONG(3); break;
+        case 4: PFF_PROLONG(4); break;
         default: return cudaErrorInvalidValue;
     }
+#undef PFF_PROLONG
     count_launches(1);
     return cudaGetLastError();
 }
@@ -280,13 +347,25 @@ cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, do
         all.hx = nsc;
         all.cy0 = lo;
         all.hy = hi - lo;
-        const unsigned g = (unsigned)(((int64_t)all.hx * all.hy + 127) / 128);
         double* ev = C.ev();
-        switch (F.mesh.p) {
-            case 1: k_restrict<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
-            case 2: k_restrict<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
-            case 3: k_restrict<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
-            case 4: k_restrict<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+        // measured: the per-(cell, component, row) split wins on the latency-bound
+        // small levels, the per-cell kernel on the large ones (fewer loads)
+        const bool split = nsc <= 64;
+        const int64_t nthr = (int64_t)all.hx * all.hy * (split ? 3 * (F.mesh.p + 1) : 1);
+        const unsigned g = (unsigned)((nthr + 127) / 128);
+        if (!split) {
+            switch (F.mesh.p) {
+                case 1: k_restrict<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+                case 2: k_restrict<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+                case 3: k_restrict<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+                case 4: k_restrict<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+                default: return cudaErrorInvalidValue;
+            }
+        } else switch (F.mesh.p) {
+            case 1: k_restrict_ev<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
+            case 2: k_restrict_ev<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
+            case 3: k_restrict_ev<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
+            case 4: k_restrict_ev<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
             default: return cudaErrorInvalidValue;
         }
         const unsigned gn = blocks(C.mesh.n);

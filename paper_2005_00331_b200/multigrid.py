@@ -735,9 +735,9 @@ class GmgPreconditioner:
             rho_old = 1.0 / sigma1
             for k in range(1, sweeps):
                 rho = 1.0 / (2.0 * sigma1 - rho_old)
-                call("pff_apply_cheb_first" if k == 1 else "pff_apply_cheb", h, mode, ptr(d_in),
-                     ptr(d_out), ptr(src), ptr(cr), ptr(inv), ptr(acc), rho * rho_old,
-                     2.0 * rho / delta, st)
+                fl = (_lib.CHEB_FIRST if k == 1 else 0) | (_lib.CHEB_LAST if k == sweeps - 1 else 0)
+                call("pff_apply_cheb_ex", h, mode, ptr(d_in), ptr(d_out), ptr(src), ptr(cr),
+                     ptr(inv), ptr(acc), rho * rho_old, 2.0 * rho / delta, fl, st)
                 rho_old = rho
                 src = cr
                 d_in, d_out = d_out, d_in
@@ -753,8 +753,9 @@ class GmgPreconditioner:
             rho_old = 1.0 / sigma1
             for k in range(1, sweeps):
                 rho = 1.0 / (2.0 * sigma1 - rho_old)
-                call("pff_apply_cheb", h, mode, ptr(d_in), ptr(d_out), ptr(src), ptr(cr),
-                     ptr(inv), ptr(acc), rho * rho_old, 2.0 * rho / delta, st)
+                call("pff_apply_cheb_ex", h, mode, ptr(d_in), ptr(d_out), ptr(src), ptr(cr),
+                     ptr(inv), ptr(acc), rho * rho_old, 2.0 * rho / delta,
+                     _lib.CHEB_LAST if k == sweeps - 1 else 0, st)
                 rho_old = rho
                 src = cr
                 d_in, d_out = d_out, d_in
