@@ -141,6 +141,43 @@ __device__ __forceinline__ void node_cells(const Mesh& m, int64_t g, int row_lo,
     }
 }
 
+// node_cells with the degree P at compile time and 32-bit index math (levels
+// with fewer than 2^31 nodes): no 64-bit divisions -- the per-node gathers
+// are instruction-bound on those.  Same cells, same order.
+template <int P, class F>
+__device__ __forceinline__ void node_cells_p(const Mesh& m, int64_t g, int row_lo, int row_hi,
+                                             F&& f) {
+    if (m.n >= (int64_t(1) << 31)) {
+        node_cells(m, g, row_lo, row_hi, f);
+        return;
+    }
+    const int ns = m.nside, np1 = (int)m.np1, imid = (int)m.i_mid;
+    const int g32 = (int)g, ngrid = (int)m.n_grid;
+    int i, j;
+    int cy_lo = row_lo, cy_hi = row_hi < ns ? row_hi : ns;
+    if (g32 < ngrid) {
+        j = (int)((unsigned)g32 / (unsigned)np1);
+        i = g32 - j * np1;
+        if (m.level >= 1 && j == imid && i < imid && cy_hi > (ns >> 1)) cy_hi = ns >> 1;
+    } else {
+        i = g32 - ngrid;
+        j = imid;
+        if (cy_lo < (ns >> 1)) cy_lo = ns >> 1;
+    }
+    const int cy0 = j > 0 ? (j - 1) / P : 0, cy1 = j / P;
+    const int cx0 = i > 0 ? (i - 1) / P : 0, cx1 = i / P;
+    for (int cy = cy0; cy <= cy1; ++cy) {
+        if (cy < cy_lo || cy >= cy_hi) continue;
+        const int b = j - cy * P;
+        if (b < 0 || b > P) continue;
+        for (int cx = cx0; cx <= cx1 && cx < ns; ++cx) {
+            const int a = i - cx * P;
+            if (a < 0 || a > P) continue;
+            f(cx, cy, a, b);
+        }
+    }
+}
+
 // a Chebyshev step fused into a block application (pff_apply_cheb): after
 // cr = cr - G d, d_out = c1 d + c2 invd cr and acc += d_out, per component
 struct ChebArgs {

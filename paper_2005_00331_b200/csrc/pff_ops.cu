@@ -194,7 +194,7 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
         cons[c] = comp[c] < 2 ? (f & F_DIR) : (f & F_ACT);
     }
     double acc[3] = {0.0, 0.0, 0.0};
-    node_cells(m, i, 0, m.nside, [&](int cx, int cy, int a, int b) {
+    node_cells_p<P>(m, i, 0, m.nside, [&](int cx, int cy, int a, int b) {
         const int64_t cell = (int64_t)cy * m.nside + cx;
 #pragma unroll
         for (int c = 0; c < NO; ++c)

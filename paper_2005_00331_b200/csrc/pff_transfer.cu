@@ -256,7 +256,7 @@ __global__ void k_restrict_gather(Mesh mc, const double* __restrict__ ev, double
     if (c >= mc.n) return;
     const int64_t nc = mc.n_cells();
     double acc[3] = {0.0, 0.0, 0.0};
-    node_cells(mc, c, lo, hi, [&](int cx, int cy, int a, int b) {
+    node_cells_p<P>(mc, c, lo, hi, [&](int cx, int cy, int a, int b) {
         const int64_t cell = (int64_t)cy * mc.nside + cx;
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc[k] += ev[((int64_t)k * nc + cell) * QQ + b * N1 + a];
