@@ -263,7 +263,8 @@ def run_ours(args):
         return
     peak, peak_src = peaks()
     achieved = BYTES_PER_DOF * dofs / ws / (ms_step * 1e-3) / 1e9   # per GPU
-    cpu = cpu_baseline(args) if not args.no_cpu_baseline else None
+    # the CPU baseline is an N=1 figure (rank 0 at N=1 only); the N>1 lines skip it
+    cpu = cpu_baseline(args) if (not args.no_cpu_baseline and ws == 1) else None
     out = {
         "metric": "GDoF/s of fp64 Jacobian vmult (apply_jacobian, 1024^2 Q2)",
         "value": round(value, 3),
