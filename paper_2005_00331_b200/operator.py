@@ -357,6 +357,23 @@ _NC_IN = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHI
 _NC_OUT = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 1}
 
 
+# chunk weights of the pipeline: small first and last chunks shorten the fill
+# (the first chunk's H2D runs alone) and the drain (the last chunk's D2H)
+_PIPE_RAMP = (1, 2, 4, 4, 4, 4, 4, 4, 2, 1)
+
+
+def _pipe_cuts(ns: int):
+    w = _PIPE_RAMP if _PIPE_RAMP else (1,) * _PIPE_CHUNKS
+    if len(w) > ns:
+        w = (1,) * min(_PIPE_CHUNKS, ns)
+    tot = float(sum(w))
+    cuts, acc = [0], 0.0
+    for x in w:
+        acc += x
+        cuts.append(int(round(acc / tot * ns)))
+    return [c for i, c in enumerate(cuts) if i == 0 or c > cuts[i - 1]]
+
+
 def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor) -> torch.Tensor:
     """Host (pinned) -> device -> host application with the transfers of
     cell-row chunks overlapped with the sweep kernel (pff_apply_rows): H2D of
@@ -374,8 +391,8 @@ def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor) -> torch.
     main = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     s_in.wait_stream(main)
-    K = min(_PIPE_CHUNKS, ns)
-    cuts = [k * ns // K for k in range(K + 1)]
+    cuts = _pipe_cuts(ns)
+    K = len(cuts) - 1
     ev_out = []
     loaded = -1                      # last node row already on the device
     dups_in = nd == 0

@@ -20,8 +20,12 @@ xh = torch.from_numpy(x).pin_memory()
 xd = torch.from_numpy(x).cuda()
 yd = torch.empty_like(xd)
 st.apply_into(0, xd, yd)
-for K in (2, 4, 6, 8, 12, 16):
-    OP._PIPE_CHUNKS = K
+RAMPS = {"uniform8": None, "ramp10": (1, 2, 4, 4, 4, 4, 4, 4, 2, 1),
+         "ramp12": (1, 2, 3, 4, 4, 4, 4, 4, 4, 3, 2, 1), "ramp8": (1, 3, 4, 4, 4, 4, 3, 1),
+         "ramp14": (1, 1, 2, 4, 4, 4, 4, 4, 4, 4, 4, 2, 1, 1)}
+for K, ramp in RAMPS.items():
+    OP._PIPE_CHUNKS = 8
+    OP._PIPE_RAMP = ramp
     for _ in range(3):
         y = P.apply_jacobian(st, xh)
     torch.cuda.synchronize()
@@ -31,4 +35,4 @@ for K in (2, 4, 6, 8, 12, 16):
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t) / 20
     assert torch.equal(y.cuda(), yd)
-    print(f"K={K:2d}: {dt * 1e3:.2f} ms  {3 * st.n_scalar / dt / 1e9:.2f} GDoF/s")
+    print(f"{K}: {dt * 1e3:.2f} ms  {3 * st.n_scalar / dt / 1e9:.2f} GDoF/s")
