@@ -68,6 +68,9 @@ def back(t: torch.Tensor, was_np):
     return t.cpu().numpy() if was_np else t
 
 
+_PINNED_MIN = 1 << 20   # host mirrors with at least this many entries are pinned
+
+
 class _Dual:
     """A host numpy array and its device mirror, synchronised lazily.
 
@@ -88,16 +91,26 @@ class _Dual:
         return torch.bool if self._dtype is bool else torch.from_numpy(
             np.empty(0, dtype=self._dtype)).dtype
 
+    def _alloc_host(self) -> np.ndarray:
+        # large mirrors live in pinned memory: their uploads then run at the
+        # full PCIe rate (torch's caching host allocator recycles the blocks)
+        if self._n >= _PINNED_MIN and torch.cuda.is_available():
+            return torch.empty(self._n, dtype=self._tdtype(), pin_memory=True).numpy()
+        return np.empty(self._n, dtype=self._dtype)
+
     def _host_array(self) -> np.ndarray:
         if self._h is None:
-            self._h = np.full(self._n, self._fill, dtype=self._dtype)
+            self._h = self._alloc_host()
+            self._h[:] = self._fill
             if self._tail is not None:
                 self._h[self._tail[0]:] = self._tail[1]
         return self._h
 
     def host(self) -> np.ndarray:
         if self._dev_new:
-            self._h = self._d.cpu().numpy().copy()
+            h = self._alloc_host()        # a fresh array, as before (callers may hold the old one)
+            torch.from_numpy(h).copy_(self._d)
+            self._h = h
             self._dev_new = False
         self._host_array()
         self._host_new = True
