@@ -13,7 +13,7 @@ OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libpff_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills", "-Xcompiler", "-fopenmp"]   # OpenMP: host-side Ritz values
+         "-Xptxas", "-warn-spills", "-Xcompiler", "-fopenmp"] + os.environ.get("PFF_NVCC_EXTRA", "").split()   # OpenMP: host-side Ritz values
 
 
 def _nvcc() -> str:
