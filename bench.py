@@ -247,6 +247,34 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item()) / e2e_steps
         h2d = d2h = 8 * 3 * st.ln
+    # the other split's vmult on the same inputs (N=1; not the headline: the
+    # reference default is Miehe), CUDA events over 200 applications
+    other = None
+    if ws == 1 and args.other_split:
+        osp = "none" if args.split == "miehe" else "miehe"
+        so = P.LinearizationState(h, level, params, split=osp)
+        so.set_solution(U)
+        so.set_phi_tilde(pt)
+        so.set_phi_old(pt)
+        so.set_active(act)
+        so.set_dirichlet_nodes(dirn)
+        so.refresh_cache()
+        for _ in range(max(3, args.warmup)):
+            so.apply_into(_lib.MODE_FULL, xd, yd)
+        reps = 200
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            so.apply_into(_lib.MODE_FULL, xd, yd)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        oms = e0.elapsed_time(e1) / reps
+        ov = dofs / (oms * 1e-3) / 1e9
+        opk, _ = peaks()
+        other = {"split": osp, "value": round(ov, 3), "unit": "GDoF/s", "ms_per_step": round(oms, 5),
+                 "steps": reps, "roofline_frac": round(BYTES_PER_DOF * ov / opk, 4),
+                 "traffic": traffic_from_profiles(osp)}
+        del so
     newton = None
     if args.newton:
         # the vmult state (tangent caches, vectors) is not needed any more: give its
@@ -299,6 +327,8 @@ def run_ours(args):
     }
     if newton is not None:
         out["newton_step"] = newton
+    if other is not None:
+        out["other_split"] = other
     print(json.dumps(out))
 
 
@@ -518,6 +548,8 @@ def main():
     ap.add_argument("--newton-level", type=int, default=10)
     ap.add_argument("--level", type=int, default=10, help="vmult mesh level (10 = configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-split", dest="other_split", action="store_false",
+                    help="skip the other split's vmult (reported beside the headline)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
