@@ -409,12 +409,7 @@ def newton_step_ours(args, P, torch):
         res, t_setup, t_gmres, t_dev, mid_phases = runs[len(runs) // 2]
         phases.clear()
         phases.update(mid_phases)
-    # HBM floor of the solve: per fine scalar node and GMRES
-    # iteration j, 2.53 kB for the V-cycle over all levels (sweeps=3), 81 B for
-    # the operator and 72 (j+2) B for orthogonalisation + normalisation
-    floor_b = n * sum(2530 + 81 + 72 * (j % 50 + 2) for j in range(res.iterations))
-    peak, peak_src = peaks()
-    floor_s = floor_b / (peak * 1e9)
+    roof = newton_floor(n, res.iterations, 1, t_dev)
     return {"config": f"configs[3]: {2 ** level}^2 Q2 notch, levels 2..{level}, sweeps=3, "
                       "restart 50, rtol 1e-8",
             "split": args.split, "iterations": res.iterations, "converged": res.converged,
@@ -423,10 +418,7 @@ def newton_step_ours(args, P, torch):
             "warm_runs_total_s": [round(r[1] + r[2], 4) for r in runs],
             "cold_setup_s": round(c_setup, 4), "cold_gmres_s": round(c_gmres, 4),
             "gmres_device_s": round(t_dev, 4),
-            "roofline": {"bound": "hbm", "floor_s": round(floor_s, 4),
-                         "frac": round(floor_s / t_dev, 3), "peak_gbs": peak,
-                         "model": "SURVEY.md 8(d) fused-minimum dataflow: per fine node and "
-                                  "iteration 2.53 kB V-cycle + 81 B operator + 72(j+2) B MGS"},
+            "roofline": roof,
             "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
             "note": ("median of three warm solves (fresh state + preconditioner each) after a "
                      "cold one" if warm
@@ -472,8 +464,23 @@ def newton_step_distributed(args, P, torch, ws, rank, dev):
             "split": args.split, "iterations": res.iterations, "converged": res.converged,
             "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
             "total_s": round(t_setup + t_gmres, 4), "orthogonalisation": "CGS2",
+            "roofline": newton_floor(n, res.iterations, ws, t_gmres),
             "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
             "timing": "max over ranks, wall clock around synchronised regions"}
+
+
+def newton_floor(n, iterations, ngpu, t):
+    """HBM floor of the GMRES+GMG solve (SURVEY.md 8(d) fused-minimum dataflow): per fine
+    scalar node and GMRES iteration j, 2.53 kB for the V-cycle over all levels (sweeps=3),
+    81 B for the operator and 72 (j+2) B for orthogonalisation + normalisation, spread over
+    ngpu GPUs' HBM; frac = floor / t (t: the measured solve time)."""
+    floor_b = n * sum(2530 + 81 + 72 * (j % 50 + 2) for j in range(iterations))
+    peak, _ = peaks()
+    floor_s = floor_b / (ngpu * peak * 1e9)
+    return {"bound": "hbm", "floor_s": round(floor_s, 4), "frac": round(floor_s / t, 3),
+            "peak_gbs": peak, "n_gpus": ngpu,
+            "model": "SURVEY.md 8(d) fused-minimum dataflow: per fine node and iteration 2.53 kB "
+                     "V-cycle + 81 B operator + 72(j+2) B MGS, over n_gpus x peak"}
 
 
 # ------------------------------------------------------------ CPU sides
