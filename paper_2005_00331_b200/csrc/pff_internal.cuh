@@ -98,9 +98,15 @@ struct Level {
     // into this level: [component][cell][local node], 3 x cells x (p+1)^2
     int64_t ev_len() const { return 3 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells(); }
     // weighted tangent cache of the generic application (Miehe levels without
-    // the sweep kernel): [T00 T01 T02 T11 T12 T22 cw0 cw1 cw2 pc][k][cell]
+    // the sweep kernel), in warp groups of gtan_group() cells (the cooperative
+    // kernel's cells per warp): [group][array T00 T01 T02 T11 T12 T22 cw0 cw1 cw2
+    // pc][jq][cell in group][iq] -- a warp's load for one (array, jq) is one
+    // contiguous run over its (cell, iq) lanes
+    int gtan_group() const { return 32 / (mesh.p + 1); }
     int64_t gtan_len() const {
-        return miehe && !sweep_ok() ? 10 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells() : 0;
+        const int64_t cg = gtan_group();
+        const int64_t cells = (local_cells() + cg - 1) / cg * cg;
+        return miehe && !sweep_ok() ? 10 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * cells : 0;
     }
     int64_t qcache_len() const { return generic_len() + tile_len() + gtan_len() + ev_len(); }
     double* qtile() const { return qcache + generic_len(); }

@@ -149,17 +149,22 @@ __global__ void k_refresh_gtan(Mesh m, Win w, Shape S, Material M, const double*
     miehe_dsig(M, g, mq, 0.0, 0.0, 1.0, Mc[0][2], Mc[1][2], Mc[2][2], sp);
     double q11, q22, q12;
     sigplus2(M.lam, M.mu, tre, e, q11, q22, q12);
-    double* o = gt + t;
+    // warp-group layout (Level::gtan_len): [group][array][jq][cell in group][iq]
+    constexpr int CG = 32 / N1;
+    const int64_t cell = t - (int64_t)k * nc, grp = cell / CG;
+    const int cig = (int)(cell - grp * CG);
+    const int64_t ag = (int64_t)QQ * CG;              // array stride within a group
+    double* o = gt + grp * (10 * ag) + (int64_t)(jq * CG + cig) * N1 + iq;
     o[0] = wv * Mc[0][0];
-    o[fs] = wv * 0.5 * (Mc[0][1] + Mc[1][0]);
-    o[2 * fs] = wv * 0.5 * (Mc[0][2] + 2.0 * Mc[2][0]);
-    o[3 * fs] = wv * Mc[1][1];
-    o[4 * fs] = wv * 0.5 * (Mc[1][2] + 2.0 * Mc[2][1]);
-    o[5 * fs] = wv * 2.0 * Mc[2][2];
-    o[6 * fs] = wv * dg * q11;
-    o[7 * fs] = wv * dg * q22;
-    o[8 * fs] = wv * dg * 2.0 * q12;
-    o[9 * fs] = wv * q[5 * fs];
+    o[ag] = wv * 0.5 * (Mc[0][1] + Mc[1][0]);
+    o[2 * ag] = wv * 0.5 * (Mc[0][2] + 2.0 * Mc[2][0]);
+    o[3 * ag] = wv * Mc[1][1];
+    o[4 * ag] = wv * 0.5 * (Mc[1][2] + 2.0 * Mc[2][1]);
+    o[5 * ag] = wv * 2.0 * Mc[2][2];
+    o[6 * ag] = wv * dg * q11;
+    o[7 * ag] = wv * dg * q22;
+    o[8 * ag] = wv * dg * 2.0 * q12;
+    o[9 * ag] = wv * q[5 * fs];
 }
 
 // ----------------------------------------------------- Jacobian (generic)
@@ -323,18 +328,22 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
             const double d11 = yn[1] * inv_h;                 // N_y (D_x u)
             const double d22 = yd[2] * inv_h;                 // D_y (N_x v)
             const double d12 = 0.5 * (yd[0] + yn[3]) * inv_h;
-            const double* g = TC ? gt + (int64_t)(jq * N1 + iq) * nc + cell : nullptr;
+            // warp-group layout: this warp's group is its cell block, lanes (c, iq) contiguous
+            const double* g = TC ? gt + ((int64_t)blockIdx.x * COOP_WARPS + warp) * (10 * QQ * CPW) +
+                                       (int64_t)(jq * CPW + c) * N1 + iq
+                                 : nullptr;
+            constexpr int64_t gs = (int64_t)QQ * CPW;   // array stride
             if (T::NEED_U && TC) {
                 // cached weighted tangent (x wv); the backward passes expect x wg = wv / h
                 if (T::DO_UU) {
-                    const double t00 = g[0], t01 = g[fs], t02 = g[2 * fs];
-                    const double t11 = g[3 * fs], t12 = g[4 * fs], t22 = g[5 * fs];
+                    const double t00 = g[0], t01 = g[gs], t02 = g[2 * gs];
+                    const double t11 = g[3 * gs], t12 = g[4 * gs], t22 = g[5 * gs];
                     s11 = fma(t00, d11, fma(t01, d22, t02 * d12)) * inv_h;
                     s22 = fma(t01, d11, fma(t11, d22, t12 * d12)) * inv_h;
                     s12 = 0.5 * fma(t02, d11, fma(t12, d22, t22 * d12)) * inv_h;
                 }
                 if (T::DO_COUP)
-                    coup = fma(g[6 * fs], d11, fma(g[7 * fs], d22, g[8 * fs] * d12));   // x wv
+                    coup = fma(g[6 * gs], d11, fma(g[7 * gs], d22, g[8 * gs] * d12));   // x wv
             } else if (T::NEED_U) {
                 double ds11, ds22, ds12, spde;
                 dsig<MIEHE>(M.lam, M.mu, q[3 * fs], q[0], q[fs], q[2 * fs], d11, d22, d12, ds11,
@@ -347,7 +356,7 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
             double fv = 0.0, fgx = 0.0, fgy = 0.0;
             if (T::DO_PP) {
                 if (TC) {
-                    fv = g[9 * fs] * yn[4];
+                    fv = g[9 * gs] * yn[4];
                     if (T::DO_COUP) fv += coup;
                 } else {
                     double pval = q[5 * fs] * yn[4];
