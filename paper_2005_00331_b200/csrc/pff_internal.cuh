@@ -102,11 +102,13 @@ struct Level {
     // kernel's cells per warp): [group][array T00 T01 T02 T11 T12 T22 cw0 cw1 cw2
     // pc][jq][cell in group][iq] -- a warp's load for one (array, jq) is one
     // contiguous run over its (cell, iq) lanes
+    // (none: [g w][cw0 cw1 cw2][pc], 5 arrays)
     int gtan_group() const { return 32 / (mesh.p + 1); }
+    int gtan_arrays() const { return miehe ? 10 : 5; }
     int64_t gtan_len() const {
         const int64_t cg = gtan_group();
         const int64_t cells = (local_cells() + cg - 1) / cg * cg;
-        return miehe && !sweep_ok() ? 10 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * cells : 0;
+        return !sweep_ok() ? gtan_arrays() * (int64_t)(mesh.p + 1) * (mesh.p + 1) * cells : 0;
     }
     int64_t qcache_len() const { return generic_len() + tile_len() + gtan_len() + ev_len(); }
     double* qtile() const { return qcache + generic_len(); }

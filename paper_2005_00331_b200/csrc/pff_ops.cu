@@ -125,7 +125,7 @@ k_refresh(Mesh m, Win w, Shape S, Material M, const double* __restrict__ U,
 // cache_tensors quantities (src/_kernels.py:517-548) per (q-point, cell) from
 // the q-point cache, weight w_jq w_iq h^2 folded in; symmetric form
 // (ds11, ds22, 2 ds12) = T (d11, d22, d12) as in the Q2 tiles (pff_sweep.cu)
-template <int P>
+template <int P, bool MIEHE>
 __global__ void k_refresh_gtan(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc,
                                double* __restrict__ gt) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
@@ -138,6 +138,20 @@ __global__ void k_refresh_gtan(Mesh m, Win w, Shape S, Material M, const double*
     const double* q = qc + t;
     const double e11 = q[0], e22 = q[fs], e12 = q[2 * fs], g = q[3 * fs], dg = q[4 * fs];
     const double tre = e11 + e22;
+    // warp-group layout (Level::gtan_len): [group][array][jq][cell in group][iq]
+    constexpr int CG = 32 / N1;
+    const int64_t cell = t - (int64_t)k * nc, grp = cell / CG;
+    const int cig = (int)(cell - grp * CG);
+    const int64_t ag = (int64_t)QQ * CG;              // array stride within a group
+    if (!MIEHE) {   // [g w][cw (sigma(e) x g' w)][pc w], as the Q2 tiles' none form
+        double* o = gt + grp * (5 * ag) + (int64_t)(jq * CG + cig) * N1 + iq;
+        o[0] = wv * g;
+        o[ag] = wv * dg * (M.lam * tre + 2.0 * M.mu * e11);
+        o[2 * ag] = wv * dg * (M.lam * tre + 2.0 * M.mu * e22);
+        o[3 * ag] = wv * dg * 2.0 * (2.0 * M.mu * e12);
+        o[4 * ag] = wv * q[5 * fs];
+        return;
+    }
     const double mm = 0.5 * (e11 + e22), dh = 0.5 * (e11 - e22);
     const double r = sqrt(dh * dh + e12 * e12);
     const Eig e = eig2(e11, e22, e12);
@@ -149,11 +163,6 @@ __global__ void k_refresh_gtan(Mesh m, Win w, Shape S, Material M, const double*
     miehe_dsig(M, g, mq, 0.0, 0.0, 1.0, Mc[0][2], Mc[1][2], Mc[2][2], sp);
     double q11, q22, q12;
     sigplus2(M.lam, M.mu, tre, e, q11, q22, q12);
-    // warp-group layout (Level::gtan_len): [group][array][jq][cell in group][iq]
-    constexpr int CG = 32 / N1;
-    const int64_t cell = t - (int64_t)k * nc, grp = cell / CG;
-    const int cig = (int)(cell - grp * CG);
-    const int64_t ag = (int64_t)QQ * CG;              // array stride within a group
     double* o = gt + grp * (10 * ag) + (int64_t)(jq * CG + cig) * N1 + iq;
     o[0] = wv * Mc[0][0];
     o[ag] = wv * 0.5 * (Mc[0][1] + Mc[1][0]);
@@ -329,21 +338,28 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
             const double d22 = yd[2] * inv_h;                 // D_y (N_x v)
             const double d12 = 0.5 * (yd[0] + yn[3]) * inv_h;
             // warp-group layout: this warp's group is its cell block, lanes (c, iq) contiguous
-            const double* g = TC ? gt + ((int64_t)blockIdx.x * COOP_WARPS + warp) * (10 * QQ * CPW) +
+            constexpr int NARR = MIEHE ? 10 : 5, GCW = MIEHE ? 6 : 1, GPC = GCW + 3;
+            const double* g = TC ? gt + ((int64_t)blockIdx.x * COOP_WARPS + warp) * (NARR * QQ * CPW) +
                                        (int64_t)(jq * CPW + c) * N1 + iq
                                  : nullptr;
             constexpr int64_t gs = (int64_t)QQ * CPW;   // array stride
             if (T::NEED_U && TC) {
                 // cached weighted tangent (x wv); the backward passes expect x wg = wv / h
-                if (T::DO_UU) {
+                if (T::DO_UU && MIEHE) {
                     const double t00 = g[0], t01 = g[gs], t02 = g[2 * gs];
                     const double t11 = g[3 * gs], t12 = g[4 * gs], t22 = g[5 * gs];
                     s11 = fma(t00, d11, fma(t01, d22, t02 * d12)) * inv_h;
                     s22 = fma(t01, d11, fma(t11, d22, t12 * d12)) * inv_h;
                     s12 = 0.5 * fma(t02, d11, fma(t12, d22, t22 * d12)) * inv_h;
+                } else if (T::DO_UU) {   // none: g w (lambda tr de I + 2 mu de)
+                    const double gw = g[0] * inv_h;
+                    const double lt = M.lam * (d11 + d22), mu2 = 2.0 * M.mu;
+                    s11 = gw * fma(mu2, d11, lt);
+                    s22 = gw * fma(mu2, d22, lt);
+                    s12 = (gw * mu2) * d12;
                 }
                 if (T::DO_COUP)
-                    coup = fma(g[6 * gs], d11, fma(g[7 * gs], d22, g[8 * gs] * d12));   // x wv
+                    coup = fma(g[GCW * gs], d11, fma(g[(GCW + 1) * gs], d22, g[(GCW + 2) * gs] * d12));   // x wv
             } else if (T::NEED_U) {
                 double ds11, ds22, ds12, spde;
                 dsig<MIEHE>(M.lam, M.mu, q[3 * fs], q[0], q[fs], q[2 * fs], d11, d22, d12, ds11,
@@ -356,7 +372,7 @@ k_apply_coop(Mesh m, Shape S, Material M, const double* __restrict__ qc,
             double fv = 0.0, fgx = 0.0, fgy = 0.0;
             if (T::DO_PP) {
                 if (TC) {
-                    fv = g[9 * gs] * yn[4];
+                    fv = g[GPC * gs] * yn[4];
                     if (T::DO_COUP) fv += coup;
                 } else {
                     double pval = q[5 * fs] * yn[4];
@@ -638,7 +654,7 @@ struct RefreshL {
         count_launches(1);
         if (L->gtan_len() > 0) {
             const int64_t nq = (int64_t)(P + 1) * (P + 1) * w.ncell;
-            k_refresh_gtan<P><<<grid_for(nq, 256), 256, 0, s>>>(m, w, L->shape, L->mat, L->qcache,
+            k_refresh_gtan<P, MIEHE><<<grid_for(nq, 256), 256, 0, s>>>(m, w, L->shape, L->mat, L->qcache,
                                                                L->gtan());
             count_launches(1);
         }
@@ -660,7 +676,7 @@ struct ApplyL {
         const double* q = L->qcache;
         const uint8_t* f = L->flags;
         double* ev = L->ev();
-        const bool tc = MIEHE && L->gtan_len() > 0;
+        const bool tc = L->gtan_len() > 0;
         const double* gt = tc ? L->gtan() : nullptr;
         switch (mode) {
             case MODE_FULL:
