@@ -172,16 +172,20 @@ __device__ __forceinline__ void node_cells_p(const Mesh& m, int64_t g, int row_l
         j = imid;
         if (cy_lo < (ns >> 1)) cy_lo = ns >> 1;
     }
+    // at most two cell rows and columns, visited in increasing cell index (the
+    // same cells and order as node_cells), unrolled
     const int cy0 = j > 0 ? (j - 1) / P : 0, cy1 = j / P;
     const int cx0 = i > 0 ? (i - 1) / P : 0, cx1 = i / P;
-    for (int cy = cy0; cy <= cy1; ++cy) {
-        if (cy < cy_lo || cy >= cy_hi) continue;
+#pragma unroll
+    for (int ry = 0; ry < 2; ++ry) {
+        const int cy = ry ? cy1 : cy0;
+        if ((ry && cy1 == cy0) || cy < cy_lo || cy >= cy_hi) continue;
         const int b = j - cy * P;
-        if (b < 0 || b > P) continue;
-        for (int cx = cx0; cx <= cx1 && cx < ns; ++cx) {
-            const int a = i - cx * P;
-            if (a < 0 || a > P) continue;
-            f(cx, cy, a, b);
+#pragma unroll
+        for (int rx = 0; rx < 2; ++rx) {
+            const int cx = rx ? cx1 : cx0;
+            if ((rx && cx1 == cx0) || cx >= ns) continue;
+            f(cx, cy, i - cx * P, b);
         }
     }
 }
