@@ -69,16 +69,18 @@ k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
         wy[m] = Es[chy][b][m];
     }
     double acc[3] = {0.0, 0.0, 0.0};
+    // branch-free: a dropped weight (|w| <= 1e-14, multigrid.py:81-83) is an exact
+    // zero, and fma(0, x, acc) == acc for finite x -- the same sums without the
+    // per-lane divergent filter (neighbouring fine nodes have different patterns)
 #pragma unroll
     for (int my = 0; my < N1; ++my)
 #pragma unroll
         for (int mx = 0; mx < N1; ++mx) {
-            const double w = wy[my] * wx[mx];
-            if (fabs(w) > 1e-14) {
-                const int64_t c = mc.node(ccx, ccy, mx, my);
+            const double w0 = wy[my] * wx[mx];
+            const double w = fabs(w0) > 1e-14 ? w0 : 0.0;
+            const int64_t c = mc.node(ccx, ccy, mx, my);
 #pragma unroll
-                for (int k = 0; k < 3; ++k) acc[k] = fma(w, xc[k * mc.n + c], acc[k]);
-            }
+            for (int k = 0; k < 3; ++k) acc[k] = fma(w, xc[k * mc.n + c], acc[k]);
         }
     if (add_masked) {
         // z += where(cons, 0, P zc)  (src/multigrid.py:340-342)
