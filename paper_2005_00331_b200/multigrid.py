@@ -41,6 +41,7 @@ FUSE_INIT = os.environ.get("PFF_FUSE_INIT", "1") != "0"
 # the FULL residual emitting the u block's d0 measured slower (+4.5 ms per Newton
 # solve at 1024^2) than the separate pff_cheb_init pass it replaces: off
 EMIT_FULL = os.environ.get("PFF_EMIT_FULL", "0") != "0"
+EMIT_PHIROW = os.environ.get("PFF_EMIT_PHIROW", "1") != "0"
 DENSE_COARSE = os.environ.get("PFF_DENSE_COARSE", "1") != "0"
 COARSE_DENSE_NMAX = 256
 NATIVE_LANCZOS = True   # setup's batched Lanczos driven by pff_lanczos_ranges (C++)
@@ -798,10 +799,13 @@ class GmgPreconditioner:
                 s.apply_into(_lib.MODE_FULL, z, W.res, r)
             self._cheb(l, _lib.MODE_UU, W.res[:2 * n], c * hu, C * hu, self.cheb.sweeps, z[:2 * n],
                        False, pre_d=first or EMIT_FULL)
-            call("pff_apply_emit", h, _lib.MODE_PHIROW, ptr(z), ptr(W.resphi), ptr(r[2 * n:]),
-                 ptr(inv_p), ptr(W.d), th_p, st)
+            if EMIT_PHIROW:
+                call("pff_apply_emit", h, _lib.MODE_PHIROW, ptr(z), ptr(W.resphi), ptr(r[2 * n:]),
+                     ptr(inv_p), ptr(W.d), th_p, st)
+            else:
+                s.apply_into(_lib.MODE_PHIROW, z, W.resphi, r[2 * n:])
             self._cheb(l, _lib.MODE_PHIPHI, W.resphi, c * hp, C * hp, self.cheb.sweeps, z[2 * n:],
-                       False, pre_d=True)
+                       False, pre_d=EMIT_PHIROW)
             return
         if first:
             # z = SELECT(r): r - G z is r with the constrained rows zeroed, exactly
