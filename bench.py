@@ -341,10 +341,12 @@ def release_device_memory(torch):
 
 def newton_step_ours(args, P, torch):
     """configs[3]: one Newton step's GMRES+GMG solve on 1024^2 Q2.  A fresh
-    state and preconditioner each time: the first solve (cold: module loads,
-    graph capture first use) is reported as cold_*, then three warm solves,
-    of which the median (setup + GMRES) is the steady-state figure a
-    simulation sees every step."""
+    linearisation state (from host arrays) every time; the first solve (cold:
+    module loads, first graph capture, allocations) is reported as cold_*, then
+    three warm solves re-using the preconditioner object -- GmgPreconditioner.setup
+    on the new state, as the reference's ActiveSetSolver does every Newton step
+    (src/active_set_solver.py:129-145) -- of which the median (setup + GMRES) is
+    the steady-state figure a simulation sees every step."""
     level = args.newton_level
     h, params, U, pt, act, dirn, x = baseline_inputs(2, level, args.split, seed=0, notch=True)
     rhs = x.copy()
@@ -355,6 +357,7 @@ def newton_step_ours(args, P, torch):
     sol_h = torch.empty(rhs_h.numel(), dtype=torch.float64, pin_memory=True)
 
     phases = {}
+    keep = {}
 
     def one():
         st = P.LinearizationState(h, level, params, split=args.split)
@@ -368,7 +371,10 @@ def newton_step_ours(args, P, torch):
         st.refresh_cache()
         torch.cuda.synchronize()
         ta = time.perf_counter()
-        gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+        gmg = keep.get("gmg")
+        if gmg is None:
+            gmg = keep["gmg"] = P.GmgPreconditioner(h, coarse_level=2,
+                                                    cheb=P.ChebyshevConfig(sweeps=3))
         gmg.setup(st)
         torch.cuda.synchronize()
         tb = time.perf_counter()
@@ -404,7 +410,7 @@ def newton_step_ours(args, P, torch):
         # shared boxes is large; each run's numbers are kept below)
         for _ in range(3):
             runs.append(one() + (dict(phases),))
-            release_device_memory(torch)
+        release_device_memory(torch)
         runs.sort(key=lambda r: r[1] + r[2])
         res, t_setup, t_gmres, t_dev, mid_phases = runs[len(runs) // 2]
         phases.clear()
@@ -420,8 +426,8 @@ def newton_step_ours(args, P, torch):
             "gmres_device_s": round(t_dev, 4),
             "roofline": roof,
             "final_rel_residual": res.residual_history[-1] / res.residual_history[0],
-            "note": ("median of three warm solves (fresh state + preconditioner each) after a "
-                     "cold one" if warm
+            "note": ("median of three warm solves (fresh state each, the preconditioner "
+                     "object re-setup as ActiveSetSolver does) after a cold one" if warm
                      else "single (cold) solve: two hierarchies would not fit next to each other")
                     + "; gmres_s includes the rhs H2D and solution D2H"}
 
