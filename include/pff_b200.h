@@ -267,6 +267,11 @@ int pff_apply_emit(const pff_level* L, int mode, const double* src, double* dst,
 int pff_smooth_init(const pff_level* L, const double* r, double* z, double* res_u,
                     const double* invd_u, double* d_u, double theta, void* stream);
 
+/* y = M x for a row-major dense device matrix M (rows x cols); x != y.  The
+ * V-cycle below a small level as one precomputed linear map. */
+int pff_dense_matvec(int64_t rows, int64_t cols, const double* M, const double* x, double* y,
+                     void* stream);
+
 /* Coarse-level solve of the V-cycle (replaces the coarse Chebyshev passes of
  * src/multigrid.py:311-328 on a coarse level of n <= 256 scalar nodes):
  * z_u = Cu r_u, t = r_phi - Gpu z_u, z_phi = Cp t, then z = r on the rows

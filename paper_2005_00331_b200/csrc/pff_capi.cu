@@ -407,6 +407,13 @@ int pff_combine(int64_t n, int k, const double* V, int64_t ldv, const double* y,
     return check(pff::launch_combine(n, k, V, ldv, y, out, accumulate, S(stream)), "pff_combine");
 }
 
+int pff_dense_matvec(int64_t rows, int64_t cols, const double* M, const double* x, double* y,
+                     void* stream) {
+    if (rows < 1 || cols < 1 || rows > (1 << 24) || cols > (1 << 24) || !M || !x || !y || x == y)
+        return fail(PFF_E_ARG, "%s", "pff_dense_matvec: bad argument");
+    return check(pff::launch_dense_matvec((int)rows, (int)cols, M, x, y, S(stream)), "pff_dense_matvec");
+}
+
 int pff_coarse_dense(int64_t n, const double* Cu, const double* Gpu, const double* Cp,
                      const uint8_t* cmask, const double* r, double* z, void* stream) {
     if (n < 1 || n > pff::coarse_dense_nmax() || !Cu || !Gpu || !Cp || !cmask || !r || !z)

@@ -57,9 +57,32 @@ k_coarse_dense(int n, const double* __restrict__ Cu, const double* __restrict__ 
     }
 }
 
+// y = M x, M row-major (rows x cols), one warp per row, lane-strided columns
+// and a fixed shuffle tree (deterministic); M stays L2-resident across calls
+__global__ void __launch_bounds__(256)
+k_dense_matvec(int rows, int cols, const double* __restrict__ M, const double* __restrict__ x,
+               double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const double* mr = M + (int64_t)row * cols;
+    double acc = 0.0;
+    for (int j = lane; j < cols; j += 32) acc = fma(mr[j], x[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) y[row] = acc;
+}
+
 }  // namespace
 
 int coarse_dense_nmax() { return CD_NMAX; }
+
+cudaError_t launch_dense_matvec(int rows, int cols, const double* M, const double* x, double* y,
+                                cudaStream_t s) {
+    if (rows < 1 || cols < 1) return cudaErrorInvalidValue;
+    k_dense_matvec<<<(rows + 7) / 8, 256, 0, s>>>(rows, cols, M, x, y);
+    count_launches(1);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_coarse_dense(int n, const double* Cu, const double* Gpu, const double* Cp,
                                 const uint8_t* cmask, const double* r, double* z,

@@ -238,6 +238,9 @@ cudaError_t launch_coarse_dense(int n, const double* Cu, const double* Gpu, cons
                                 const uint8_t* cmask, const double* r, double* z,
                                 cudaStream_t s);
 
+cudaError_t launch_dense_matvec(int rows, int cols, const double* M, const double* x, double* y,
+                                cudaStream_t s);
+
 // dense per-cell matrices (pff_assemble.cu)
 cudaError_t launch_cell_matrices(const Level& L, double* gk, cudaStream_t s);
 

@@ -44,6 +44,11 @@ EMIT_FULL = os.environ.get("PFF_EMIT_FULL", "0") != "0"
 EMIT_PHIROW = os.environ.get("PFF_EMIT_PHIROW", "1") != "0"
 DENSE_COARSE = os.environ.get("PFF_DENSE_COARSE", "1") != "0"
 COARSE_DENSE_NMAX = 256
+# the whole V-cycle from the level above the coarse one as one dense map
+# (pff_dense_matvec) when that level has at most DENSE_LEVEL_NMAX scalar nodes
+# (Q2 level 3: 297)
+DENSE_LEVEL = os.environ.get("PFF_DENSE_LEVEL", "1") != "0"
+DENSE_LEVEL_NMAX = 400
 NATIVE_LANCZOS = True   # setup's batched Lanczos driven by pff_lanczos_ranges (C++)
 _EAGER_DONE: set = set()
 
@@ -484,6 +489,7 @@ class GmgPreconditioner:
         self._inv: dict[int, tuple] = {}
         self._work: dict[int, _LevelWork] = {}
         self._dense = None
+        self._dense_l = None
         self._graph = None
         self._scratch = None
 
@@ -523,6 +529,7 @@ class GmgPreconditioner:
         if todo:
             self.ranges.update(self._estimate_ranges_batched(todo))
         self._build_dense_coarse()
+        self._build_dense_level()
         self._graph = None
         if logger.isEnabledFor(logging.DEBUG):
             logger.debug("gmg setup: levels %d..%d, ranges %s", self.coarse_level, state.level,
@@ -569,6 +576,78 @@ class GmgPreconditioner:
         Gpu = G[2 * n:, :2 * n].contiguous()
         cmask = torch.from_numpy(s.constrained_mask().astype(np.uint8)).to(G.device)
         self._dense = (n, Cu, Gpu, Cp, cmask)
+
+    def _build_dense_level(self):
+        """The V-cycle from level L = coarse_level + 1 down (src/multigrid.py:330-344:
+        pre-smoothing, residual, restriction with zeroed constrained rows, the coarse
+        solve, masked prolongation, post-smoothing) is linear in r for a fixed setup:
+        compose its dense map M_L once from the masked Jacobian, the Chebyshev
+        polynomials of both blocks, the transfer matrix and the dense coarse maps,
+        then every V-cycle applies z = M_L r in one launch."""
+        self._dense_l = None
+        L = self.coarse_level + 1
+        if (not DENSE_LEVEL or self._dense is None or self.finest is None or self.finest < L
+                or L not in self.states):
+            return
+        s = self.states[L]
+        n = s.n_scalar
+        if n > DENSE_LEVEL_NMAX:
+            return
+        dev = self._dense[1].device
+        G = op.assemble_oracle(s).device.to_dense()
+        inv_u, inv_p = self._inv[L]
+        cfg = self.cheb
+
+        def poly(A, invd, a, b, sweeps):
+            nb = A.shape[0]
+            theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+            sigma1 = theta / delta
+            eye = torch.eye(nb, dtype=torch.float64, device=dev)
+            d = invd[:, None] * eye / theta
+            acc = d.clone()
+            cr = eye
+            rho_old = 1.0 / sigma1
+            for _ in range(1, sweeps):
+                rho = 1.0 / (2.0 * sigma1 - rho_old)
+                cr = cr - A @ d
+                d = (rho * rho_old) * d + (2.0 * rho / delta) * (invd[:, None] * cr)
+                acc = acc + d
+                rho_old = rho
+            return acc
+
+        hu = self.ranges[L]["uu"][1]
+        hp = self.ranges[L]["phiphi"][1]
+        Cu = poly(G[:2 * n, :2 * n], inv_u, cfg.c * hu, cfg.C * hu, cfg.sweeps)
+        Cp = poly(G[2 * n:, 2 * n:], inv_p, cfg.c * hp, cfg.C * hp, cfg.sweeps)
+        cons = torch.from_numpy(s.constrained_mask()).to(dev)
+
+        def smooth(R, Z):   # _smooth: u block on r - G z, then the phi row with the new z_u
+            Z = Z.clone()
+            Z[:2 * n] += Cu @ (R[:2 * n] - G[:2 * n] @ Z)
+            Z[2 * n:] += Cp @ (R[2 * n:] - G[2 * n:] @ Z)
+            return Z
+
+        # the coarse level: transfer (scalar P per component) and the dense solve
+        nc, Cu2, Gpu2, Cp2, cmask2 = self._dense
+        P1 = torch.from_numpy(self.transfers[L].P.toarray()).to(dev)      # (n, nc)
+        cons2 = cmask2.bool()
+
+        def coarse(Rc):
+            Zc = torch.empty_like(Rc)
+            Zc[:2 * nc] = Cu2 @ Rc[:2 * nc]
+            Zc[2 * nc:] = Cp2 @ (Rc[2 * nc:] - Gpu2 @ Zc[:2 * nc])
+            Zc[cons2] = Rc[cons2]
+            return Zc
+
+        R = torch.eye(3 * n, dtype=torch.float64, device=dev)
+        Z = smooth(R, cons[:, None] * R)                     # z = select(r), first smoothing
+        res = R - G @ Z
+        Rc = torch.cat([P1.T @ res[k * n:(k + 1) * n] for k in range(3)])
+        Rc[cons2] = 0.0                                      # restriction zeroes constrained rows
+        Zc = coarse(Rc)
+        Z = Z + (~cons)[:, None] * torch.cat([P1 @ Zc[k * nc:(k + 1) * nc] for k in range(3)])
+        Z = smooth(R, Z)
+        self._dense_l = (L, 3 * n, Z.contiguous())
 
     def _estimate_ranges(self, level: int):
         s = self.states[level]
@@ -861,6 +940,10 @@ class GmgPreconditioner:
              stream_handle())
 
     def _vcycle(self, l, r, z):
+        if self._dense_l is not None and l == self._dense_l[0]:
+            _, nn, M = self._dense_l
+            call("pff_dense_matvec", nn, nn, ptr(M), ptr(r), ptr(z), stream_handle())
+            return
         if l == self.coarse_level:
             if self._dense is not None:
                 n, Cu, Gpu, Cp, cmask = self._dense
