@@ -123,3 +123,58 @@ def test_no_cpu_fallback_without_gpu():
     st = P.LinearizationState(h, 2, P.MaterialParams())
     with pytest.raises(RuntimeError, match="CUDA"):
         st.refresh_cache()
+
+
+def test_host_argument_checks_of_session2_entries():
+    """The new entry points reject bad arguments on the host (no launch)."""
+    L = _lib.load()
+    nul = ctypes.c_void_p(0)
+    # pff_dense_matvec: rows/cols >= 1, non-null, x != y
+    assert L.pff_dense_matvec(0, 4, nul, nul, nul, nul) != 0
+    buf = ctypes.c_void_p(0x1000)
+    assert L.pff_dense_matvec(4, 4, buf, buf, buf, nul) != 0          # x == y
+    # pff_coarse_dense: n in 1..256
+    assert L.pff_coarse_dense(0, buf, buf, buf, buf, buf, buf, nul) != 0
+    assert L.pff_coarse_dense(257, buf, buf, buf, buf, buf, buf, nul) != 0
+    # pff_apply_cheb_ex / pff_apply_emit / pff_smooth_init on an unbound level
+    s = P.shape_data(2)
+    h = ctypes.c_void_p()
+    mat = _lib.material(P.MaterialParams())
+    E = s.embedding()
+    assert L.pff_level_create(ctypes.byref(h), 2, 6, 1, ctypes.byref(mat), s.values.ctypes.data,
+                              s.derivatives.ctypes.data, s.quad_weights.ctypes.data,
+                              E.ctypes.data) == 0
+    try:
+        assert L.pff_apply_cheb_ex(h, 1, buf, buf, buf, buf, buf, buf, ctypes.c_double(1.0),
+                                   ctypes.c_double(1.0), 0, nul) != 0
+        assert L.pff_apply_emit(h, 0, buf, buf, buf, buf, buf, ctypes.c_double(1.0), nul) != 0
+        assert L.pff_smooth_init(h, buf, buf, buf, buf, buf, ctypes.c_double(1.0), nul) != 0
+    finally:
+        L.pff_level_destroy(h)
+    assert b"bad argument" in L.pff_last_error() or b"not bound" in L.pff_last_error()
+
+
+@pytest.mark.parametrize("ns", [64, 100, 1024, 4096])
+def test_pipeline_chunks_partition_the_rows(ns):
+    """The e2e pipeline's ramped chunks cover the cell rows exactly, in order,
+    with small first and last chunks."""
+    from paper_2005_00331_b200 import operator as OP
+    cuts = OP._pipe_cuts(ns)
+    assert cuts[0] == 0 and cuts[-1] == ns
+    assert all(b > a for a, b in zip(cuts, cuts[1:]))
+    sizes = [b - a for a, b in zip(cuts, cuts[1:])]
+    assert sizes[0] <= max(sizes) // 2 and sizes[-1] <= max(sizes) // 2
+
+
+def test_newton_floor_model():
+    """bench.py's HBM-floor model of the Newton solve scales with
+    the node count and the GPU count."""
+    import bench
+    n = 67_129_345                    # configs[4] scalar nodes
+    a = bench.newton_floor(n, 28, 1, 1.0)
+    b = bench.newton_floor(n, 28, 4, 1.0)
+    assert abs(a["floor_s"] / b["floor_s"] - 4.0) < 0.01
+    per_node = sum(2530 + 81 + 72 * (j + 2) for j in range(28))
+    peak, _ = bench.peaks()
+    assert abs(a["floor_s"] - n * per_node / (peak * 1e9)) < 1e-4
+    assert abs(a["frac"] - a["floor_s"]) < 1e-3   # t = 1 s
