@@ -512,7 +512,7 @@ def newton_floor(n, iterations, ngpu, t):
 def cpu_baseline(args, budget_s=15.0):
     """The C oracle port on this host's cores, bounded sample of configs[1]."""
     from oracle import oracle as O
-    nt = O.max_threads()
+    nt = host_threads()
     st, x = O.baseline_state(2, 10, args.split, seed=0)
     st.refresh_cache(nthreads=nt)
     O.apply_jacobian(st, x, nthreads=nt)   # warm
@@ -529,12 +529,21 @@ def cpu_baseline(args, budget_s=15.0):
                       f"({args.split}), best of {len(times)} in a {budget_s:.0f} s budget"}
 
 
+def host_threads() -> int:
+    """Every host core this process may run on (torchrun sets OMP_NUM_THREADS=1,
+    which omp_get_max_threads would report)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:   # pragma: no cover - non-Linux
+        return max(1, os.cpu_count() or 1)
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
-    nt = O.max_threads()
+    nt = host_threads()
     st, x = O.baseline_state(2, 10, args.split, seed=0)
     st.refresh_cache(nthreads=nt)
     dofs = 3 * st.n
