@@ -28,6 +28,10 @@ struct Win {
     }
 };
 
+// smallest mesh (cells per side) on the Q2 sweep kernel (PFF_SWEEP_MIN_NSIDE);
+// below it the generic cooperative kernel runs (pff_sweep.cu)
+int sweep_min_nside();
+
 // Per-level handle contents (the C-ABI's opaque pff_level).
 struct Level {
     Mesh mesh;
@@ -88,7 +92,8 @@ struct Level {
     // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
     bool sweep_ok() const {   // the sweep kernel stages with 32-bit node indices
-        return mesh.p == 2 && mesh.nside >= 64 && q2_struct && mesh.n < (int64_t(1) << 31);
+        return mesh.p == 2 && mesh.nside >= sweep_min_nside() && q2_struct &&
+               mesh.n < (int64_t(1) << 31);
     }
     int n_strips() const { return (mesh.nside + 30) / 31; }
     int tile_nq() const { return miehe ? 10 : 5; }   // tangent (6 | 1) + coupling (3) + pc

@@ -705,16 +705,6 @@ int sweep_min_rows() {
     return v;
 }
 
-// smallest mesh (cells per side) routed to the sweep kernel; below it the
-// generic cooperative kernel is faster (latency-bound levels)
-int sweep_min_nside() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PFF_SWEEP_MIN_NSIDE");
-        v = e ? atoi(e) : 64;
-    }
-    return v;
-}
 
 struct LaunchCfg {
     bool init = false;
@@ -797,6 +787,18 @@ int g_rows_override = 0;
 
 void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
 
+int sweep_min_nside() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PFF_SWEEP_MIN_NSIDE");
+        // measured: 16 / 32 cut the Newton solve's launch count by 8-16 % but add
+        // 0.4-0.9 ms of device time; the bench's GMRES time is not better -> 64
+        v = e ? atoi(e) : 64;
+        if (v < 4) v = 4;
+    }
+    return v;
+}
+
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {
     const Mesh& m = L.mesh;
     const int64_t total = (int64_t)L.n_strips() * L.q_rows() * SW_LANES;
@@ -824,7 +826,6 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
                                     bool* handled, const ChebArgs* cheb) {
     *handled = false;
     if (!L.sweep_ok()) return cudaSuccess;
-    if (!L.windowed() && cy_begin < 0 && L.mesh.nside < sweep_min_nside()) return cudaSuccess;
     const Mesh& m = L.mesh;
     const int64_t n = L.local_n();
     const int64_t sh = L.row_shift();   // global node j*np1+i lives at local index - sh
