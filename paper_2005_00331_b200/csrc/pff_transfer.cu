@@ -62,6 +62,15 @@ k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
     const int a = (int)(i - (int64_t)P * fx), b = (int)(j - (int64_t)P * fy);
     const int ccx = fx >> 1, ccy = fy >> 1, chx = fx & 1, chy = fy & 1;
     const int64_t g = wf.loc(mf, gg);     // local index of the fine node
+    // the add form's flag and z loads first: their latency overlaps the gathers
+    uint8_t f = 0;
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (add_masked) {
+        f = flags_f[g];
+        z0 = yf[g];
+        z1 = yf[wf.n + g];
+        z2 = yf[2 * wf.n + g];
+    }
     double wx[N1], wy[N1];
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
@@ -84,12 +93,11 @@ k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
         }
     if (add_masked) {
         // z += where(cons, 0, P zc)  (src/multigrid.py:340-342)
-        const uint8_t f = flags_f[g];
         if (!(f & F_DIR)) {
-            yf[g] += acc[0];
-            yf[wf.n + g] += acc[1];
+            yf[g] = z0 + acc[0];
+            yf[wf.n + g] = z1 + acc[1];
         }
-        if (!(f & F_ACT)) yf[2 * wf.n + g] += acc[2];
+        if (!(f & F_ACT)) yf[2 * wf.n + g] = z2 + acc[2];
     } else {
 #pragma unroll
         for (int k = 0; k < 3; ++k) yf[k * wf.n + g] = acc[k];

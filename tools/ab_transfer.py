@@ -55,7 +55,9 @@ for l in range(10, 2, -1):
         lib.pff_restrict(hf, hc, yf.data_ptr(), r0.data_ptr(), 1, s)
         tp = timed(lambda: lib.pff_prolongate(hf, hc, xc.data_ptr(), p0.data_ptr(), 0, s))
         tr = timed(lambda: lib.pff_restrict(hf, hc, yf.data_ptr(), r0.data_ptr(), 1, s))
-        out[name] = (p0, p1, r0, tp, tr)
+        tpa = timed(lambda: lib.pff_prolongate(hf, hc, xc.data_ptr(), p1.data_ptr(), 1, s))
+        out[name] = (p0, p1, r0, tp, tr, tpa)
     same = [torch.equal(a, b) for a, b in zip(out["new"][:3], out["old"][:3])]
-    print(f"level {l}: prolong {out['old'][3]:.1f} -> {out['new'][3]:.1f} us, "
+    print(f"level {l}: prolong-add {out['old'][5]:.1f} -> {out['new'][5]:.1f} us, "
+          f"prolong {out['old'][3]:.1f} -> {out['new'][3]:.1f} us, "
           f"restrict {out['old'][4]:.1f} -> {out['new'][4]:.1f} us, bitwise {same}", flush=True)
