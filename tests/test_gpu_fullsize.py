@@ -1,0 +1,94 @@
+"""Full-size (BASELINE.json configs) checks on the GPU: the diagonal and the
+residual at configs[1] against the C oracle, size-independent properties of the
+V-cycle, and the configs[3] Newton-step solve against the reference's
+iteration counts (28 Miehe, 19 none)."""
+
+import numpy as np
+import pytest
+import torch
+
+import bench
+from conftest import block_rel
+import paper_2005_00331_b200 as P
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _device_state(ost, p, level, split):
+    h = P.build_hierarchy(level, p)
+    st = P.LinearizationState(h, level, ost.params, split=split)
+    st.set_solution(ost.U)
+    st.set_phi_tilde(ost.phi_tilde)
+    st.set_phi_old(ost.phi_old)
+    st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    return st
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_diagonals_and_residual_full_size(split):
+    """configs[1] (1024^2 Q2): both block diagonals and the residual
+    (src/pff_operator.py:218-241, 305-327) against the C oracle per block."""
+    ost, _ = O.baseline_state(2, 10, split, seed=0)
+    nt = O.max_threads()
+    ost.refresh_cache(nthreads=nt)
+    st = _device_state(ost, 2, 10, split)
+    n = st.n_scalar
+    for block in ("uu", "phiphi"):
+        want = O.block_diagonal(ost, block, nthreads=nt)
+        got = P.block_diagonal(st, block)
+        got = got.cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got)
+        assert max(block_rel(got, want, n)) <= TOL, block
+    want = O.residual(ost, nthreads=nt)
+    got = P.residual(st)
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got)
+    assert max(block_rel(got, want, n)) <= TOL
+
+
+def test_vcycle_linearity_full_size():
+    """configs[3] hierarchy (1024^2 Q2, 9 levels): the V-cycle is a fixed linear
+    operator -- M(a x + b y) = a M x + b M y to rounding -- and repeatable bit for
+    bit (graph replay)."""
+    h, params, U, pt, act, dirn, x = bench.baseline_inputs(2, 10, "miehe", seed=0, notch=True)
+    st = P.LinearizationState(h, 10, params, split="miehe")
+    st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    st.refresh_cache()
+    gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xd = torch.rand(x.size, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    yd = torch.rand(x.size, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    mx, my = gmg.apply(xd), gmg.apply(yd)
+    mxy = gmg.apply(2.0 * xd - 3.0 * yd)
+    ref = 2.0 * mx - 3.0 * my
+    assert float((mxy - ref).norm() / ref.norm()) <= 1e-12
+    assert torch.equal(gmg.apply(xd), mx)
+
+
+@pytest.mark.parametrize("split,its", [("miehe", 28), ("none", 19)])
+def test_newton_step_configs3_iterations(split, its):
+    """configs[3]: one Newton step, GMRES(50) + GMG(sweeps=3) to 1e-8 -- the
+    reference needs 28 (Miehe) / 19 (none) iterations on these inputs; the
+    north star allows +-1."""
+    h, params, U, pt, act, dirn, x = bench.baseline_inputs(2, 10, split, seed=0, notch=True)
+    st = P.LinearizationState(h, 10, params, split=split)
+    st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    st.refresh_cache()
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    res = P.gmres_solve(P.JacobianOperator(st), torch.from_numpy(rhs).cuda(),
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    assert res.converged
+    assert abs(res.iterations - its) <= 1
+    assert res.residual_history[-1] <= 1e-8 * res.residual_history[0]
+    # the true residual of the returned solution
+    r = torch.from_numpy(rhs).cuda() - P.apply_jacobian(st, res.solution)
+    assert float(r.norm()) <= 1.01e-8 * float(np.linalg.norm(rhs))
