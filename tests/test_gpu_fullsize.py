@@ -92,3 +92,23 @@ def test_newton_step_configs3_iterations(split, its):
     # the true residual of the returned solution
     r = torch.from_numpy(rhs).cuda() - P.apply_jacobian(st, res.solution)
     assert float(r.norm()) <= 1.01e-8 * float(np.linalg.norm(rhs))
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
+@pytest.mark.parametrize("p,level", [(2, 10), (4, 9)])
+def test_block_modes_full_size(split, p, level):
+    """configs[1] / configs[2]: the smoother's block applications
+    (src/pff_operator.py:273-302) against the C oracle per block."""
+    ost, x = O.baseline_state(p, level, split, seed=1)
+    nt = O.max_threads()
+    ost.refresh_cache(nthreads=nt)
+    st = _device_state(ost, p, level, split)
+    n = st.n_scalar
+    cases = ((O.apply_block_uu, P.apply_block_uu, x[:2 * n]),
+             (O.apply_block_phiphi, P.apply_block_phiphi, x[2 * n:]),
+             (O.apply_phi_row, P.apply_phi_row, x))
+    for ofn, pfn, v in cases:
+        want = ofn(ost, v, nthreads=nt)
+        got = pfn(st, v)
+        got = got.cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got)
+        assert max(block_rel(got, want, n)) <= TOL, ofn.__name__
