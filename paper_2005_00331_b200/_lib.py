@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpff_b200.so")
+# PFF_LIB: an alternative build of the same ABI (A/B experiments, tools/)
+LIB_PATH = os.environ.get("PFF_LIB") or os.path.join(_HERE, "libpff_b200.so")
 
 _c_dp = ctypes.c_void_p   # device pointers are passed as raw addresses
 _i, _d, _i64 = ctypes.c_int, ctypes.c_double, ctypes.c_int64
