@@ -178,3 +178,11 @@ def test_newton_floor_model():
     peak, _ = bench.peaks()
     assert abs(a["floor_s"] - n * per_node / (peak * 1e9)) < 1e-4
     assert abs(a["frac"] - a["floor_s"]) < 1e-3   # t = 1 s
+
+
+def test_integration_doc_names_every_entry_point():
+    """INTEGRATION.md maps every exported entry point to the reference
+    interface it replaces (or says it has none)."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    missing = [s for s in header_symbols() if s not in doc]
+    assert not missing, missing
