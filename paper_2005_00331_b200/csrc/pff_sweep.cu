@@ -72,12 +72,10 @@ struct Use {
     static constexpr int NF = slot(NFIELDS);
 };
 
-template <int NF, int NQ, int NRHS>
+// (the fused forms keep rhs / D^-1 / acc in registers: nothing else is staged)
+template <int NF, int NQ>
 struct __align__(16) WarpSmem {
     double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
-    // fused form: rhs of this lane's output nodes [0, NC); with a fused
-    // Chebyshev step also D^-1 [NC, 2 NC) and acc [2 NC, 3 NC)
-    double rb[NRHS > 0 ? 6 : 1][NRHS > 0 ? NRHS : 1][NRHS > 0 ? SW_LANES : 1];
     alignas(16) double v[RING][NF][RW];      // node-row ring (TMA destinations: 16-B aligned)
     alignas(16) uint8_t f[RING][FW];         // flag rows
     int voff[RING][NF];                      // element offset of staged column 0
@@ -260,7 +258,7 @@ k_sweep_q2(const SweepArgs A) {
     // the fused forms prefetch rhs (and D^-1, acc) of the lane's output nodes
     // into registers at the top of the row step: no staging buffer in shared
     // memory, so they run at the plain kernel's CTAs per SM
-    using Smem = WarpSmem<NF, NQ, 0>;
+    using Smem = WarpSmem<NF, NQ>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -715,7 +713,7 @@ template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false
 cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
     // must match k_sweep_q2's Smem (the fused forms keep rhs / D^-1 / acc in registers)
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, 0>);
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ>);
     auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB, EMIT>;
     static LaunchCfg cfg;
     static int n_sm = 0;
