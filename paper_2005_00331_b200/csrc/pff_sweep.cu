@@ -78,8 +78,6 @@ struct __align__(16) WarpSmem {
     double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
     alignas(16) double v[RING][NF][RW];      // node-row ring (TMA destinations: 16-B aligned)
     alignas(16) uint8_t f[RING][FW];         // flag rows
-    int voff[RING][NF];                      // element offset of staged column 0
-    int foff[RING];
     unsigned long long bar[2];
 };
 
@@ -309,13 +307,11 @@ k_sweep_q2(const SweepArgs A) {
                 const int ae = lo - ((lo + fmis[f]) & 1);
                 const int be = hi + ((hi + fmis[f]) & 1);
                 bulk_g2s(W.v[slot][U::slot(f)], A.fld[f] + ae, (unsigned)(8 * (be - ae)), bar);
-                W.voff[slot][U::slot(f)] = rowb + gc0 - ae;
                 bytes += (unsigned)(8 * (be - ae));
             }
             const int ab = lo - ((lo + flmis) & 15);
             const int bb = hi + ((16 - ((hi + flmis) & 15)) & 15);
             bulk_g2s(W.f[slot], A.flags + ab, (unsigned)(bb - ab), bar);
-            W.foff[slot] = rowb + gc0 - ab;
             return bytes + (unsigned)(bb - ab);
         };
         auto issue_qblock = [&](int cy, int stage) -> unsigned {
@@ -324,29 +320,41 @@ k_sweep_q2(const SweepArgs A) {
             bulk_g2s(W.q[stage], src, (unsigned)(NQ * QARR * 8), &W.bar[stage]);
             return (unsigned)(NQ * QARR * 8);
         };
-        // reads of the staged rows
-        auto val = [&](int slot, int f, int k) -> double {
-            return W.v[slot][U::slot(f)][W.voff[slot][U::slot(f)] + k];
+        // reads of the staged rows b = 0, 1, 2 of the current cell row: ring slot
+        // sb[b], element offset of staged column 0 vo[b][field slot] / fo[b] -- the
+        // alignment shifts of issue_row, recomputed in registers per row step
+        int sb[3] = {0, 0, 0}, vo[3][NF], fo[3] = {0, 0, 0};
+        auto set_window = [&](int j0) {
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                const int j = j0 + b;
+                const int lo = j * np1i + lo_c;
+                sb[b] = j % RING;
+#pragma unroll
+                for (int f = 0; f < NFIELDS; ++f)
+                    if (U::used(f)) vo[b][U::slot(f)] = gc0 - lo_c + ((lo + fmis[f]) & 1);
+                fo[b] = gc0 - lo_c + ((lo + flmis) & 15);
+            }
         };
-        auto flag = [&](int slot, int k) -> uint8_t { return W.f[slot][W.foff[slot] + k]; };
-        auto setv = [&](int slot, int f, int k, double x) {
-            W.v[slot][U::slot(f)][W.voff[slot][U::slot(f)] + k] = x;
+        auto val = [&](int b, int f, int k) -> double {
+            return W.v[sb[b]][U::slot(f)][vo[b][U::slot(f)] + k];
         };
-        // the upper cell row reads the upper slit copies of node row i_mid
-        auto patch_slit = [&](int slot) {
+        auto flag = [&](int b, int k) -> uint8_t { return W.f[sb[b]][fo[b] + k]; };
+        // the upper cell row reads the upper slit copies of node row i_mid (b = 0)
+        auto patch_slit = [&]() {
             for (int k = lane; k < SW_COLS; k += SW_LANES) {
                 const int64_t gc = gcol0 + k;
                 if (gc < 0 || gc >= m.i_mid) continue;
 #pragma unroll
                 for (int f = 0; f < NFIELDS; ++f)
-                    if (U::used(f)) setv(slot, f, k, A.fld[f][A.dupoff + gc]);
-                W.f[slot][W.foff[slot] + k] = A.flags[A.dupoff + gc];
+                    if (U::used(f)) W.v[sb[0]][U::slot(f)][vo[0][U::slot(f)] + k] = A.fld[f][A.dupoff + gc];
+                W.f[sb[0]][fo[0] + k] = A.flags[A.dupoff + gc];
             }
         };
-        // stores: identity rows take the raw staged src value (slot/column) or,
-        // on the rare paths (slot < 0), a global load; rh[0|1|2][c] = this row's
+        // stores: identity rows take the raw staged src value (window row b, column
+        // k) or, on the rare paths (b < 0), a global load; rh[0|1|2][c] = this row's
         // fused rhs, D^-1, acc per component (register prefetch, FUSED only)
-        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int slot, int k,
+        auto store = [&](int64_t gid, const double (&v)[3], uint8_t f, int wb, int k,
                          const double (&rh)[3][3]) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
@@ -356,7 +364,7 @@ k_sweep_q2(const SweepArgs A) {
                 // raw src value of this row (the identity row's entry, the Chebyshev d)
                 double sv = 0.0;
                 if (cons || CHEB)
-                    sv = slot >= 0 ? val(slot, pc == 0 ? FX : pc == 1 ? FY : FP, k) : A.src_out[c][gid];
+                    sv = wb >= 0 ? val(wb, pc == 0 ? FX : pc == 1 ? FY : FP, k) : A.src_out[c][gid];
                 if (cons) x = sv;
                 if (FUSED) x = rh[0][c] - x;
                 if (!CHEB || !A.last) A.dst[c][gid] = x;
@@ -415,19 +423,18 @@ k_sweep_q2(const SweepArgs A) {
             }
             mbar_wait(&W.bar[stage], (phase >> stage) & 1u);
             phase ^= 1u << stage;
-            const int s0 = (2 * cy) % RING, s1 = (2 * cy + 1) % RING, s2 = (2 * cy + 2) % RING;
+            set_window(2 * cy);
             const bool slit_row = m.level >= 1 && cy == half;
             if (slit_row) {
                 __syncwarp();
-                patch_slit(s0);
+                patch_slit();
             }
             __syncwarp();
-            const int sl[3] = {s0, s1, s2};
             const double* rowp[3][NF];   // this lane's staged column 2*lane, per row and field
 #pragma unroll
             for (int b = 0; b < 3; ++b)
 #pragma unroll
-                for (int q = 0; q < NF; ++q) rowp[b][q] = &W.v[sl[b]][q][W.voff[sl[b]][q] + 2 * lane];
+                for (int q = 0; q < NF; ++q) rowp[b][q] = &W.v[sb[b]][q][vo[b][q] + 2 * lane];
             // identity columns (src/pff_operator.py:267): constrained direction
             // entries read as zero; the staged rows keep the raw values
             unsigned mdir = 0u, mact = 0u;
@@ -435,7 +442,7 @@ k_sweep_q2(const SweepArgs A) {
             for (int b = 0; b < 3; ++b)
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const uint8_t fl = flag(sl[b], 2 * lane + a);
+                    const uint8_t fl = flag(b, 2 * lane + a);
                     mdir |= (fl & F_DIR) ? 1u << (3 * b + a) : 0u;
                     mact |= (fl & F_ACT) ? 1u << (3 * b + a) : 0u;
                 }
@@ -655,7 +662,7 @@ k_sweep_q2(const SweepArgs A) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) v[c] = r[c][0][a] + (a == 0 ? left[c][0] : 0.0);
                             rhs_of(A.dupoff + gc, -1, rh);
-                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], s0, 2 * lane + a, rh);
+                            store(A.dupoff + gc, v, A.flags[A.dupoff + gc], 0, 2 * lane + a, rh);
                             continue;
                         }
 #pragma unroll
@@ -663,7 +670,7 @@ k_sweep_q2(const SweepArgs A) {
                             v[c] = r[c][b][a] + (a == 0 ? left[c][b] : 0.0) +
                                    (b == 0 ? carry[c][a] : 0.0);
                         rhs_of(j * np1 + gc, b * 3 + a, rh);
-                        store(j * np1 + gc, v, flag(sl[b], 2 * lane + a), sl[b], 2 * lane + a, rh);
+                        store(j * np1 + gc, v, flag(b, 2 * lane + a), b, 2 * lane + a, rh);
                     }
                 }
             }
@@ -678,7 +685,7 @@ k_sweep_q2(const SweepArgs A) {
                     if (a >= na_out) break;
                     double v[3] = {carry[0][a], carry[1][a], carry[2][a]}, rh[3][3];
                     rhs_of(j * np1 + 2 * (int64_t)cx + a, -1, rh);
-                    store(j * np1 + 2 * (int64_t)cx + a, v, flag(s2, 2 * lane + a), s2,
+                    store(j * np1 + 2 * (int64_t)cx + a, v, flag(2, 2 * lane + a), 2,
                           2 * lane + a, rh);
                 }
             }
