@@ -38,8 +38,16 @@ def main(rep, top=15):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    data = rows[2:]
     isrc, iw = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
+
+    def num(x):
+        try:
+            float(x[iw] or 0)
+            return True
+        except (ValueError, IndexError):
+            return False
+    # several captured launches repeat the header: keep the numeric rows only
+    data = [x for x in rows[2:] if num(x)]
     tot = sum(float(x[iw] or 0) for x in data) or 1
     c = Counter()
     for x in data:
