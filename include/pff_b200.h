@@ -121,6 +121,20 @@ int pff_apply(const pff_level* L, int mode, const double* src, double* dst,
 int pff_apply_rows(const pff_level* L, int mode, const double* src, double* dst,
                    const double* rhs, int cy_begin, int cy_end, void* stream);
 
+/* pff_apply from HOST buffers (the reference's operator takes host arrays,
+ * src/pff_operator.py:262-302): xh (inputs of the mode, component-major as
+ * pff_apply) -> yh, pipelined over cell-row chunks -- every H2D chunk queued
+ * first on an internal copy stream, the row sweep of chunk k on `stream` once
+ * its rows are resident, its D2H on a second copy stream -- so both PCIe
+ * directions and the kernel overlap.  xd / yd are device work buffers of the
+ * input / output size.  Asynchronous: ordered after the work already on
+ * `stream`, and `stream` waits for the last copy, so synchronising `stream`
+ * makes yh valid.  xh / yh should be page-locked for the overlap.
+ * nchunks == 0: the default ramp of chunk sizes; 1..64: equal chunks.
+ * Whole-mesh Q2 sweep levels (>= 64x64 cells) only. */
+int pff_apply_host(const pff_level* L, int mode, const double* xh, double* yh, double* xd,
+                   double* yd, int nchunks, void* stream);
+
 /* block_diagonal (src/pff_operator.py:305-327 -> src/_kernels.py:700-746):
  * diag_uu (2n), diag_pp (n); constrained entries 1; invert != 0 stores 1/d. */
 int pff_diagonal(const pff_level* L, double* diag_uu, double* diag_pp, int invert,

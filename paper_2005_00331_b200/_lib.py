@@ -48,6 +48,7 @@ SIGNATURES = {
     "pff_dense_matvec": (_i, [_i64, _i64, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_coarse_dense": (_i, [_i64, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_apply_rows": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, _i, _i, ctypes.c_void_p]),
+    "pff_apply_host": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_diagonal": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_residual": (_i, [ctypes.c_void_p, _c_dp, _i, _i, ctypes.c_void_p]),
     "pff_cell_matrices": (_i, [ctypes.c_void_p, _c_dp, ctypes.c_void_p]),

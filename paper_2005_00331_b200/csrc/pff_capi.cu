@@ -1,5 +1,10 @@
 // pff_capi.cu -- extern "C" entry points of libpff_b200.so (include/pff_b200.h).
+#include <algorithm>
 #include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -232,6 +237,136 @@ int pff_apply_rows(const pff_level* h, int mode, const double* src, double* dst,
     if (!handled && e == cudaSuccess)
         return fail(PFF_E_ARG, "%s", "pff_apply_rows: needs the Q2 sweep kernel (p = 2, >= 64x64 cells)");
     return check(e, "pff_apply_rows");
+}
+
+namespace {
+
+// Copy streams and events of pff_apply_host: created once per process (the
+// pipeline is enqueue-bound when they are made per call), one pipeline at a
+// time (the mutex), events recycled from a fixed pool.
+struct HostPipe {
+    std::mutex mu;
+    bool ready = false;
+    int device = -1;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    static constexpr int NEV = 3 * 64 + 2;
+    cudaEvent_t ev[NEV] = {};
+    cudaError_t init() {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (ready && dev == device) return cudaSuccess;
+        if (ready) return cudaErrorNotSupported;   // one device per process
+        if ((e = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (auto& x : ev)
+            if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+        device = dev;
+        ready = true;
+        return cudaSuccess;
+    }
+};
+HostPipe g_pipe;
+
+// chunk weights: small first and last chunks shorten the fill (the first
+// chunk's H2D runs alone) and the drain (the last chunk's D2H);
+// PFF_PIPE_RAMP="w0,w1,..." overrides (measurement knob)
+std::vector<int> pipe_ramp() {
+    std::vector<int> w;
+    if (const char* env = std::getenv("PFF_PIPE_RAMP")) {
+        for (const char* c = env; *c;) {
+            char* end = nullptr;
+            const long v = std::strtol(c, &end, 10);
+            if (end == c) break;
+            if (v > 0) w.push_back((int)v);
+            c = *end ? end + 1 : end;
+        }
+    }
+    if (w.empty()) w = {1, 2, 4, 4, 4, 4, 4, 4, 2, 1};
+    return w;
+}
+
+}  // namespace
+
+int pff_apply_host(const pff_level* h, int mode, const double* xh, double* yh, double* xd, double* yd,
+                   int nchunks, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_apply_host: state not bound");
+    if (mode < 0 || mode > 3 || !xh || !yh || !xd || !yd || nchunks < 0 || nchunks > 64)
+        return fail(PFF_E_ARG, "%s", "pff_apply_host: bad mode, null buffer or nchunks outside 0..64");
+    if (L->windowed() || !L->sweep_ok())
+        return fail(PFF_E_ARG, "%s", "pff_apply_host: needs a whole-mesh level on the Q2 sweep kernel (p = 2, >= 64x64 cells)");
+    static const int NC_IN[4] = {3, 2, 1, 3}, NC_OUT[4] = {3, 2, 1, 1};
+    const int cin = NC_IN[mode], cout = NC_OUT[mode];
+    const pff::Mesh& m = L->mesh;
+    const int64_t n = m.n, np1 = m.np1, ng = m.n_grid, nd = m.n_dup, im = m.i_mid;
+    const int ns = m.nside, p = m.p;
+    // chunk boundaries in cell rows
+    std::vector<int> w = nchunks > 0 ? std::vector<int>(nchunks, 1) : pipe_ramp();
+    if ((int)w.size() > ns) w.assign(ns < 8 ? ns : 8, 1);
+    if ((int)w.size() > 64) return fail(PFF_E_ARG, "%s", "pff_apply_host: more than 64 chunks");
+    double tot = 0.0;
+    for (int x : w) tot += x;
+    std::vector<int> cuts{0};
+    double acc = 0.0;
+    for (int x : w) {
+        acc += x;
+        const int c = (int)std::lround(acc / tot * ns);
+        if (c > cuts.back()) cuts.push_back(c);
+    }
+    const int K = (int)cuts.size() - 1;
+    std::lock_guard<std::mutex> lock(g_pipe.mu);
+    cudaError_t e = g_pipe.init();
+    if (e != cudaSuccess) return check(e, "pff_apply_host: streams");
+    cudaStream_t main = S(stream), s_in = g_pipe.s_in, s_out = g_pipe.s_out;
+    cudaEvent_t* ev_in = g_pipe.ev;            // [K]: chunk k's inputs on the device
+    cudaEvent_t* ev_done = g_pipe.ev + 64;     // [K]: chunk k's sweep done
+    cudaEvent_t ev_start = g_pipe.ev[192], ev_end = g_pipe.ev[193];
+    auto copy = [&](double* dst, const double* src, int64_t a, int64_t cnt, int nc, cudaStream_t s) {
+        const size_t pitch = (size_t)n * sizeof(double);
+        return cudaMemcpy2DAsync(dst + a, pitch, src + a, pitch, (size_t)cnt * sizeof(double),
+                                 (size_t)nc, cudaMemcpyDefault, s);
+    };
+#define PFF_TRY(x) do { if ((e = (x)) != cudaSuccess) return check(e, "pff_apply_host"); } while (0)
+    // the caller's earlier work on xd / yd / xh / yh comes first
+    PFF_TRY(cudaEventRecord(ev_start, main));
+    PFF_TRY(cudaStreamWaitEvent(s_in, ev_start, 0));
+    PFF_TRY(cudaStreamWaitEvent(s_out, ev_start, 0));
+    // every H2D first: the copy engine's queue never waits on the host
+    int64_t loaded = -1;   // last node row on the device
+    bool dups_in = nd == 0;
+    for (int k = 0; k < K; ++k) {
+        const int c1 = cuts[k + 1];
+        const int64_t hi = std::min<int64_t>((int64_t)p * c1 + (c1 < ns ? 1 : 0), np1 - 1);
+        if (hi > loaded) {   // all components of the new node rows: one strided copy
+            PFF_TRY(copy(xd, xh, (loaded + 1) * np1, (hi - loaded) * np1, cin, s_in));
+            loaded = hi;
+        }
+        if (!dups_in && c1 > ns / 2) {
+            PFF_TRY(copy(xd, xh, ng, nd, cin, s_in));
+            dups_in = true;
+        }
+        PFF_TRY(cudaEventRecord(ev_in[k], s_in));
+    }
+    for (int k = 0; k < K; ++k) {
+        const int c0 = cuts[k], c1 = cuts[k + 1];
+        PFF_TRY(cudaStreamWaitEvent(main, ev_in[k], 0));
+        bool handled = false;
+        PFF_TRY(pff::launch_sweep_apply_rows(*L, mode, xd, yd, nullptr, c0, c1, main, &handled));
+        if (!handled) return fail(PFF_E_ARG, "%s", "pff_apply_host: sweep kernel refused the rows");
+        PFF_TRY(cudaEventRecord(ev_done[k], main));
+        PFF_TRY(cudaStreamWaitEvent(s_out, ev_done[k], 0));
+        const int64_t top = (int64_t)p * c1 + (c1 == ns ? 1 : 0);
+        PFF_TRY(copy(yh, yd, (int64_t)p * c0 * np1, (top - (int64_t)p * c0) * np1, cout, s_out));
+        if (nd && (int64_t)p * c0 <= im && im < top) PFF_TRY(copy(yh, yd, ng, nd, cout, s_out));
+    }
+    // the caller's stream resumes after the last D2H (and the last H2D)
+    PFF_TRY(cudaEventRecord(ev_end, s_out));
+    PFF_TRY(cudaStreamWaitEvent(main, ev_end, 0));
+    PFF_TRY(cudaEventRecord(ev_start, s_in));
+    PFF_TRY(cudaStreamWaitEvent(main, ev_start, 0));
+#undef PFF_TRY
+    return 0;
 }
 
 int pff_diagonal(const pff_level* h, double* duu, double* dpp, int invert, void* stream) {

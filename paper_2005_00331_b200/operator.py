@@ -365,84 +365,26 @@ class LinearizationState:
         return dst
 
 
-_PIPE_CHUNKS = 8
 _NC_IN = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 3}
 _NC_OUT = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 1}
 
 
-# chunk weights of the pipeline: small first and last chunks shorten the fill
-# (the first chunk's H2D runs alone) and the drain (the last chunk's D2H)
-_PIPE_RAMP = (1, 2, 4, 4, 4, 4, 4, 4, 2, 1)
-
-
-def _pipe_cuts(ns: int):
-    w = _PIPE_RAMP if _PIPE_RAMP else (1,) * _PIPE_CHUNKS
-    if len(w) > ns:
-        w = (1,) * min(_PIPE_CHUNKS, ns)
-    tot = float(sum(w))
-    cuts, acc = [0], 0.0
-    for x in w:
-        acc += x
-        cuts.append(int(round(acc / tot * ns)))
-    return [c for i, c in enumerate(cuts) if i == 0 or c > cuts[i - 1]]
-
-
-def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor) -> torch.Tensor:
-    """Host (pinned) -> device -> host application with the transfers of
-    cell-row chunks overlapped with the sweep kernel (pff_apply_rows): H2D of
-    chunk k+1, compute of chunk k and D2H of chunk k-1 run concurrently on
-    three streams.  Same arithmetic as the one-shot path."""
-    dm = state.dof_map
-    n, np1, ng, nd, im = dm.n_scalar, dm.nodes_per_side, dm.n_grid, dm.n_dup, dm.i_mid
-    ns, p = 2 ** state.level, state.hierarchy.degree
-    cin, cout = _NC_IN[mode], _NC_OUT[mode]
+def _pipelined(state: LinearizationState, mode: int, xh: torch.Tensor, nchunks: int = 0) -> torch.Tensor:
+    """Host (pinned) -> device -> host application through pff_apply_host: the
+    library queues the H2D of every cell-row chunk on one copy stream, sweeps
+    chunk k on the current stream once its rows are resident and copies it
+    back on a second copy stream, so both PCIe directions and the kernel
+    overlap and no per-chunk work is left to the host.  Same arithmetic as the
+    one-shot path (nchunks 0: the library's ramp of chunk sizes)."""
+    n = state.dof_map.n_scalar
     dev = _dev()
-    h = state.bind()
-    xd = torch.empty(cin * n, dtype=torch.float64, device=dev)
-    yd = torch.empty(cout * n, dtype=torch.float64, device=dev)
-    yh = torch.empty(cout * n, dtype=torch.float64, pin_memory=True)
+    xd = torch.empty(_NC_IN[mode] * n, dtype=torch.float64, device=dev)
+    yd = torch.empty(_NC_OUT[mode] * n, dtype=torch.float64, device=dev)
+    yh = torch.empty(_NC_OUT[mode] * n, dtype=torch.float64, pin_memory=True)
     main = torch.cuda.current_stream()
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    s_in.wait_stream(main)
-    cuts = _pipe_cuts(ns)
-    K = len(cuts) - 1
-    ev_out = []
-    loaded = -1                      # last node row already on the device
-    dups_in = nd == 0
-    for k in range(K):
-        c0, c1 = cuts[k], cuts[k + 1]
-        hi = min(p * c1 + (1 if c1 < ns else 0), np1 - 1)
-        with torch.cuda.stream(s_in):
-            if hi > loaded:   # all components of the new node rows: one strided copy
-                a, b = (loaded + 1) * np1, (hi + 1) * np1
-                call("pff_copy_components", xd.data_ptr() + 8 * a, xh.data_ptr() + 8 * a, b - a,
-                     cin, n, s_in.cuda_stream)
-                loaded = hi
-            if not dups_in and c1 > ns // 2:
-                call("pff_copy_components", xd.data_ptr() + 8 * ng, xh.data_ptr() + 8 * ng, nd,
-                     cin, n, s_in.cuda_stream)
-                dups_in = True
-            ev = torch.cuda.Event()
-            ev.record(s_in)
-        main.wait_event(ev)
-        call("pff_apply_rows", h, mode, ptr(xd), ptr(yd), None, c0, c1, main.cuda_stream)
-        evc = torch.cuda.Event()
-        evc.record(main)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(evc)
-            a, b = p * c0 * np1, (p * c1 + (1 if c1 == ns else 0)) * np1
-            call("pff_copy_components", yh.data_ptr() + 8 * a, yd.data_ptr() + 8 * a, b - a, cout,
-                 n, s_out.cuda_stream)
-            if nd and p * c0 <= im < p * c1 + (1 if c1 == ns else 0):
-                call("pff_copy_components", yh.data_ptr() + 8 * ng, yd.data_ptr() + 8 * ng, nd,
-                     cout, n, s_out.cuda_stream)
-            e = torch.cuda.Event()
-            e.record(s_out)
-            ev_out.append(e)
-    main.wait_stream(s_out)
-    ev_out[-1].synchronize()
-    xd.record_stream(s_in)
-    yd.record_stream(s_out)
+    call("pff_apply_host", state.bind(), mode, xh.data_ptr(), yh.data_ptr(), xd.data_ptr(),
+         yd.data_ptr(), nchunks, main.cuda_stream)
+    main.synchronize()
     return yh
 
 

@@ -149,21 +149,10 @@ def test_host_argument_checks_of_session2_entries():
                                    ctypes.c_double(1.0), 0, nul) != 0
         assert L.pff_apply_emit(h, 0, buf, buf, buf, buf, buf, ctypes.c_double(1.0), nul) != 0
         assert L.pff_smooth_init(h, buf, buf, buf, buf, buf, ctypes.c_double(1.0), nul) != 0
+        assert L.pff_apply_host(h, 0, buf, buf, buf, buf, 0, nul) != 0     # unbound
     finally:
         L.pff_level_destroy(h)
     assert b"bad argument" in L.pff_last_error() or b"not bound" in L.pff_last_error()
-
-
-@pytest.mark.parametrize("ns", [64, 100, 1024, 4096])
-def test_pipeline_chunks_partition_the_rows(ns):
-    """The e2e pipeline's ramped chunks cover the cell rows exactly, in order,
-    with small first and last chunks."""
-    from paper_2005_00331_b200 import operator as OP
-    cuts = OP._pipe_cuts(ns)
-    assert cuts[0] == 0 and cuts[-1] == ns
-    assert all(b > a for a, b in zip(cuts, cuts[1:]))
-    sizes = [b - a for a, b in zip(cuts, cuts[1:])]
-    assert sizes[0] <= max(sizes) // 2 and sizes[-1] <= max(sizes) // 2
 
 
 def test_newton_floor_model():

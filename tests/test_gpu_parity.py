@@ -315,7 +315,7 @@ def test_sweep_matches_generic_all_modes(generic_apply, split, level, rows):
 @pytest.mark.parametrize("level", [6, 9])
 def test_pipelined_host_path_matches_device_path(split, level):
     """apply_* with a pinned host tensor runs the chunked H2D/compute/D2H
-    pipeline (pff_apply_rows); results must equal the device path exactly."""
+    pipeline (pff_apply_host); results must equal the device path exactly."""
     ost, x = O.baseline_state(2, level, split, seed=11)
     h = P.build_hierarchy(level, 2)
     st = P.LinearizationState(h, level, ost.params, split=split)
@@ -331,6 +331,27 @@ def test_pipelined_host_path_matches_device_path(split, level):
         assert not got.is_cuda
         want = fn(st, xd[sl].contiguous())
         assert torch.equal(got, want.cpu())
+
+@pytest.mark.parametrize("nchunks", [1, 2, 7, 64])
+def test_apply_host_chunkings(nchunks):
+    """pff_apply_host with equal chunkings (one chunk, two, odd, the maximum
+    64 on a 64-row level: one cell row each) equals the device path per mode."""
+    from paper_2005_00331_b200 import operator as OP
+    from paper_2005_00331_b200 import _lib
+    ost, x = O.baseline_state(2, 6, "miehe", seed=12)
+    h = P.build_hierarchy(6, 2)
+    st = P.LinearizationState(h, 6, ost.params, split="miehe")
+    st.set_solution(ost.U); st.set_phi_tilde(ost.phi_tilde); st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    n = st.n_scalar
+    xd = torch.from_numpy(x).cuda()
+    for mode, sl, nout in ((_lib.MODE_FULL, slice(0, 3 * n), 3 * n), (_lib.MODE_UU, slice(0, 2 * n), 2 * n),
+                           (_lib.MODE_PHIPHI, slice(2 * n, 3 * n), n), (_lib.MODE_PHIROW, slice(0, 3 * n), n)):
+        got = OP._pipelined(st, mode, xd[sl].cpu().contiguous().pin_memory(), nchunks)
+        want = torch.empty(nout, dtype=torch.float64, device="cuda")
+        st.apply_into(mode, xd[sl].contiguous(), want)
+        assert torch.equal(got, want.cpu()), mode
 
 
 @pytest.mark.gpu
