@@ -215,10 +215,12 @@ int pff_mul(int64_t n, const double* a, const double* x, double* y, void* stream
  * 259-275): run r applies mode modes[r] (PFF_MODE_UU or PFF_MODE_PHIPHI) of
  * levels[r] scaled by dhalf[r] = diag^-1/2 (ns[r] entries) for at most
  * max_iterations steps; work[r] holds 4 ns[r] doubles whose first ns[r] are the
- * start vector on entry.  The runs advance in lockstep (two host
- * synchronisations per round); lo_hi (host, 2 nruns) receives the extreme Ritz
- * values; partials: nruns * pff_reduce_scratch_len() doubles, dots: nruns
- * doubles (device).  Synchronises the stream. */
+ * start vector on entry.  The runs advance in lockstep with the recurrence's
+ * scalars kept on the device; the host's stopping tests trail the GPU by one
+ * round (a stopped run's extra round is discarded: same ranges bit for bit);
+ * lo_hi (host, 2 nruns) receives the extreme Ritz values; partials: nruns *
+ * pff_reduce_scratch_len() doubles, dots: 2 nruns doubles (device: alpha,
+ * beta^2 per run).  Synchronises the stream. */
 int pff_lanczos_ranges(int nruns, const pff_level* const* levels, const int* modes,
                        const int64_t* ns, const double* const* dhalf, double* const* work,
                        int max_iterations, double* lo_hi, double* partials, double* dots,

@@ -2,9 +2,10 @@
 // (src/multigrid.py:123-162 estimate_lambda_range, run for every level and
 // block as in GmgPreconditioner._estimate_ranges, 259-275).
 //
-// The runs are independent; they advance in lockstep so each round costs two
-// host synchronisations for all of them (alpha = v.w, then |w|), and the loop,
-// the launches and the tridiagonal Ritz values stay in C++ instead of ~150
+// The runs are independent; they advance in lockstep, the scalars of the
+// recurrence stay on the device, and the host (Ritz values, stopping tests)
+// trails the GPU by one round, so no round waits on the host; the loop, the
+// launches and the tridiagonal Ritz values stay in C++ instead of ~150
 // Python/ctypes calls per round.  Per run and iteration, exactly the
 // reference's recurrence on the Jacobi-scaled operator D^-1/2 A D^-1/2:
 //   w = D^-1/2 A D^-1/2 v - beta v_prev;  alpha = v.w;  w -= alpha v;
@@ -16,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "pff_internal.cuh"
@@ -70,8 +72,8 @@ struct LzBatch {
     double* vp[LZ_MAX];
     double* w[LZ_MAX];
     double* tmp[LZ_MAX];
-    double s[LZ_MAX];            // beta (post, pre: divisor) or alpha
-    int div[LZ_MAX];             // pre: v = v / s first
+    int first;                   // round 0: no v / beta scaling, beta_prev = 0
+    const double* sc;            // device scalars: sc[2 run] = alpha, sc[2 run + 1] = beta^2
 };
 
 __device__ __forceinline__ double lz_block_sum(double v) {
@@ -91,15 +93,16 @@ __device__ __forceinline__ double lz_block_sum(double v) {
     return t;
 }
 
-// (v = v / s;) tmp = dhalf v
+// (v = v / beta;) tmp = dhalf v -- beta = sqrt of the previous round's w.w,
+// read on the device (IEEE sqrt: the same double the host's std::sqrt gives)
 __global__ void __launch_bounds__(RED_THREADS) k_lz_pre(const LzBatch B) {
     const int r = blockIdx.y;
     const int64_t n = B.n[r];
     const double* dh = B.dhalf[r];
     double* v = B.v[r];
     double* t = B.tmp[r];
-    const bool dv = B.div[r] != 0;
-    const double sv = B.s[r];
+    const bool dv = !B.first;
+    const double sv = dv ? sqrt(B.sc[2 * B.slot[r] + 1]) : 1.0;
     for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
          i += (int64_t)RED_BLOCKS * RED_THREADS) {
         double x = v[i];
@@ -117,7 +120,8 @@ template <bool POST>
 __global__ void __launch_bounds__(RED_THREADS) k_lz_update(const LzBatch B, double* part) {
     const int r = blockIdx.y;
     const int64_t n = B.n[r];
-    const double a = -B.s[r];
+    // POST: -beta_prev (-0 in round 0, as the host's beta = 0 gave);  alpha step: -alpha
+    const double a = POST ? (B.first ? -0.0 : -sqrt(B.sc[2 * B.slot[r] + 1])) : -B.sc[2 * B.slot[r]];
     const double* dh = B.dhalf[r];
     const double* v = B.v[r];
     const double* x = POST ? B.vp[r] : B.v[r];
@@ -135,16 +139,26 @@ __global__ void __launch_bounds__(RED_THREADS) k_lz_update(const LzBatch B, doub
     if (threadIdx.x == 0) part[(int64_t)B.slot[r] * 2 * RED_BLOCKS + blockIdx.x] = t;
 }
 
-// dots[slot] = fixed-order sum of the run's RED_BLOCKS partials
+// dots[2 slot + which] = fixed-order sum of the run's RED_BLOCKS partials
 __global__ void __launch_bounds__(RED_THREADS) k_lz_final(const LzBatch B, const double* part,
-                                                          double* dots) {
+                                                          double* dots, int which) {
     const int slot = B.slot[blockIdx.x];
     const double* p = part + (int64_t)slot * 2 * RED_BLOCKS;
     double v = 0.0;
     for (int k = threadIdx.x; k < RED_BLOCKS; k += RED_THREADS) v += p[k];
     const double t = lz_block_sum(v);
-    if (threadIdx.x == 0) dots[slot] = t;
+    if (threadIdx.x == 0) dots[2 * slot + which] = t;
 }
+
+// pinned history of the per-round scalars (grown on demand, one driver at a time)
+struct LzHost {
+    std::mutex mu;
+    double* hist = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev[4] = {};
+    int device = -1;
+};
+LzHost g_lz;
 
 struct Run {
     const Level* L;
@@ -180,22 +194,50 @@ cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* mod
         cudaError_t e = cudaMemsetAsync(R.vp, 0, sizeof(double) * R.n, s);
         if (e != cudaSuccess) return e;
     }
-    std::vector<double> host(nruns);
-    auto fetch = [&]() -> cudaError_t {
-        cudaError_t e = cudaMemcpyAsync(host.data(), dots, sizeof(double) * nruns,
-                                        cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        return e;
-    };
-    cudaError_t e = cudaSuccess;
+    // The scalars never leave the device inside a round: alpha and beta^2 land in
+    // dots[2 r], dots[2 r + 1] and the kernels read them from there.  Each round
+    // ends with an async copy of dots into a pinned history slot; the host
+    // processes round k (Ritz values, stopping tests) while the GPU already runs
+    // round k + 1.  A run that stops at round k has done one extra round on its
+    // own scratch vectors, which nothing reads: its alphas / betas, hence its
+    // range, are those of the synchronous recurrence, bit for bit.
+    std::lock_guard<std::mutex> lock(g_lz.mu);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (g_lz.device != dev) {
+        if (g_lz.device >= 0) return cudaErrorNotSupported;   // one device per process
+        for (auto& x : g_lz.ev)
+            if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+        g_lz.device = dev;
+    }
+    const int max_rounds = std::max(1, max_it) + 2;
+    const size_t need = (size_t)max_rounds * 2 * nruns;
+    if (g_lz.cap < need) {
+        if (g_lz.hist) cudaFreeHost(g_lz.hist);
+        g_lz.hist = nullptr;
+        g_lz.cap = 0;
+        if ((e = cudaHostAlloc(&g_lz.hist, need * sizeof(double), cudaHostAllocDefault)) != cudaSuccess) return e;
+        g_lz.cap = need;
+    }
     // the active runs in batches of LZ_MAX; per phase one launch per batch
-    auto batches = [&](auto&& fill, auto&& launch) -> cudaError_t {
+    std::vector<char> live(nruns);   // in the round being enqueued
+    auto batches = [&](int first, auto&& launch) -> cudaError_t {
         LzBatch B;
         B.nr = 0;
+        B.first = first;
+        B.sc = dots;
         for (int r = 0; r < nruns; ++r) {
-            if (runs[r].done) continue;
-            fill(B, B.nr, r);
-            B.slot[B.nr] = r;
+            if (!live[r]) continue;
+            const Run& R = runs[r];
+            const int k = B.nr;
+            B.n[k] = R.n;
+            B.dhalf[k] = R.dhalf;
+            B.v[k] = R.v;
+            B.vp[k] = R.vp;
+            B.w[k] = R.w;
+            B.tmp[k] = R.tmp;
+            B.slot[k] = r;
             if (++B.nr == LZ_MAX) {
                 cudaError_t x = launch(B);
                 if (x != cudaSuccess) return x;
@@ -204,87 +246,91 @@ cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* mod
         }
         return B.nr ? launch(B) : cudaSuccess;
     };
-    auto base = [&](LzBatch& B, int k, int r) {
-        const Run& R = runs[r];
-        B.n[k] = R.n;
-        B.dhalf[k] = R.dhalf;
-        B.v[k] = R.v;
-        B.vp[k] = R.vp;
-        B.w[k] = R.w;
-        B.tmp[k] = R.tmp;
-        B.div[k] = 0;
-        B.s[k] = 0.0;
-    };
-    auto final_dots = [&](const LzBatch& B) -> cudaError_t {
-        k_lz_final<<<B.nr, RED_THREADS, 0, s>>>(B, partials, dots);
+    auto final_dots = [&](const LzBatch& B, int which) -> cudaError_t {
+        k_lz_final<<<B.nr, RED_THREADS, 0, s>>>(B, partials, dots, which);
         count_launches(1);
         return cudaGetLastError();
     };
-    std::vector<double> pending_div(nruns, 0.0);   // v = v / beta at the next round's start
-    for (;;) {
-        bool any = false;
-        for (int r = 0; r < nruns; ++r) any = any || !runs[r].done;
-        if (!any) break;
-        // (v = v / beta;) tmp = D^-1/2 v
-        e = batches([&](LzBatch& B, int k, int r) {
-                        base(B, k, r);
-                        B.div[k] = pending_div[r] != 0.0;
-                        B.s[k] = pending_div[r];
-                    },
-                    [&](const LzBatch& B) -> cudaError_t {
-                        k_lz_pre<<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B);
-                        count_launches(1);
-                        return cudaGetLastError();
-                    });
-        if (e != cudaSuccess) return e;
-        for (int r = 0; r < nruns; ++r) {
-            pending_div[r] = 0.0;
-            Run& R = runs[r];
-            if (R.done) continue;
-            if ((e = launch_apply(*R.L, R.mode, R.tmp, R.w, nullptr, s)) != cudaSuccess) return e;
-        }
+    // one round for the runs in `live`: device work, then the scalars to hist[round]
+    auto enqueue = [&](int round) -> cudaError_t {
+        cudaError_t x = batches(round == 0, [&](const LzBatch& B) -> cudaError_t {
+            // (v = w_prev / beta;) tmp = D^-1/2 v
+            k_lz_pre<<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B);
+            count_launches(1);
+            return cudaGetLastError();
+        });
+        if (x != cudaSuccess) return x;
+        for (int r = 0; r < nruns; ++r)
+            if (live[r] && (x = launch_apply(*runs[r].L, runs[r].mode, runs[r].tmp, runs[r].w, nullptr, s)) != cudaSuccess)
+                return x;
         // w = D^-1/2 w - beta v_prev;  alpha = v.w
-        e = batches([&](LzBatch& B, int k, int r) {
-                        base(B, k, r);
-                        B.s[k] = runs[r].beta;
-                    },
-                    [&](const LzBatch& B) -> cudaError_t {
-                        k_lz_update<true><<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B, partials);
-                        count_launches(1);
-                        cudaError_t x = cudaGetLastError();
-                        return x != cudaSuccess ? x : final_dots(B);
-                    });
-        if (e != cudaSuccess) return e;
-        if ((e = fetch()) != cudaSuccess) return e;
+        x = batches(round == 0, [&](const LzBatch& B) -> cudaError_t {
+            k_lz_update<true><<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B, partials);
+            count_launches(1);
+            cudaError_t y = cudaGetLastError();
+            return y != cudaSuccess ? y : final_dots(B, 0);
+        });
+        if (x != cudaSuccess) return x;
+        // w -= alpha v;  beta^2 = w.w
+        x = batches(round == 0, [&](const LzBatch& B) -> cudaError_t {
+            k_lz_update<false><<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B, partials);
+            count_launches(1);
+            cudaError_t y = cudaGetLastError();
+            return y != cudaSuccess ? y : final_dots(B, 1);
+        });
+        if (x != cudaSuccess) return x;
+        x = cudaMemcpyAsync(g_lz.hist + (size_t)round * 2 * nruns, dots, sizeof(double) * 2 * nruns,
+                            cudaMemcpyDeviceToHost, s);
+        if (x != cudaSuccess) return x;
+        // v_prev, v, w = v, w, v_prev for the next round (the swap the recurrence does
+        // after a non-stopping round; a stopped run's later rounds are never read)
+        for (int r = 0; r < nruns; ++r)
+            if (live[r]) {
+                Run& R = runs[r];
+                double* old_vp = R.vp;
+                R.vp = R.v;
+                R.v = R.w;
+                R.w = old_vp;
+            }
+        return cudaEventRecord(g_lz.ev[round & 3], s);
+    };
+    std::vector<std::vector<char>> members;   // runs in each enqueued round
+    auto any_live = [&]() {
+        for (int r = 0; r < nruns; ++r) live[r] = !runs[r].done;
+        for (int r = 0; r < nruns; ++r)
+            if (live[r]) return true;
+        return false;
+    };
+    int enq = 0;
+    if (any_live()) {
+        members.push_back(live);
+        if ((e = enqueue(enq++)) != cudaSuccess) return e;
+    }
+    for (int k = 0; k < enq; ++k) {
+        // keep the GPU one round ahead: round k + 1 for every run not known to be done
+        if (k + 1 == enq && enq < max_rounds && any_live()) {
+            members.push_back(live);
+            if ((e = enqueue(enq++)) != cudaSuccess) return e;
+        }
+        if ((e = cudaEventSynchronize(g_lz.ev[k & 3])) != cudaSuccess) return e;
+        const double* h = g_lz.hist + (size_t)k * 2 * nruns;
+        const std::vector<char>& in = members[k];
+        for (int r = 0; r < nruns; ++r)
+            if (in[r] && !runs[r].done) runs[r].alphas.push_back(h[2 * r]);
         // largest Ritz value of every active run (it drives the stopping test;
         // the smallest is needed only once a run stops): independent
         // bisections, spread over the host cores
-        for (int r = 0; r < nruns; ++r)
-            if (!runs[r].done) runs[r].alphas.push_back(host[r]);
 #pragma omp parallel for schedule(dynamic, 1)
         for (int r = 0; r < nruns; ++r) {
             Run& R = runs[r];
-            if (R.done) continue;
+            if (!in[r] || R.done) continue;
             if (R.betas.empty()) R.lo = R.hi = R.alphas.back();
             else R.hi = tridiag_eig(R.alphas, R.betas, (int)R.alphas.size() - 1);
         }
-        // w -= alpha v;  beta^2 = w.w
-        e = batches([&](LzBatch& B, int k, int r) {
-                        base(B, k, r);
-                        B.s[k] = runs[r].alphas.back();
-                    },
-                    [&](const LzBatch& B) -> cudaError_t {
-                        k_lz_update<false><<<dim3(RED_BLOCKS, B.nr), RED_THREADS, 0, s>>>(B, partials);
-                        count_launches(1);
-                        cudaError_t x = cudaGetLastError();
-                        return x != cudaSuccess ? x : final_dots(B);
-                    });
-        if (e != cudaSuccess) return e;
-        if ((e = fetch()) != cudaSuccess) return e;
         for (int r = 0; r < nruns; ++r) {
             Run& R = runs[r];
-            if (R.done) continue;
-            const double beta = std::sqrt(host[r]);
+            if (!in[r] || R.done) continue;
+            const double beta = std::sqrt(h[2 * r + 1]);
             R.beta = beta;
             R.left -= 1;
             if (beta < 1e-12 * std::max(1.0, std::fabs(R.hi))) { R.done = true; continue; }
@@ -296,14 +342,11 @@ cudaError_t lanczos_ranges(int nruns, const Level* const* levels, const int* mod
             R.prev = R.hi;
             R.has_prev = true;
             R.betas.push_back(beta);
-            double* old_vp = R.vp;
-            R.vp = R.v;
-            R.v = R.w;
-            R.w = old_vp;
-            pending_div[r] = beta;   // v = w / beta, fused into the next round's scaling
             if (R.left <= 0) R.done = true;
         }
     }
+    // the speculative last round has finished before the caller reuses dots / work
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int r = 0; r < nruns; ++r) {
         Run& R = runs[r];

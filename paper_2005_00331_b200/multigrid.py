@@ -729,7 +729,7 @@ class GmgPreconditioner:
         dev = descs[0][6].device
         plen = _lib.load().pff_reduce_scratch_len()
         partials = torch.empty(R * plen, dtype=torch.float64, device=dev)
-        dots = torch.empty(R, dtype=torch.float64, device=dev)
+        dots = torch.empty(2 * R, dtype=torch.float64, device=dev)   # alpha, beta^2 per run
         lo_hi = np.zeros(2 * R)
         arr = lambda ctype, vals: (ctype * R)(*vals)  # noqa: E731
         call("pff_lanczos_ranges", R, arr(ctypes.c_void_p, [d[2].value for d in descs]),
