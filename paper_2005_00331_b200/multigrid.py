@@ -557,15 +557,17 @@ class GmgPreconditioner:
             theta, delta = 0.5 * (b + a), 0.5 * (b - a)
             sigma1 = theta / delta
             eye = torch.eye(nb, dtype=torch.float64, device=A.device)
-            d = invd[:, None] * eye / theta
+            dcol = invd[:, None].contiguous()
+            d = dcol * eye / theta
             acc = d.clone()
             cr = eye
             rho_old = 1.0 / sigma1
+            # in place, four launches per step (the setup is launch-bound here)
             for _ in range(1, sweeps):
                 rho = 1.0 / (2.0 * sigma1 - rho_old)
-                cr = cr - A @ d
-                d = (rho * rho_old) * d + (2.0 * rho / delta) * (invd[:, None] * cr)
-                acc = acc + d
+                cr = torch.addmm(cr, A, d, alpha=-1.0)
+                d.mul_(rho * rho_old).addcmul_(dcol, cr, value=2.0 * rho / delta)
+                acc.add_(d)
                 rho_old = rho
             return acc.contiguous()
 
