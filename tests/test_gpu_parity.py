@@ -354,6 +354,33 @@ def test_apply_host_chunkings(nchunks):
         assert torch.equal(got, want.cpu()), mode
 
 
+def test_apply_host_pageable_buffers():
+    """pff_apply_host on pageable (numpy) host buffers: the copies are staged by
+    the driver instead of overlapped, the result is the same bit for bit."""
+    import ctypes
+    from paper_2005_00331_b200 import _lib
+    ost, x = O.baseline_state(2, 6, "none", seed=13)
+    h = P.build_hierarchy(6, 2)
+    st = P.LinearizationState(h, 6, ost.params, split="none")
+    st.set_solution(ost.U); st.set_phi_tilde(ost.phi_tilde); st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    n = st.n_scalar
+    xh = np.ascontiguousarray(x, dtype=np.float64)
+    yh = np.zeros(3 * n)
+    xd = torch.empty(3 * n, dtype=torch.float64, device="cuda")
+    yd = torch.empty(3 * n, dtype=torch.float64, device="cuda")
+    L = _lib.load()
+    s = torch.cuda.current_stream()
+    assert L.pff_apply_host(st.bind(), _lib.MODE_FULL, xh.ctypes.data_as(ctypes.c_void_p),
+                            yh.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(xd.data_ptr()),
+                            ctypes.c_void_p(yd.data_ptr()), 5, ctypes.c_void_p(s.cuda_stream)) == 0
+    s.synchronize()
+    want = torch.empty(3 * n, dtype=torch.float64, device="cuda")
+    st.apply_into(_lib.MODE_FULL, torch.from_numpy(xh).cuda(), want)
+    assert np.array_equal(yh, want.cpu().numpy())
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("split", ["miehe", "none"])
 def test_vcycle_fused_chebyshev_start_bitwise(split):
