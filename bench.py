@@ -319,7 +319,7 @@ def run_ours(args):
         "e2e": {"value": round(dofs / e2e_s / 1e9, 4), "unit": "GDoF/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "paper_2005_00331_b200.apply_jacobian(state, pinned host tensor): "
-                "row-chunked H2D / sweep / D2H pipeline on three streams"
+                "one pff_apply_host call: row-chunked H2D / sweep / D2H pipeline (copy streams driven natively)"
                         if ws == 1 else "SlabState.apply_into with pinned host slab buffers"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
