@@ -78,6 +78,18 @@ k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
         wy[m] = Es[chy][b][m];
     }
     double acc[3] = {0.0, 0.0, 0.0};
+    const double* xk[3] = {xc, xc + mc.n, xc + 2 * mc.n};
+    // coarse node of (mx, my) in the parent cell (Mesh::node; 32-bit when SMALL:
+    // the coarse level is a quarter of the fine one)
+    const bool cup = mc.level >= 1 && ccy >= (mc.nside >> 1);
+    auto cnode = [&](int mx, int my) -> int64_t {
+        if (SMALL) {
+            const int jc = P * ccy + my, ic = P * ccx + mx;
+            const int imc = (int)mc.i_mid;
+            return cup && jc == imc && ic < imc ? (int)mc.n_grid + ic : jc * (int)mc.np1 + ic;
+        }
+        return mc.node(ccx, ccy, mx, my);
+    };
     // branch-free: a dropped weight (|w| <= 1e-14, multigrid.py:81-83) is an exact
     // zero, and fma(0, x, acc) == acc for finite x -- the same sums without the
     // per-lane divergent filter (neighbouring fine nodes have different patterns)
@@ -87,9 +99,9 @@ k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
         for (int mx = 0; mx < N1; ++mx) {
             const double w0 = wy[my] * wx[mx];
             const double w = fabs(w0) > 1e-14 ? w0 : 0.0;
-            const int64_t c = mc.node(ccx, ccy, mx, my);
+            const int64_t c = cnode(mx, my);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) acc[k] = fma(w, xc[k * mc.n + c], acc[k]);
+            for (int k = 0; k < 3; ++k) acc[k] = fma(w, xk[k][c], acc[k]);
         }
     if (add_masked) {
         // z += where(cons, 0, P zc)  (src/multigrid.py:340-342)
