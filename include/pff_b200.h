@@ -65,8 +65,11 @@ int64_t pff_launch_counter(void);
 /* tuning / testing knobs (process-wide):
  *   PFF_OPT_GENERIC_APPLY: 1 = route pff_apply through the generic per-cell
  *     atomic kernel for every degree (the Q2 sweep kernel is the default)
- *   PFF_OPT_SWEEP_ROWS: cell rows per warp chunk of the Q2 sweep (0 = auto) */
-enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2 };
+ *   PFF_OPT_SWEEP_ROWS: cell rows per warp chunk of the Q2 sweep (0 = auto)
+ *   PFF_OPT_SWEEP_MIN_NSIDE: smallest Q2 mesh (cells per side) on the sweep
+ *     kernel for levels created AFTER the call (a level keeps the layout it was
+ *     created with); 0 = PFF_SWEEP_MIN_NSIDE or the default 64, minimum 4 */
+enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2, PFF_OPT_SWEEP_MIN_NSIDE = 3 };
 int pff_set_option(int key, int value);
 
 /* One mesh level (replaces DofMap + LinearizationState's static data,
@@ -81,6 +84,9 @@ int pff_level_destroy(pff_level* L);
 int64_t pff_level_n_scalar(const pff_level* L);
 int64_t pff_level_n_cells(const pff_level* L);
 int64_t pff_level_qcache_len(const pff_level* L);
+/* 1 when the level's applications run the Q2 sweep kernel (fixed at creation,
+ * PFF_OPT_SWEEP_MIN_NSIDE), 0 for the generic cooperative kernel, -1 on NULL */
+int pff_level_uses_sweep(const pff_level* L);
 
 /* Slab window for multi-GPU runs: the handle then owns cell
  * rows [cy_begin, cy_end) of the global mesh and every array bound to it or

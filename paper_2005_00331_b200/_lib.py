@@ -30,6 +30,7 @@ SIGNATURES = {
     "pff_level_n_scalar": (_i64, [ctypes.c_void_p]),
     "pff_level_n_cells": (_i64, [ctypes.c_void_p]),
     "pff_level_qcache_len": (_i64, [ctypes.c_void_p]),
+    "pff_level_uses_sweep": (_i, [ctypes.c_void_p]),
     "pff_level_set_window": (_i, [ctypes.c_void_p, _i, _i]),
     "pff_level_window": (_i, [ctypes.c_void_p, ctypes.c_void_p]),
     "pff_level_bind": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp]),
@@ -82,7 +83,7 @@ MODE_FULL, MODE_UU, MODE_PHIPHI, MODE_PHIROW = 0, 1, 2, 3
 FLAG_DIRICHLET, FLAG_ACTIVE = 1, 2
 LAYOUT_FULL, LAYOUT_UU, LAYOUT_PHI = 0, 1, 2
 CONS_SELECT, CONS_ZERO, CONS_COPY, CONS_EXCLUDE = 0, 1, 2, 3
-OPT_GENERIC_APPLY, OPT_SWEEP_ROWS = 1, 2
+OPT_GENERIC_APPLY, OPT_SWEEP_ROWS, OPT_SWEEP_MIN_NSIDE = 1, 2, 3
 CHEB_FIRST, CHEB_LAST = 1, 2
 
 

@@ -52,6 +52,7 @@ int pff_set_option(int key, int value) {
     switch (key) {
         case PFF_OPT_GENERIC_APPLY: pff::set_generic_apply(value != 0); return 0;
         case PFF_OPT_SWEEP_ROWS: pff::set_sweep_rows_per_chunk(value); return 0;
+        case PFF_OPT_SWEEP_MIN_NSIDE: pff::set_sweep_min_nside(value); return 0;
     }
     return fail(PFF_E_ARG, "%s", "pff_set_option: unknown key");
 }
@@ -90,6 +91,7 @@ int pff_level_create(pff_level** out, int degree, int level, int split, const pf
         for (int a = 0; a < 3; ++a)   // mirror symmetry of the outer Gauss points
             ok = ok && near(S.N[2][a], S.N[0][2 - a], 1e-14) && near(S.D[2][a], -S.D[0][2 - a], 1e-13);
         L->q2_struct = ok;
+        L->min_nside = pff::sweep_min_nside();
     }
     L->miehe = split;
     *out = reinterpret_cast<pff_level*>(L);
@@ -140,6 +142,10 @@ int64_t pff_level_n_cells(const pff_level* L) {
 
 int64_t pff_level_qcache_len(const pff_level* L) {
     return L ? reinterpret_cast<const Level*>(L)->qcache_len() : -1;
+}
+
+int pff_level_uses_sweep(const pff_level* L) {
+    return L ? (reinterpret_cast<const Level*>(L)->sweep_ok() ? 1 : 0) : -1;
 }
 
 int pff_level_bind(pff_level* h, const double* U, const double* phi_tilde, const uint8_t* flags,

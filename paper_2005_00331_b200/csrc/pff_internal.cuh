@@ -31,6 +31,7 @@ struct Win {
 // smallest mesh (cells per side) on the Q2 sweep kernel (PFF_SWEEP_MIN_NSIDE);
 // below it the generic cooperative kernel runs (pff_sweep.cu)
 int sweep_min_nside();
+void set_sweep_min_nside(int nside);
 
 // Per-level handle contents (the C-ABI's opaque pff_level).
 struct Level {
@@ -91,8 +92,9 @@ struct Level {
     // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
     // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
+    int min_nside = 64;       // sweep_min_nside() when the level was created (fixes its layout)
     bool sweep_ok() const {   // the sweep kernel stages with 32-bit node indices
-        return mesh.p == 2 && mesh.nside >= sweep_min_nside() && q2_struct &&
+        return mesh.p == 2 && mesh.nside >= min_nside && q2_struct &&
                mesh.n < (int64_t(1) << 31);
     }
     int n_strips() const { return (mesh.nside + 30) / 31; }

@@ -792,16 +792,21 @@ int g_rows_override = 0;
 
 void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
 
+static int g_min_nside = -1;   // -1: PFF_SWEEP_MIN_NSIDE or the default
+
+void set_sweep_min_nside(int v) { g_min_nside = v <= 0 ? -1 : (v < 4 ? 4 : v); }
+
 int sweep_min_nside() {
-    static int v = -1;
-    if (v < 0) {
+    static int env = -1;
+    if (g_min_nside > 0) return g_min_nside;
+    if (env < 0) {
         const char* e = getenv("PFF_SWEEP_MIN_NSIDE");
         // measured: 16 / 32 cut the Newton solve's launch count by 8-16 % but add
         // 0.4-0.9 ms of device time; the bench's GMRES time is not better -> 64
-        v = e ? atoi(e) : 64;
-        if (v < 4) v = 4;
+        env = e ? atoi(e) : 64;
+        if (env < 4) env = 4;
     }
-    return v;
+    return env;
 }
 
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s) {

@@ -253,6 +253,10 @@ class LinearizationState:
             self._dir.set(None, index=nodes)
         self._version += 1
 
+    def uses_sweep_kernel(self) -> bool:
+        """True when this level's applications run the Q2 sweep kernel."""
+        return _lib.load().pff_level_uses_sweep(self._level_handle()) == 1
+
     def constrained_mask(self) -> np.ndarray:
         d = self.dirichlet_nodes
         return np.concatenate([d, d, self.active])

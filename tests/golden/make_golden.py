@@ -246,7 +246,66 @@ SIMULATION = {
 }
 
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from conftest import sketch  # noqa: E402  (the tests recompute it from the device result)
+
+
+def production_case(p, level, split, seed, full, gmres=True, restart=50, sweeps=3):
+    """The configs[3] Newton-step inputs (notch phi0) at `level`, solved by the
+    reference (src/multigrid.py:228-344 + src/krylov.py:37-119).  full=True
+    stores the V-cycle and GMRES vectors; otherwise only their sketches."""
+    import time
+    h = build_hierarchy(level, p)
+    st, x = make(h, level, split, seed, True)
+    n = st.n_scalar
+    t0 = time.perf_counter()
+    gmg = GmgPreconditioner(h, coarse_level=2, cheb=ChebyshevConfig(sweeps=sweeps))
+    gmg.setup(st)
+    d = {"setup_s": np.array([time.perf_counter() - t0])}
+    for l, rg in gmg.ranges.items():
+        d[f"range_{l}"] = np.array([rg["uu"][0], rg["uu"][1], rg["phiphi"][0], rg["phiphi"][1]])
+    t0 = time.perf_counter()
+    z = gmg.apply(x)
+    d["vcycle_s"] = np.array([time.perf_counter() - t0])
+    if full:
+        d["vcycle"] = z
+    else:
+        for k, v in sketch(z, n).items():
+            d["vcycle_" + k] = v
+    if gmres:
+        rhs = x.copy()
+        rhs[st.constrained_mask()] = 0.0
+        t0 = time.perf_counter()
+        res = gmres_solve(lambda v: op.apply_jacobian(st, v), rhs,
+                          KrylovConfig(relative_tolerance=1e-8, restart=restart),
+                          preconditioner=gmg.apply)
+        d["gmres_s"] = np.array([time.perf_counter() - t0])
+        d["gmres_iters"] = np.array([res.iterations])
+        d["gmres_hist"] = np.array(res.residual_history)
+        d["gmres_conv"] = np.array([int(res.converged)])
+        if full:
+            d["gmres_x"] = res.solution
+        else:
+            for k, v in sketch(res.solution, n).items():
+                d["gmres_x_" + k] = v
+    d["meta"] = np.array([p, level, seed, 1 if split == "miehe" else 0, 1, sweeps, restart])
+    return d
+
+
 def main():
+    if "--production" in sys.argv:   # production-size pins (the configs[3] inputs)
+        # python make_golden.py --production LEVEL SPLIT {full|sketch|vcycle} [RESTART]
+        i = sys.argv.index("--production")
+        level, split, kind = int(sys.argv[i + 1]), sys.argv[i + 2], sys.argv[i + 3]
+        restart = int(sys.argv[i + 4]) if len(sys.argv) > i + 4 else 50
+        d = production_case(2, level, split, 0, full=(kind == "full"),
+                            gmres=(kind != "vcycle"), restart=restart)
+        tag = "" if restart == 50 else f"_r{restart}"
+        name = f"prod_p2_l{level}_{split}{tag}" + ("_vcycle" if kind == "vcycle" else "")
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+        print(name, {k: v.tolist() for k, v in d.items()
+                     if k.endswith(("_s", "iters")) or k.startswith("range_")})
+        return
     if "--assembled" in sys.argv:   # only the assembled-path fixtures
         for p, level, split, seed in ((2, 2, "miehe", 4), (2, 2, "none", 4), (1, 3, "miehe", 8),
                                       (3, 2, "miehe", 2)):

@@ -1,0 +1,220 @@
+"""Production-size parity: the multigrid and Krylov layers where the Q2 sweep
+kernel and the large-level transfer paths actually run.
+
+The small solver goldens (levels 4-5, tests/test_gpu_parity.py) sit below the
+sweep kernel's threshold (64 cells per side), so these tests pin, against the
+REFERENCE itself (fixtures tests/golden/prod_*.npz from
+`make_golden.py --production`) and against the C oracle:
+
+* level 7 (128^2 Q2, levels 6-7 on the sweep kernel): Lanczos ranges, one
+  V-cycle and the GMRES(50) solve of the configs[3] inputs;
+* level 10 (configs[3], 1024^2): the ranges and the V-cycle against a sketch
+  of the reference's output (norms, projections, 4096 sampled entries per
+  block) and the whole vector against oracle.Gmg;
+* the PR1 goldens (32^2) with the sweep kernel forced onto that level;
+* the fine-level transfer kernels bound to states (element-vector scratch,
+  shared-memory-staged restriction, 32-bit prolongation) against P / P^T.
+
+Reference: src/multigrid.py:123-162, 201-344; src/krylov.py:37-119.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import bench
+from conftest import block_rel, load_golden, rel_l2, sketch, sketch_rel
+import paper_2005_00331_b200 as P
+from paper_2005_00331_b200 import _lib
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _state(level, split, p=2):
+    h, params, U, pt, act, dirn, x = bench.baseline_inputs(p, level, split, seed=0, notch=True)
+    st = P.LinearizationState(h, level, params, split=split)
+    st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    st.refresh_cache()
+    return st, x
+
+
+def _oracle_state(level, split, nt):
+    ost, x = O.baseline_state(2, level, split, seed=0, notch=True)
+    ost.refresh_cache(nthreads=nt)
+    return ost, x
+
+
+def _ranges(d, level):
+    out = {}
+    for l in range(2, level + 1):
+        r = d[f"range_{l}"]
+        out[l] = {"uu": (float(r[0]), float(r[1])), "phiphi": (float(r[2]), float(r[3]))}
+    return out
+
+
+def _check_ranges(gmg, d, level):
+    for l in range(2, level + 1):
+        got = gmg.ranges[l]
+        assert np.allclose([got["uu"][0], got["uu"][1], got["phiphi"][0], got["phiphi"][1]],
+                           d[f"range_{l}"], rtol=1e-10, atol=0), l
+
+
+def _np(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_level7_vcycle_and_gmres_vs_reference(split):
+    """128^2 Q2 (configs[3] inputs): ranges, V-cycle (graph and eager, with
+    estimated and with injected ranges) and GMRES(50) against the reference."""
+    d = load_golden(f"prod_p2_l7_{split}")
+    st, x = _state(7, split)
+    n = st.n_scalar
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    _check_ranges(gmg, d, 7)
+    z = _np(gmg.apply(x))
+    assert max(block_rel(z, d["vcycle"], n)) <= TOL
+    gmg.use_graph = False
+    assert max(block_rel(_np(gmg.apply(x)), d["vcycle"], n)) <= TOL
+    gmg.use_graph = True
+    gi = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gi.setup(st, ranges=_ranges(d, 7))
+    assert max(block_rel(_np(gi.apply(x)), d["vcycle"], n)) <= TOL
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    res = P.gmres_solve(P.JacobianOperator(st), rhs,
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    assert res.converged and bool(d["gmres_conv"][0])
+    assert res.iterations == int(d["gmres_iters"][0])
+    assert max(block_rel(_np(res.solution), d["gmres_x"], n)) <= 1e-8
+    # the residual history follows the reference's to well below the tolerance
+    h_ref = d["gmres_hist"]
+    h_got = np.asarray(res.residual_history)
+    assert h_got.shape == h_ref.shape
+    assert np.max(np.abs(h_got - h_ref) / h_ref[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_level7_gmres_vs_oracle(split):
+    """The same solve against the oracle's GMRES + V-cycle (iterations equal,
+    solution <= 1e-8 per block)."""
+    nt = O.max_threads()
+    st, x = _state(7, split)
+    ost, _ = _oracle_state(7, split, nt)
+    n = st.n_scalar
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    og = O.Gmg(2, 7, coarse_level=2, cheb=O.ChebCfg(sweeps=3), nthreads=nt)
+    og.setup(ost)
+    res = P.gmres_solve(P.JacobianOperator(st), rhs,
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    ores = O.gmres(lambda v: O.apply_jacobian(ost, v, nt), rhs, tol=1e-8, restart=50,
+                   preconditioner=og.apply)
+    assert res.iterations == ores.iterations
+    assert max(block_rel(_np(res.solution), ores.solution, n)) <= 1e-8
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_level10_vcycle_vs_reference_and_oracle(split):
+    """configs[3] hierarchy (1024^2 Q2, 9 levels, every level >= 64^2 on the
+    sweep kernel with its fused Chebyshev / emit / last forms, the staged
+    restriction, the dense level-3 map): the ranges and the V-cycle against the
+    reference (sketch) and the whole V-cycle against oracle.Gmg, once with the
+    ranges estimated independently and once injected."""
+    d = load_golden(f"prod_p2_l10_{split}")
+    st, x = _state(10, split)
+    n = st.n_scalar
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    _check_ranges(gmg, d, 10)
+    z = _np(gmg.apply(torch.from_numpy(x).cuda()))
+    want = {k[len("vcycle_"):]: d[k] for k in d if k.startswith("vcycle_") and k != "vcycle_s"}
+    assert sketch_rel(sketch(z, n), want) <= TOL
+    nt = O.max_threads()
+    ost, _ = _oracle_state(10, split, nt)
+    og = O.Gmg(2, 10, coarse_level=2, cheb=O.ChebCfg(sweeps=3), nthreads=nt)
+    og.setup(ost, ranges=_ranges(d, 10))
+    zo = og.apply(x)
+    assert max(block_rel(z, zo, n)) <= TOL
+    assert sketch_rel(sketch(zo, n), want) <= TOL   # the oracle itself, at full size
+    gi = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gi.setup(st, ranges=_ranges(d, 10))
+    assert max(block_rel(_np(gi.apply(torch.from_numpy(x).cuda())), zo, n)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["pr1_miehe", "pr1_none"])
+def test_pr1_goldens_through_sweep_kernel(name):
+    """PR1 (32^2 Q2) is below the sweep kernel's default threshold; force the
+    sweep kernel onto it (PFF_OPT_SWEEP_MIN_NSIDE) and check the whole operator
+    family against the reference's vectors, plus the V-cycle golden at level 5
+    with every level >= 8^2 on the sweep kernel."""
+    d = load_golden(name)
+    split = "miehe" if int(d["meta"][3]) else "none"
+    _lib.set_option(_lib.OPT_SWEEP_MIN_NSIDE, 8)
+    try:
+        h = P.build_hierarchy(5, 2)
+        st = P.LinearizationState(h, 5, O.baseline_material(5), split=split)
+        st.set_solution(d["U"]); st.set_phi_tilde(d["phi_tilde"]); st.set_phi_old(d["phi_old"])
+        st.set_active(d["active"]); st.set_dirichlet_nodes(np.flatnonzero(d["dirichlet"]))
+        st.refresh_cache()
+        assert st.uses_sweep_kernel()
+        n, x = st.n_scalar, d["x"]
+        assert max(block_rel(_np(P.apply_jacobian(st, x)), d["jac"], n)) <= TOL
+        assert max(block_rel(_np(P.apply_block_uu(st, x[:2 * n])), d["uu"], n)) <= TOL
+        assert rel_l2(_np(P.apply_block_phiphi(st, x[2 * n:])), d["pp"]) <= TOL
+        assert rel_l2(_np(P.apply_phi_row(st, x)), d["prow"]) <= TOL
+        s = load_golden(f"solve_p2_l5_{split}_rand")
+        st2 = P.LinearizationState(h, 5, O.baseline_material(5), split=split)
+        st2.set_solution(s["U"]); st2.set_phi_tilde(s["phi_tilde"]); st2.set_phi_old(s["phi_old"])
+        st2.set_active(s["active"]); st2.set_dirichlet_nodes(np.flatnonzero(s["dirichlet"]))
+        st2.refresh_cache()
+        gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+        gmg.setup(st2)
+        assert max(block_rel(_np(gmg.apply(s["x"])), s["vcycle"], n)) <= TOL
+    finally:
+        _lib.set_option(_lib.OPT_SWEEP_MIN_NSIDE, 0)
+
+
+@pytest.mark.parametrize("level", [9, 10])
+def test_bound_transfers_vs_csr(level):
+    """The V-cycle's transfer kernels with both levels bound to states (the
+    restriction's element-vector scratch, its shared-memory-staged stores on
+    >= 256^2 coarse meshes, the 32-bit prolongation) against the oracle's CSR
+    P / P^T (src/multigrid.py:44-120), unmasked and masked."""
+    st, _ = _state(level, "miehe")
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    sf, sc = gmg.states[level], gmg.states[level - 1]
+    nf, nc = sf.n_scalar, sc.n_scalar
+    T = O.Transfer(2, level)
+    g = torch.Generator(device="cuda").manual_seed(level)
+    y = torch.rand(3 * nf, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    xc = torch.rand(3 * nc, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    yh, xh = y.cpu().numpy(), xc.cpu().numpy()
+    cons_f, cons_c = sf.constrained_mask(), sc.constrained_mask()
+    s = P.multigrid.stream_handle()
+    for zero_cons in (0, 1):
+        out = torch.empty(3 * nc, dtype=torch.float64, device="cuda")
+        _lib.call("pff_restrict", sf.bind(), sc.bind(), _lib.ptr(y), _lib.ptr(out), zero_cons, s)
+        want = T.restrict(yh)
+        if zero_cons:
+            want[cons_c] = 0.0
+        assert max(block_rel(out.cpu().numpy(), want, nc)) <= 1e-14
+    out = torch.empty(3 * nf, dtype=torch.float64, device="cuda")
+    _lib.call("pff_prolongate", sf.bind(), sc.bind(), _lib.ptr(xc), _lib.ptr(out), 0, s)
+    want = T.prolongate(xh)
+    assert max(block_rel(out.cpu().numpy(), want, nf)) <= 1e-14
+    base = torch.rand(3 * nf, dtype=torch.float64, device="cuda", generator=g)
+    out = base.clone()
+    _lib.call("pff_prolongate", sf.bind(), sc.bind(), _lib.ptr(xc), _lib.ptr(out), 1, s)
+    want = base.cpu().numpy() + np.where(cons_f, 0.0, T.prolongate(xh))
+    assert max(block_rel(out.cpu().numpy(), want, nf)) <= 1e-14
