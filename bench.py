@@ -44,6 +44,53 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def fp64_peak():
+    """Measured FP64 issue peak (tools/micro/dfma_peak.cu -> profiles/fp64_peak.json):
+    DFMA thread-instructions per second over the whole GPU."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["dfma_per_s"]), "measured (profiles/fp64_peak.json, tools/micro/dfma_peak.cu)"
+    except Exception:
+        return 148 * 64 * 1.965e9, "fallback (148 SMs x 64 FP64 lanes x 1.965 GHz)"
+
+
+def fp64_counts(tag):
+    """FP64 thread-instructions (DFMA + DADD + DMUL) per launch of each kernel of
+    one application, from the committed ncu capture (profiles/ncu_fp64.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fp64.json")) as f:
+            d = json.load(f)[tag]
+        return sum(v["fp64_thread_inst"] for v in d.values()), sum(v["dram_bytes"] for v in d.values())
+    except Exception:
+        return None, None
+
+
+def fp64_roof(tag, ms):
+    """FP64 pipe fraction of one application: its ncu-counted FP64 instructions
+    over its measured time, against the measured DFMA issue peak."""
+    inst, _ = fp64_counts(tag)
+    pk, src = fp64_peak()
+    if inst is None:
+        return None
+    ach = inst / (ms * 1e-3)
+    return {"bound": "fp64", "achieved": round(ach / 1e12, 3), "peak": round(pk / 1e12, 3),
+            "unit": "T FP64 inst/s", "frac": round(ach / pk, 4),
+            "inst_per_launch": inst, "peak_source": src,
+            "counted": "smsp__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on (ncu, "
+                       "profiles/ncu_fp64.json)"}
+
+
+def workload_config(args, ws):
+    """The `config` object of both arms (ours and --impl reference)."""
+    level, dofs = args.level, 3 * ((2 * 2 ** args.level + 1) ** 2 + 2 ** args.level)
+    return {"workload": f"configs[1]: {2 ** level}x{2 ** level} Q2 apply_jacobian, {dofs:,} DoFs",
+            "split": args.split, "degree": 2, "level": level, "dofs": dofs,
+            "l2": f"inputs larger than L2 ({27 * dofs / 1e6:.0f} MB per step), no flush",
+            "parallelism": f"cell-row slabs x{ws}, NCCL ghost-row exchange per step"
+                           if ws > 1 else "single GPU"}
+
+
 def baseline_inputs(p, level, split, seed=0, notch=False):
     """BASELINE.json synthetic draws: u0 ~ U[-1e-3,1e-3] (2n),
     phi0 ~ U[0,1] (n) or the notch profile, x ~ U[-1,1] (3n);
@@ -81,7 +128,7 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.h = nvml_handle(pynvml, index)
             self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception as e:   # pragma: no cover - no NVML
@@ -116,6 +163,18 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def nvml_handle(pynvml, device: int):
+    """NVML handle of CUDA device `device`, found by its PCI bus id: NVML's own
+    indices ignore CUDA_VISIBLE_DEVICES and CUDA's device order."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(device)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+    except Exception:
+        return pynvml.nvmlDeviceGetHandleByIndex(device)
 
 
 def dist_env():
@@ -221,39 +280,41 @@ def run_ours(args):
     # first-touched there); the affinity is restored before the CPU baseline
     aff0 = os.sched_getaffinity(0)
     local_cpus = gpu_local_cpus(local)
-    if local_cpus:
-        os.sched_setaffinity(0, local_cpus)
-    if ws == 1:
-        xh = torch.from_numpy(x).pin_memory()
-        for _ in range(3):            # warm the pinned-buffer cache with the timed loop's
-            yh = P.apply_jacobian(st, xh)   # pattern (previous result alive: two blocks)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            yh = P.apply_jacobian(st, xh)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-        h2d = d2h = 8 * dofs
-        # correctness of the timed output (bench never reports an unchecked number)
-        yref = P.apply_jacobian(st, xd)
-        assert torch.equal(yref, yd)
-        assert torch.equal(yh.to(dev), yd)
-    else:
-        xh = xd.cpu().pin_memory()
-        yh = torch.empty(yd.shape, dtype=torch.float64, pin_memory=True)
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            xd.copy_(xh, non_blocking=True)
-            st.apply_into(_lib.MODE_FULL, xd, yd)
-            yh.copy_(yd)
-        torch.cuda.synchronize()
-        t = torch.tensor([time.perf_counter() - t0], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item()) / e2e_steps
-        h2d = d2h = 8 * 3 * st.ln
-    os.sched_setaffinity(0, aff0)
+    try:
+        if local_cpus:
+            os.sched_setaffinity(0, local_cpus)
+        if ws == 1:
+            xh = torch.from_numpy(x).pin_memory()
+            for _ in range(3):            # warm the pinned-buffer cache with the timed loop's
+                yh = P.apply_jacobian(st, xh)   # pattern (previous result alive: two blocks)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                yh = P.apply_jacobian(st, xh)
+            torch.cuda.synchronize()
+            e2e_s = (time.perf_counter() - t0) / e2e_steps
+            h2d = d2h = 8 * dofs
+            # correctness of the timed output (bench never reports an unchecked number)
+            yref = P.apply_jacobian(st, xd)
+            assert torch.equal(yref, yd)
+            assert torch.equal(yh.to(dev), yd)
+        else:
+            xh = xd.cpu().pin_memory()
+            yh = torch.empty(yd.shape, dtype=torch.float64, pin_memory=True)
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                xd.copy_(xh, non_blocking=True)
+                st.apply_into(_lib.MODE_FULL, xd, yd)
+                yh.copy_(yd)
+            torch.cuda.synchronize()
+            t = torch.tensor([time.perf_counter() - t0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item()) / e2e_steps
+            h2d = d2h = 8 * 3 * st.ln
+    finally:
+        os.sched_setaffinity(0, aff0)
     # the other split's vmult on the same inputs (N=1; not the headline: the
     # reference default is Miehe), CUDA events over 200 applications
     other = None
@@ -282,6 +343,12 @@ def run_ours(args):
                  "steps": reps, "roofline_frac": round(BYTES_PER_DOF * ov / opk, 4),
                  "traffic": traffic_from_profiles(osp)}
         del so
+    q4 = None
+    if ws == 1 and args.q4:
+        try:
+            q4 = q4_section(args, P, torch, _lib, stream)
+        except Exception as e:   # reported, never silently dropped
+            q4 = {"error": f"{type(e).__name__}: {e}"}
     newton = None
     if args.newton:
         # the vmult state (tangent caches, vectors) is not needed any more: give its
@@ -293,6 +360,21 @@ def run_ours(args):
                       else newton_step_distributed(args, P, torch, ws, rank, dev))
         except Exception as e:   # reported, never silently dropped
             newton = {"error": f"{type(e).__name__}: {e}"}
+        if ws == 1 and rank == 0 and not args.no_cpu_baseline and isinstance(newton, dict) \
+                and "iterations" in newton:
+            newton["cpu_baseline"] = newton_cpu_baseline(args, newton["iterations"])
+    newton4 = None
+    if ws == 1 and args.configs4 and args.newton_level != 12:
+        # configs[4] (4096^2 Q2, 201 M DoFs) on this one GPU: the N=1 point of the
+        # scaling case (bench.py --gpus N runs it over N slabs)
+        release_device_memory(torch)
+        try:
+            a4 = argparse.Namespace(**vars(args))
+            a4.newton_level = 12
+            newton4 = newton_step_ours(a4, P, torch, warm_runs=False)
+        except Exception as e:
+            newton4 = {"error": f"{type(e).__name__}: {e}"}
+        release_device_memory(torch)
 
     if rank != 0:
         return
@@ -313,16 +395,13 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE.json configs[1] draws, seed 0)",
-        "config": {"workload": f"configs[1]: {2 ** level}x{2 ** level} Q2 apply_jacobian, "
-                               f"{dofs:,} DoFs",
-                   "split": args.split, "degree": p, "level": level, "dofs": dofs,
-                   "l2": f"inputs larger than L2 ({27 * dofs / 1e6:.0f} MB per step), no flush",
-                   "parallelism": f"cell-row slabs x{ws}, NCCL ghost-row exchange per step"
-                                  if ws > 1 else "single GPU"},
+        "config": workload_config(args, ws),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic_from_profiles(args.split),
-                     "algorithmic_bytes_per_dof": BYTES_PER_DOF, "peak_source": peak_src},
+                     "algorithmic_bytes_per_dof": BYTES_PER_DOF, "peak_source": peak_src,
+                     "fp64": fp64_roof(f"degree2level10split{args.split}", ms_step)
+                             if (ws == 1 and level == 10) else None},
         "e2e": {"value": round(dofs / e2e_s / 1e9, 4), "unit": "GDoF/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "host_cpus": (f"GPU-local NUMA node ({len(local_cpus)} CPUs)" if local_cpus
@@ -338,6 +417,10 @@ def run_ours(args):
         out["newton_step"] = newton
     if other is not None:
         out["other_split"] = other
+    if q4 is not None:
+        out["q4"] = q4
+    if newton4 is not None:
+        out["newton_step_configs4"] = newton4
     print(json.dumps(out))
 
 
@@ -348,7 +431,72 @@ def release_device_memory(torch):
     torch.cuda.empty_cache()
 
 
-def newton_step_ours(args, P, torch):
+def q4_section(args, P, torch, _lib, stream):
+    """configs[2]: the same operator on 512^2 Q4 cells (12.6 M DoFs, 5-point Gauss),
+    100 repeated applications per split (CUDA events), HBM fraction at the same
+    27 B/DoF and the FP64 pipe fraction from the ncu-counted FP64 instructions."""
+    level, p = 9, 4
+    out = {"config": "configs[2]: 512x512 Q4 apply_jacobian, 5-point Gauss", "reps": 100}
+    pk, _ = peaks()
+    for split in ("miehe", "none"):
+        h, params, U, pt, act, dirn, x = baseline_inputs(p, level, split, seed=0)
+        st = P.LinearizationState(h, level, params, split=split)
+        st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
+        st.set_dirichlet_nodes(dirn)
+        st.refresh_cache()
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        for _ in range(5):
+            st.apply_into(_lib.MODE_FULL, xd, yd)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(100):
+            st.apply_into(_lib.MODE_FULL, xd, yd)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 100
+        dofs = xd.numel()
+        v = dofs / (ms * 1e-3) / 1e9
+        _, traffic = fp64_counts(f"degree4level9split{split}")
+        out[split] = {"value": round(v, 3), "unit": "GDoF/s", "ms_per_step": round(ms, 5),
+                      "dofs": dofs, "hbm_frac": round(BYTES_PER_DOF * v / pk, 4),
+                      "traffic": traffic,
+                      "fp64": fp64_roof(f"degree4level9split{split}", ms)}
+        del st, xd, yd
+        release_device_memory(torch)
+    return out
+
+
+def newton_cpu_baseline(args, iterations, budget_iters=2):
+    """The Newton-step solve of configs[3] on the host cores with the C oracle
+    port (oracle/oracle.py Gmg + gmres, OpenMP cell kernels): the GMG setup
+    (Lanczos on every level) timed whole, then `budget_iters` GMRES iterations
+    timed; the total is projected to the GPU's iteration count (a bounded
+    sample: the whole solve would take minutes)."""
+    from oracle import oracle as O
+    nt = host_threads()
+    t0 = time.perf_counter()
+    ost, x = O.baseline_state(2, args.newton_level, args.split, seed=0, notch=True)
+    ost.refresh_cache(nthreads=nt)
+    og = O.Gmg(2, args.newton_level, coarse_level=2, cheb=O.ChebCfg(sweeps=3), nthreads=nt)
+    og.setup(ost)
+    t_setup = time.perf_counter() - t0
+    rhs = x.copy()
+    rhs[ost.constrained_mask()] = 0.0
+    t0 = time.perf_counter()
+    O.gmres(lambda v: O.apply_jacobian(ost, v, nt), rhs, tol=1e-8, restart=50,
+            max_iterations=budget_iters, preconditioner=og.apply)
+    t_it = (time.perf_counter() - t0) / budget_iters
+    return {"setup_s": round(t_setup, 2), "seconds_per_iteration": round(t_it, 3),
+            "projected_total_s": round(t_setup + iterations * t_it, 1),
+            "cores": nt, "kind": "port",
+            "sample": f"oracle Gmg.setup + {budget_iters} GMRES(50) iterations of configs[3] "
+                      f"({args.split}); total projected to {iterations} iterations (the early "
+                      "Arnoldi steps are the cheapest: MGS cost grows with j)"}
+
+
+def newton_step_ours(args, P, torch, warm_runs=True):
     """configs[3]: one Newton step's GMRES+GMG solve on 1024^2 Q2.  A fresh
     linearisation state (from host arrays) every time; the first solve (cold:
     module loads, first graph capture, allocations) is reported as cold_*, then
@@ -412,7 +560,8 @@ def newton_step_ours(args, P, torch):
     res, c_setup, c_gmres, t_dev = one()
     t_setup, t_gmres = c_setup, c_gmres
     release_device_memory(torch)
-    warm = 8 * n * (70 + 3 * 51) < 0.45 * torch.cuda.get_device_properties(0).total_memory
+    warm = warm_runs and \
+        8 * n * (70 + 3 * 51) < 0.45 * torch.cuda.get_device_properties(0).total_memory
     runs = []
     reuse_s = None
     if warm:
@@ -442,7 +591,8 @@ def newton_step_ours(args, P, torch):
         phases.clear()
         phases.update(mid_phases)
     roof = newton_floor(n, res.iterations, 1, t_dev)
-    return {"config": f"configs[3]: {2 ** level}^2 Q2 notch, levels 2..{level}, sweeps=3, "
+    cfg = "configs[3]" if level == 10 else ("configs[4]" if level == 12 else f"level {level}")
+    return {"config": f"{cfg}: {2 ** level}^2 Q2 notch, levels 2..{level}, sweeps=3, "
                       "restart 50, rtol 1e-8",
             "split": args.split, "iterations": res.iterations, "converged": res.converged,
             "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
@@ -545,7 +695,7 @@ def gpu_local_cpus(device: int):
         import pynvml
         pynvml.nvmlInit()
         try:
-            bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(device)).busId
+            bus = pynvml.nvmlDeviceGetPciInfo(nvml_handle(pynvml, device)).busId
         finally:
             pynvml.nvmlShutdown()
         bus = bus.decode() if isinstance(bus, bytes) else bus
@@ -598,8 +748,7 @@ def run_reference(args):
         "ms_per_step": round(1e3 * el / done, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json configs[1] draws)",
-        "config": {"workload": "configs[1]: 1024x1024 Q2 apply_jacobian, 12,598,275 DoFs",
-                   "split": args.split},
+        "config": workload_config(args, 1),
         "cpu_baseline": {"value": round(value, 5), "unit": "GDoF/s", "cores": nt, "kind": "port",
                          "sample": f"{done} full applications (capped at {budget:.0f} s)"},
         "e2e": {"value": round(value, 5), "unit": "GDoF/s", "h2d_bytes_per_step": 0,
@@ -618,13 +767,33 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--split", choices=["miehe", "none"], default="miehe")
     ap.add_argument("--no-newton", dest="newton", action="store_false")
-    ap.add_argument("--newton-level", type=int, default=10)
+    ap.add_argument("--newton-level", type=int, default=None,
+                    help="Newton-step mesh level (default: 10 = configs[3] at N=1, "
+                         "12 = configs[4] at N>1)")
+    ap.add_argument("--no-configs4", dest="configs4", action="store_false",
+                    help="N=1: skip the single configs[4] solve beside configs[3]")
+    ap.add_argument("--no-q4", dest="q4", action="store_false",
+                    help="N=1: skip the configs[2] (512^2 Q4) vmult object")
     ap.add_argument("--level", type=int, default=10, help="vmult mesh level (10 = configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-split", dest="other_split", action="store_false",
                     help="skip the other split's vmult (reported beside the headline)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: at least 3 warm-up steps
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch our own ranks (the driver may also start us
+        # under torchrun, in which case WORLD_SIZE is set and must match --gpus)
+        import subprocess
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={os.environ.get('MASTER_PORT', '29531')}",
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if ws != args.gpus and not (ws == 1 and args.gpus == 1):
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if args.newton_level is None:
+        args.newton_level = 12 if ws > 1 else 10
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -333,7 +333,14 @@ int pff_apply_host(const pff_level* h, int mode, const double* xh, double* yh, d
         return cudaMemcpy2DAsync(dst + a, pitch, src + a, pitch, (size_t)cnt * sizeof(double),
                                  (size_t)nc, cudaMemcpyDefault, s);
     };
-#define PFF_TRY(x) do { if ((e = (x)) != cudaSuccess) return check(e, "pff_apply_host"); } while (0)
+    // on a failure part-way, copies already queued on s_in / s_out still read xh /
+    // write yh and the device buffers: drain both copy streams before returning,
+    // so the caller may free or reuse every buffer once the error is reported
+    auto drain = [&]() {
+        cudaStreamSynchronize(s_in);
+        cudaStreamSynchronize(s_out);
+    };
+#define PFF_TRY(x) do { if ((e = (x)) != cudaSuccess) { drain(); return check(e, "pff_apply_host"); } } while (0)
     // the caller's earlier work on xd / yd / xh / yh comes first
     PFF_TRY(cudaEventRecord(ev_start, main));
     PFF_TRY(cudaStreamWaitEvent(s_in, ev_start, 0));
@@ -359,7 +366,10 @@ int pff_apply_host(const pff_level* h, int mode, const double* xh, double* yh, d
         PFF_TRY(cudaStreamWaitEvent(main, ev_in[k], 0));
         bool handled = false;
         PFF_TRY(pff::launch_sweep_apply_rows(*L, mode, xd, yd, nullptr, c0, c1, main, &handled));
-        if (!handled) return fail(PFF_E_ARG, "%s", "pff_apply_host: sweep kernel refused the rows");
+        if (!handled) {
+            drain();
+            return fail(PFF_E_ARG, "%s", "pff_apply_host: sweep kernel refused the rows");
+        }
         PFF_TRY(cudaEventRecord(ev_done[k], main));
         PFF_TRY(cudaStreamWaitEvent(s_out, ev_done[k], 0));
         const int64_t top = (int64_t)p * c1 + (c1 == ns ? 1 : 0);
