@@ -91,8 +91,20 @@ int pff_level_create(pff_level** out, int degree, int level, int split, const pf
         for (int a = 0; a < 3; ++a)   // mirror symmetry of the outer Gauss points
             ok = ok && near(S.N[2][a], S.N[0][2 - a], 1e-14) && near(S.D[2][a], -S.D[0][2 - a], 1e-13);
         L->q2_struct = ok;
-        L->min_nside = pff::sweep_min_nside();
     }
+    if (degree == 4) {   // mirror symmetry of the 5-point Gauss basis (even-odd form)
+        const auto& S = L->shape;
+        auto near = [](double a, double b, double tol) { return a - b <= tol && b - a <= tol; };
+        bool ok = near(S.D[2][2], 0.0, 1e-12);
+        for (int q = 0; q < 5; ++q) {
+            ok = ok && near(S.w[q], S.w[4 - q], 1e-15);
+            for (int a = 0; a < 5; ++a)
+                ok = ok && near(S.N[4 - q][4 - a], S.N[q][a], 1e-13) &&
+                     near(S.D[4 - q][4 - a], -S.D[q][a], 1e-12);
+        }
+        L->q4_struct = ok;
+    }
+    L->min_nside = pff::sweep_min_nside();
     L->miehe = split;
     *out = reinterpret_cast<pff_level*>(L);
     return 0;
@@ -145,7 +157,9 @@ int64_t pff_level_qcache_len(const pff_level* L) {
 }
 
 int pff_level_uses_sweep(const pff_level* L) {
-    return L ? (reinterpret_cast<const Level*>(L)->sweep_ok() ? 1 : 0) : -1;
+    if (!L) return -1;
+    const Level* V = reinterpret_cast<const Level*>(L);
+    return (V->sweep_ok() || V->sweep4_ok()) ? 1 : 0;
 }
 
 int pff_level_bind(pff_level* h, const double* U, const double* phi_tilde, const uint8_t* flags,

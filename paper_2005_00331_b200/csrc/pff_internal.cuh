@@ -117,7 +117,20 @@ struct Level {
         const int64_t cells = (local_cells() + cg - 1) / cg * cg;
         return !sweep_ok() ? gtan_arrays() * (int64_t)(mesh.p + 1) * (mesh.p + 1) * cells : 0;
     }
-    int64_t qcache_len() const { return generic_len() + tile_len() + gtan_len() + ev_len(); }
+    // Q4 sweep kernel (pff_sweep4.cu): strips of 6 cells (5 own + the left
+    // neighbour), per (strip, cell row) one tangent block [array][jq][cell][iq]
+    bool q4_struct = false;   // mirror-symmetric 5-point basis (even-odd contractions)
+    bool sweep4_ok() const {
+        return mesh.p == 4 && !windowed() && mesh.nside >= min_nside && q4_struct &&
+               mesh.n < (int64_t(1) << 31);
+    }
+    int n_strips4() const { return (mesh.nside + 4) / 5; }
+    int64_t tile4_block() const { return (int64_t)tile_nq() * 25 * 6; }
+    int64_t tile4_len() const { return sweep4_ok() ? (int64_t)n_strips4() * mesh.nside * tile4_block() : 0; }
+    int64_t qcache_len() const {
+        return generic_len() + tile_len() + gtan_len() + ev_len() + tile4_len();
+    }
+    double* qtile4() const { return ev() + ev_len(); }
     double* qtile() const { return qcache + generic_len(); }
     double* gtan() const { return qcache + generic_len() + tile_len(); }
     double* ev() const { return qcache + generic_len() + tile_len() + gtan_len(); }
@@ -223,6 +236,10 @@ void set_sweep_rows_per_chunk(int rows);
 
 // Q2 sweep kernel (pff_sweep.cu)
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s);
+// Q4 sweep kernel (pff_sweep4.cu)
+cudaError_t launch_refresh_tile4(const Level& L, cudaStream_t s);
+cudaError_t launch_sweep4_apply(const Level& L, int mode, const double* src, double* dst,
+                                const double* rhs, cudaStream_t s, bool* handled);
 cudaError_t launch_sweep_apply(const Level& L, int mode, const double* src, double* dst,
                                const double* rhs, cudaStream_t s, bool* handled,
                                const ChebArgs* cheb = nullptr);

@@ -754,6 +754,7 @@ struct ResidualL {
 cudaError_t launch_refresh(const Level& L, cudaStream_t s) {
     cudaError_t e = dispatch_p_split<RefreshL>(L.mesh.p, L.miehe, &L, s);
     if (e == cudaSuccess && L.sweep_ok()) e = launch_refresh_tiled(L, s);
+    if (e == cudaSuccess && L.sweep4_ok()) e = launch_refresh_tile4(L, s);
     return e;
 }
 
@@ -776,6 +777,10 @@ cudaError_t launch_apply(const Level& L, int mode, const double* src, double* ds
     if (!g_generic_apply) {
         cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled, cheb);
         if (handled || e != cudaSuccess) return e;
+        if (!cheb) {   // Q4 write-once sweep (plain and fused forms)
+            e = launch_sweep4_apply(L, mode, src, dst, rhs, s, &handled);
+            if (handled || e != cudaSuccess) return e;
+        }
     }
     return dispatch_p_split<ApplyL>(L.mesh.p, L.miehe, &L, mode, src, dst, rhs, s, cheb);
 }

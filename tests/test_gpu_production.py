@@ -218,3 +218,76 @@ def test_bound_transfers_vs_csr(level):
     _lib.call("pff_prolongate", sf.bind(), sc.bind(), _lib.ptr(xc), _lib.ptr(out), 1, s)
     want = base.cpu().numpy() + np.where(cons_f, 0.0, T.prolongate(xh))
     assert max(block_rel(out.cpu().numpy(), want, nf)) <= 1e-14
+
+
+# ------------------------------------------------------------ Q4 write-once sweep
+
+@pytest.mark.parametrize("name", ["op_p4_l3_miehe", "op_p4_l3_none"])
+def test_q4_goldens_through_sweep_kernel(name):
+    """The reference's p=4 operator goldens (8^2 Q4 cells) with the Q4 sweep
+    kernel forced onto that level (PFF_OPT_SWEEP_MIN_NSIDE)."""
+    d = load_golden(name)
+    split = "miehe" if int(d["meta"][3]) else "none"
+    _lib.set_option(_lib.OPT_SWEEP_MIN_NSIDE, 4)
+    try:
+        h = P.build_hierarchy(3, 4)
+        st = P.LinearizationState(h, 3, O.baseline_material(3), split=split)
+        st.set_solution(d["U"]); st.set_phi_tilde(d["phi_tilde"]); st.set_phi_old(d["phi_old"])
+        st.set_active(d["active"]); st.set_dirichlet_nodes(np.flatnonzero(d["dirichlet"]))
+        st.refresh_cache()
+        assert st.uses_sweep_kernel()
+        n, x = st.n_scalar, d["x"]
+        assert max(block_rel(_np(P.apply_jacobian(st, x)), d["jac"], n)) <= TOL
+        assert max(block_rel(_np(P.apply_block_uu(st, x[:2 * n])), d["uu"], n)) <= TOL
+        assert rel_l2(_np(P.apply_block_phiphi(st, x[2 * n:])), d["pp"]) <= TOL
+        assert rel_l2(_np(P.apply_phi_row(st, x)), d["prow"]) <= TOL
+    finally:
+        _lib.set_option(_lib.OPT_SWEEP_MIN_NSIDE, 0)
+
+
+@pytest.mark.parametrize("split", ["none", "miehe"])
+@pytest.mark.parametrize("level,rows", [(2, 0), (3, 1), (4, 3), (5, 0), (6, 7), (7, 0)])
+def test_q4_sweep_matches_generic_all_modes(split, level, rows, monkeypatch):
+    """The write-once Q4 kernel against the cooperative element-vector kernel
+    (k_apply_coop + k_apply_gather), every mode, plain and fused, with extra
+    active / Dirichlet nodes on the slit, over chunkings that put chunk edges
+    on and off the slit row; and bitwise repeatable."""
+    monkeypatch.setenv("PFF_SWEEP4_ROWS", str(rows))
+    ost, x = O.baseline_state(4, level, split, seed=level)
+    _lib.set_option(_lib.OPT_SWEEP_MIN_NSIDE, 4)
+    try:
+        h = P.build_hierarchy(max(level, 2), 4)
+        st = P.LinearizationState(h, level, ost.params, split=split)
+        st.set_solution(ost.U); st.set_phi_tilde(ost.phi_tilde); st.set_phi_old(ost.phi_old)
+        act = ost.active.copy()
+        act[np.random.default_rng(level).choice(st.n_scalar, 7, replace=False)] = True
+        dn = ost.dirichlet.copy()
+        dn[h.dof_map(level).slit_upper[:2]] = True
+        st.set_active(act)
+        st.set_dirichlet_nodes(np.flatnonzero(dn))
+        st.refresh_cache()
+        assert st.uses_sweep_kernel()
+    finally:
+        _lib.set_option(_lib.OPT_SWEEP_MIN_NSIDE, 0)
+    n = st.n_scalar
+    xd = torch.from_numpy(x).cuda()
+    rhs = torch.from_numpy(np.random.default_rng(1).standard_normal(3 * n)).cuda()
+    cases = [(0, xd, 3 * n), (1, xd[:2 * n], 2 * n), (2, xd[2 * n:], n), (3, xd, n)]
+    try:
+        for mode, src, nout in cases:
+            outs = []
+            for flag in (1, 0):
+                _lib.set_option(_lib.OPT_GENERIC_APPLY, flag)
+                y = torch.empty(nout, dtype=torch.float64, device="cuda")
+                st.apply_into(mode, src, y)
+                yf = torch.empty(nout, dtype=torch.float64, device="cuda")
+                st.apply_into(mode, src, yf, rhs[:nout])
+                outs.append((y.cpu().numpy(), yf.cpu().numpy()))
+            (g, gf), (s, sf) = outs
+            assert max(block_rel(s, g, n)) <= 1e-13, (mode, block_rel(s, g, n))
+            assert max(block_rel(sf, gf, n)) <= 1e-13, mode
+    finally:
+        _lib.set_option(_lib.OPT_GENERIC_APPLY, 0)
+    y1 = P.apply_jacobian(st, xd)
+    y2 = P.apply_jacobian(st, xd)
+    assert torch.equal(y1, y2)
