@@ -23,9 +23,9 @@ namespace {
 // level has < 2^31 nodes, and the per-direction weights are read once; the
 // sums keep the (my, mx) order and the |w| > 1e-14 filter of the reference's
 // CSR rows, so the result is the same bit for bit.
-template <int P, bool SMALL>
+template <int P, bool SMALL, bool WINC = false>
 __global__ void __launch_bounds__(256)
-k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
+k_prolong(Mesh mf, Win wf, Mesh mc, Win wc, Embed E, const double* __restrict__ xc,
           double* __restrict__ yf, const uint8_t* __restrict__ flags_f, int add_masked) {
     constexpr int N1 = P + 1;
     __shared__ double Es[2][N1][N1];
@@ -78,17 +78,22 @@ k_prolong(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ xc,
         wy[m] = Es[chy][b][m];
     }
     double acc[3] = {0.0, 0.0, 0.0};
-    const double* xk[3] = {xc, xc + mc.n, xc + 2 * mc.n};
+    // WINC: the coarse vector is a slab window's local vector (global id -> local)
+    const int64_t cn = WINC ? wc.n : mc.n;
+    const double* xk[3] = {xc, xc + cn, xc + 2 * cn};
     // coarse node of (mx, my) in the parent cell (Mesh::node; 32-bit when SMALL:
     // the coarse level is a quarter of the fine one)
     const bool cup = mc.level >= 1 && ccy >= (mc.nside >> 1);
     auto cnode = [&](int mx, int my) -> int64_t {
+        int64_t gc;
         if (SMALL) {
             const int jc = P * ccy + my, ic = P * ccx + mx;
             const int imc = (int)mc.i_mid;
-            return cup && jc == imc && ic < imc ? (int)mc.n_grid + ic : jc * (int)mc.np1 + ic;
+            gc = cup && jc == imc && ic < imc ? (int)mc.n_grid + ic : jc * (int)mc.np1 + ic;
+        } else {
+            gc = mc.node(ccx, ccy, mx, my);
         }
-        return mc.node(ccx, ccy, mx, my);
+        return WINC ? wc.loc(mc, gc) : gc;
     };
     // branch-free: a dropped weight (|w| <= 1e-14, multigrid.py:81-83) is an exact
     // zero, and fma(0, x, acc) == acc for finite x -- the same sums without the
@@ -137,10 +142,12 @@ __device__ __forceinline__ bool owned_fine(const Mesh& mf, const Win& wf, int64_
 
 // ev == nullptr: colour pass (col) adding into xc; otherwise one pass over the
 // cells of rows [col.cy0, col.cy0 + col.hy) writing element vectors ev[k][cell][my][mx]
+// (ev rows are relative to the coarse level's first q-point row crow0; nce =
+// the cells held there -- the whole mesh: 0 and n_cells)
 template <int P, bool STAGED = false>
 __global__ void __launch_bounds__(128)
 k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, double* xc,
-           CellColour col, double* __restrict__ ev) {
+           CellColour col, double* __restrict__ ev, int crow0 = 0, int64_t nce = 0) {
     constexpr bool staged = STAGED;
     constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -201,7 +208,7 @@ k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, dou
     }
     }
     if (ev && !staged) {
-        const int64_t nc = mc.n_cells(), cell = (int64_t)ccy * mc.nside + ccx;
+        const int64_t nc = nce, cell = (int64_t)(ccy - crow0) * mc.nside + ccx;
 #pragma unroll
         for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -217,9 +224,9 @@ k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, dou
         // memory and store them as one contiguous run -- coalesced, instead of
         // every store instruction touching 32 sectors QQ doubles apart
         __shared__ double sh[128 * QQ];
-        const int64_t nc = mc.n_cells(), tb = (int64_t)blockIdx.x * blockDim.x;
+        const int64_t nc = nce, tb = (int64_t)blockIdx.x * blockDim.x;
         const int nb = (int)(ntot - tb < 128 ? ntot - tb : 128);
-        const int64_t cell0 = (int64_t)col.cy0 * mc.nside + tb;
+        const int64_t cell0 = (int64_t)(col.cy0 - crow0) * mc.nside + tb;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             if (valid) {
@@ -255,7 +262,7 @@ k_restrict(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, dou
 template <int P>
 __global__ void __launch_bounds__(128)
 k_restrict_ev(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, int cy0, int hy,
-              double* __restrict__ ev) {
+              double* __restrict__ ev, int crow0, int64_t nce) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
     const int64_t ncw = (int64_t)mc.nside * hy;          // coarse cells of the window rows
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -292,7 +299,7 @@ k_restrict_ev(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, 
             }
         }
     }
-    const int64_t nc = mc.n_cells(), cell = (int64_t)ccy * mc.nside + ccx;
+    const int64_t nc = nce, cell = (int64_t)(ccy - crow0) * mc.nside + ccx;
     double* o = ev + ((int64_t)k * nc + cell) * QQ + my * N1;
 #pragma unroll
     for (int mx = 0; mx < N1; ++mx) o[mx] = acc[mx];
@@ -300,26 +307,32 @@ k_restrict_ev(Mesh mf, Win wf, Mesh mc, Embed E, const double* __restrict__ yf, 
 
 // coarse node gather of the element vectors (cell rows [lo, hi)), zeroing the
 // constrained rows when asked (src/multigrid.py:338)
-template <int P>
-__global__ void k_restrict_gather(Mesh mc, const double* __restrict__ ev, double* __restrict__ xc,
-                                  int lo, int hi, const uint8_t* __restrict__ flags, int zero_cons) {
+// (WINC: over the local nodes of a slab window wc -- its ghost rows included;
+// the top ghost row receives this rank's partial sums for the neighbour above)
+template <int P, bool WINC = false>
+__global__ void k_restrict_gather(Mesh mc, Win wc, const double* __restrict__ ev,
+                                  double* __restrict__ xc, int lo, int hi,
+                                  const uint8_t* __restrict__ flags, int zero_cons) {
     constexpr int N1 = P + 1, QQ = N1 * N1;
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= mc.n) return;
-    const int64_t nc = mc.n_cells();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nloc = WINC ? wc.n : mc.n;
+    if (t >= nloc) return;
+    const int64_t c = WINC ? (t < wc.dupl ? t + wc.shift : mc.n_grid + (t - wc.dupl)) : t;
+    const int64_t nc = WINC ? wc.ncell : mc.n_cells();
+    const int crow0 = WINC ? wc.row0 : 0;
     double acc[3] = {0.0, 0.0, 0.0};
     node_cells_p<P>(mc, c, lo, hi, [&](int cx, int cy, int a, int b) {
-        const int64_t cell = (int64_t)cy * mc.nside + cx;
+        const int64_t cell = (int64_t)(cy - crow0) * mc.nside + cx;
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc[k] += ev[((int64_t)k * nc + cell) * QQ + b * N1 + a];
     });
     if (zero_cons) {
-        const uint8_t f = flags[c];
+        const uint8_t f = flags[t];
         if (f & F_DIR) acc[0] = acc[1] = 0.0;
         if (f & F_ACT) acc[2] = 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) xc[k * mc.n + c] = acc[k];
+    for (int k = 0; k < 3; ++k) xc[k * nloc + t] = acc[k];
 }
 
 // rc[cons_c] = 0 (src/multigrid.py:338)
@@ -363,13 +376,18 @@ inline unsigned blocks(int64_t n) { return (unsigned)((n + 255) / 256); }
 cudaError_t launch_prolongate(const Level& F, const Level& C, const double* xc, double* yf,
                               int add_masked, cudaStream_t s) {
     if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
-    if (C.windowed()) return cudaErrorNotSupported;   // coarse side is always whole-mesh
-    const Win wf = F.win();
+    // a windowed coarse level (slab-to-slab V-cycle) holds the coarse cells of
+    // the fine window's owned rows: local coarse indices
+    if (C.windowed() && (!F.windowed() || F.cy_begin() != 2 * C.cy_begin() ||
+                         F.cy_end() != 2 * C.cy_end()))
+        return cudaErrorInvalidValue;
+    const Win wf = F.win(), wc = C.win();
     const int64_t nf = wf.n_owned(F.mesh);
     const bool small = F.mesh.n < (int64_t(1) << 31);
 #define PFF_PROLONG(PP)                                                                          \
-    (small ? k_prolong<PP, true> : k_prolong<PP, false>)<<<blocks(nf), 256, 0, s>>>(             \
-        F.mesh, wf, C.mesh, F.embed, xc, yf, F.flags, add_masked)
+    (C.windowed() ? (small ? k_prolong<PP, true, true> : k_prolong<PP, false, true>)             \
+                  : (small ? k_prolong<PP, true> : k_prolong<PP, false>))<<<blocks(nf), 256, 0, s>>>( \
+        F.mesh, wf, C.mesh, wc, F.embed, xc, yf, F.flags, add_masked)
     switch (F.mesh.p) {
         case 1: PFF_PROLONG(1); break;
         case 2: PFF_PROLONG(2); break;
@@ -385,13 +403,19 @@ cudaError_t launch_prolongate(const Level& F, const Level& C, const double* xc, 
 cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, double* xc,
                             int zero_cons, cudaStream_t s) {
     if (F.mesh.p != C.mesh.p || F.mesh.level != C.mesh.level + 1) return cudaErrorInvalidValue;
-    if (C.windowed()) return cudaErrorNotSupported;
-    const Win wf = F.win();
-    // coarse cell rows owning the window's fine rows (fine cell rows cyb-1 .. cye)
+    const bool winc = C.windowed();
+    if (winc && (!F.windowed() || F.cy_begin() != 2 * C.cy_begin() || F.cy_end() != 2 * C.cy_end() ||
+                 !C.qcache))
+        return cudaErrorInvalidValue;
+    const Win wf = F.win(), wc = C.win();
+    // coarse cell rows owning the window's fine rows (fine cell rows cyb-1 .. cye);
+    // a coarse window holds exactly rows [q_row0, cy_end) of them
     const int nsc = C.mesh.nside;
     const int cyb = F.cy_begin(), cye = F.cy_end();
     const int lo = cyb > 0 ? (cyb - 1) / 2 : 0;
-    const int hi = (cye / 2 + 1) < nsc ? cye / 2 + 1 : nsc;
+    const int hi = winc ? C.cy_end() : ((cye / 2 + 1) < nsc ? cye / 2 + 1 : nsc);
+    const int crow0 = winc ? C.q_row0() : 0;
+    const int64_t nce = winc ? C.local_cells() : C.mesh.n_cells();
     if (zero_cons && !C.flags) return cudaErrorInvalidValue;
     if (C.qcache) {   // element vectors in the coarse level's scratch + node gather
         CellColour all;
@@ -411,26 +435,30 @@ cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, do
         const unsigned g = (unsigned)((nthr + 127) / 128);
         if (!split) {
             switch (F.mesh.p) {
-                case 1: (staged ? k_restrict<1, true> : k_restrict<1, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
-                case 2: (staged ? k_restrict<2, true> : k_restrict<2, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
-                case 3: (staged ? k_restrict<3, true> : k_restrict<3, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
-                case 4: (staged ? k_restrict<4, true> : k_restrict<4, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev); break;
+                case 1: (staged ? k_restrict<1, true> : k_restrict<1, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev, crow0, nce); break;
+                case 2: (staged ? k_restrict<2, true> : k_restrict<2, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev, crow0, nce); break;
+                case 3: (staged ? k_restrict<3, true> : k_restrict<3, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev, crow0, nce); break;
+                case 4: (staged ? k_restrict<4, true> : k_restrict<4, false>)<<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, xc, all, ev, crow0, nce); break;
                 default: return cudaErrorInvalidValue;
             }
         } else switch (F.mesh.p) {
-            case 1: k_restrict_ev<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
-            case 2: k_restrict_ev<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
-            case 3: k_restrict_ev<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
-            case 4: k_restrict_ev<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev); break;
+            case 1: k_restrict_ev<1><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev, crow0, nce); break;
+            case 2: k_restrict_ev<2><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev, crow0, nce); break;
+            case 3: k_restrict_ev<3><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev, crow0, nce); break;
+            case 4: k_restrict_ev<4><<<g, 128, 0, s>>>(F.mesh, wf, C.mesh, F.embed, yf, all.cy0, all.hy, ev, crow0, nce); break;
             default: return cudaErrorInvalidValue;
         }
-        const unsigned gn = blocks(C.mesh.n);
+        const unsigned gn = blocks(winc ? wc.n : C.mesh.n);
+#define PFF_GATHER(PP)                                                                           \
+    (winc ? k_restrict_gather<PP, true> : k_restrict_gather<PP>)<<<gn, 256, 0, s>>>(             \
+        C.mesh, wc, ev, xc, lo, hi, C.flags, zero_cons)
         switch (F.mesh.p) {
-            case 1: k_restrict_gather<1><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
-            case 2: k_restrict_gather<2><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
-            case 3: k_restrict_gather<3><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
-            case 4: k_restrict_gather<4><<<gn, 256, 0, s>>>(C.mesh, ev, xc, lo, hi, C.flags, zero_cons); break;
+            case 1: PFF_GATHER(1); break;
+            case 2: PFF_GATHER(2); break;
+            case 3: PFF_GATHER(3); break;
+            case 4: PFF_GATHER(4); break;
         }
+#undef PFF_GATHER
         count_launches(2);
         return cudaGetLastError();
     }

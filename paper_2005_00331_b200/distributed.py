@@ -1,15 +1,17 @@
 """Multi-GPU Newton-step solve: GMRES + GMG over cell-row slabs.
 
-* Finest level: slab-partitioned (``parallel.SlabState``): operator family with
-  NCCL ghost-row exchange, both block diagonals, Lanczos ranges (dots
-  all-reduced, start vectors drawn globally with the reference's seeds, so the
-  ranges equal the single-GPU ones up to rounding), Chebyshev smoothing.
-* Restriction: every rank restricts its owned fine rows into a whole-mesh
-  coarse vector; one all-reduce sums the partials (= the exact P^T).
-* Coarser levels (ell-1 ... coarse_level): agglomerated -- every rank runs the
-  single-GPU V-cycle of ``multigrid.GmgPreconditioner`` redundantly on the
-  whole coarse mesh (1/4 of the fine work per level), then prolongates into
-  its own fine rows.  Same algebra as src/multigrid.py:330-344.
+* Slab levels (the finest and every coarser level with >= 16 cell rows per
+  rank): ``parallel.SlabState`` operator family with NCCL ghost-row exchange,
+  both block diagonals, Lanczos ranges (dots all-reduced, start vectors drawn
+  globally with the reference's seeds, so the ranges equal the single-GPU ones
+  up to rounding), Chebyshev smoothing.
+* Slab -> slab transfers: the restriction writes the coarse window and one
+  reverse ghost-row message per neighbour completes the exact P^T; the
+  prolongation reads the coarse window after a ghost-row exchange.
+* Below the last slab level: agglomerated -- the restriction sums whole-mesh
+  partial vectors with one all-reduce and every rank runs the single-GPU
+  V-cycle of ``multigrid.GmgPreconditioner`` on that small level, then
+  prolongates into its own rows.  Same algebra as src/multigrid.py:330-344.
 * GMRES: right-preconditioned, restarted, reference Givens/back-substitution
   (src/krylov.py:37-119) with CGS2 orthogonalisation: two batched multi-dots
   (``pff_mdot``) and all-reduces per iteration instead of j+1 sequential MGS
@@ -49,16 +51,40 @@ class _Comm:
         return t
 
 
+class _SlabLevel:
+    """One slab level of the distributed V-cycle: window state, inverse block
+    diagonals (zero off the owned rows), Chebyshev ranges and work vectors."""
+
+    def __init__(self, part: SlabPartition, state: SlabState):
+        self.part, self.st = part, state
+        self.level = part.level
+
+
 class DistributedGmg:
-    """V-cycle with the finest level in slabs and agglomerated coarse levels."""
+    """V-cycle over cell-row slabs on every level with at least ``min_rows``
+    cell rows per rank (and >= 64^2 cells: the slab kernel is the Q2 sweep),
+    agglomerated below that.
+
+    Slab levels: operator family with ghost-row exchange, both block diagonals,
+    Lanczos ranges with the reference's seeded global start vectors (so the
+    ranges equal the single-GPU ones up to rounding), Chebyshev smoothing.
+    Slab -> slab transfers are local: the restriction writes the coarse
+    window (its top ghost row gets this rank's partial sums, which one reverse
+    ghost-row message adds into the next rank's bottom owned row), the
+    prolongation reads the coarse window after a ghost-row exchange.  Below
+    the last slab level the restriction sums whole-mesh partial vectors with
+    one all-reduce and every rank runs the single-GPU CUDA-graph V-cycle of
+    ``GmgPreconditioner`` on that (small) level.  Same algebra as
+    src/multigrid.py:330-344; the paper's distributed setting assigns each
+    rank its part of every level.
+    """
 
     def __init__(self, hierarchy: MeshHierarchy, level: int, rank: int, world: int,
                  coarse_level: int = 2, cheb: ChebyshevConfig | None = None, group=None,
-                 device=None):
+                 device=None, min_rows: int = 16, max_slab_levels: int | None = None):
         if level - 1 < coarse_level:
             raise ValueError("need at least one level between the slab level and the coarse level")
-        self.h, self.level, self.rank = hierarchy, level, rank
-        self.part = SlabPartition(hierarchy.degree, level, world)
+        self.h, self.level, self.rank, self.world = hierarchy, level, rank, world
         self.comm = _Comm(world, group)
         self.group = group
         self.cheb = cheb or ChebyshevConfig()
@@ -67,10 +93,28 @@ class DistributedGmg:
         self._scratch = torch.empty(_lib.load().pff_reduce_scratch_len(), dtype=torch.float64,
                                     device=self.device)
         self._dout = torch.empty(4, dtype=torch.float64, device=self.device)
+        # slab levels: the finest always; coarser ones while each rank keeps
+        # >= min_rows cell rows, the mesh stays on the sweep kernel (>= 64^2)
+        # and a level remains below for the agglomerated V-cycle
+        levels = [level]
+        while True:
+            l = levels[-1] - 1
+            if max_slab_levels is not None and len(levels) >= max_slab_levels:
+                break
+            if l - 1 < coarse_level or 2 ** l < 64 or 2 ** l // world < max(min_rows, 2):
+                break
+            levels.append(l)
+        self.slab_levels = levels
+        self.agg_level = levels[-1] - 1
+        self.part = SlabPartition(hierarchy.degree, level, world)
+
+    @property
+    def fine(self) -> SlabState:
+        return self.lv[0].st
 
     # -- vectors ----------------------------------------------------------------
-    def _owned(self, ncomp: int) -> torch.Tensor:
-        own = self.part.owned_mask(self.rank)
+    def _owned(self, part: SlabPartition, ncomp: int) -> torch.Tensor:
+        own = part.owned_mask(self.rank)
         return torch.from_numpy(np.tile(own, ncomp)).to(self.device)
 
     def dot(self, x: torch.Tensor, y: torch.Tensor) -> float:
@@ -83,50 +127,64 @@ class DistributedGmg:
 
     # -- setup -------------------------------------------------------------------
     def setup(self, params, split, U, phi_tilde, phi_old, active, dirichlet):
-        """Global host arrays of the finest linearisation point (every rank)."""
-        part, rank = self.part, self.rank
-        self.fine = SlabState(part, rank, params, split, U, phi_tilde, active, dirichlet,
-                              device=self.device, group=self.group)
-        self.fine.refresh_cache()
-        ln = self.fine.ln
-        duu = torch.empty(2 * ln, dtype=torch.float64, device=self.device)
-        dpp = torch.empty(ln, dtype=torch.float64, device=self.device)
-        call("pff_diagonal", self.fine.handle(), ptr(duu), ptr(dpp), 0, stream_handle())
-        own1, own2 = self._owned(1), self._owned(2)
-        zero = torch.zeros((), dtype=torch.float64, device=self.device)
-        self.diag = {"uu": torch.where(own2, duu, zero), "phiphi": torch.where(own1, dpp, zero)}
-        self.inv = {k: torch.where(self._owned(2 if k == "uu" else 1), 1.0 / torch.where(
-            d == 0, torch.ones_like(d), d), zero) for k, d in self.diag.items()}
-        self.ranges = {"uu": self._lanczos(_lib.MODE_UU, "uu", 0),
-                       "phiphi": self._lanczos(_lib.MODE_PHIPHI, "phiphi", 1)}
-        # agglomerated coarse hierarchy: the whole level ell-1 on every rank
-        inj = self.h.injection(self.level)
-        n = part.n
-        coarse = LinearizationState(self.h, self.level - 1, params, split=split)
-        coarse.set_solution(np.concatenate([np.asarray(U)[k * n:(k + 1) * n][inj] for k in range(3)]))
-        coarse.set_phi_tilde(np.asarray(phi_tilde)[inj])
-        coarse.set_phi_old(np.asarray(phi_old)[inj])
-        coarse.set_active(np.asarray(active)[inj])
-        coarse._dir.set(torch.from_numpy(np.asarray(dirichlet)[inj]).to(self.device))
+        """Global host arrays of the finest linearisation point (every rank);
+        the coarser states are injected level by level (src/pff_operator.py:380-400)."""
+        rank, h = self.rank, self.h
+        U, pt, po = np.asarray(U), np.asarray(phi_tilde), np.asarray(phi_old)
+        act, dirn = np.asarray(active), np.asarray(dirichlet)
+        self.lv = []
+        for k, l in enumerate(self.slab_levels + [self.agg_level]):
+            if k > 0:   # inject the global state one level down
+                inj = h.injection(l + 1)
+                n = h.dof_map(l + 1).n_scalar
+                U = np.concatenate([U[c * n:(c + 1) * n][inj] for c in range(3)])
+                pt, po, act, dirn = pt[inj], po[inj], act[inj], dirn[inj]
+            if l == self.agg_level:
+                break
+            part = SlabPartition(h.degree, l, self.world)
+            st = SlabState(part, rank, params, split, U, pt, act, dirn, device=self.device,
+                           group=self.group)
+            st.refresh_cache()
+            L = _SlabLevel(part, st)
+            ln = st.ln
+            duu = torch.empty(2 * ln, dtype=torch.float64, device=self.device)
+            dpp = torch.empty(ln, dtype=torch.float64, device=self.device)
+            call("pff_diagonal", st.handle(), ptr(duu), ptr(dpp), 0, stream_handle())
+            own1, own2 = self._owned(part, 1), self._owned(part, 2)
+            zero = torch.zeros((), dtype=torch.float64, device=self.device)
+            L.diag = {"uu": torch.where(own2, duu, zero), "phiphi": torch.where(own1, dpp, zero)}
+            L.inv = {k2: torch.where(self._owned(part, 2 if k2 == "uu" else 1), 1.0 / torch.where(
+                d == 0, torch.ones_like(d), d), zero) for k2, d in L.diag.items()}
+            z = lambda m: torch.zeros(m * ln, dtype=torch.float64, device=self.device)  # noqa: E731
+            L.w = dict(res=z(3), resphi=z(1), d=z(2), acc=z(2), cr=z(2), r=z(3), z=z(3))
+            self.lv.append(L)
+            L.ranges = {"uu": self._lanczos(L, _lib.MODE_UU, "uu", 0),
+                        "phiphi": self._lanczos(L, _lib.MODE_PHIPHI, "phiphi", 1)}
+        # agglomerated hierarchy below the last slab level: the whole mesh on every rank
+        coarse = LinearizationState(h, self.agg_level, params, split=split)
+        coarse.set_solution(U)
+        coarse.set_phi_tilde(pt)
+        coarse.set_phi_old(po)
+        coarse.set_active(act)
+        coarse._dir.set(torch.from_numpy(dirn).to(self.device))
         coarse.refresh_cache()
         self.coarse_state = coarse
-        self.cgmg = GmgPreconditioner(self.h, coarse_level=self.coarse_level, cheb=self.cheb)
+        self.cgmg = GmgPreconditioner(h, coarse_level=self.coarse_level, cheb=self.cheb)
         self.cgmg.setup(coarse)
-        # work vectors (ghost rows stay zero)
-        z = lambda k: torch.zeros(k * ln, dtype=torch.float64, device=self.device)  # noqa: E731
-        self.w = dict(res=z(3), resphi=z(1), d=z(2), acc=z(2), cr=z(2), z=z(3))
         self.rc = torch.zeros(3 * coarse.n_scalar, dtype=torch.float64, device=self.device)
+        self.ranges = self.lv[0].ranges
+        self.diag, self.inv, self.w = self.lv[0].diag, self.lv[0].inv, self.lv[0].w
 
-    def _lanczos(self, mode, block, blk_index):
+    def _lanczos(self, L: _SlabLevel, mode, block, blk_index):
         """estimate_lambda_range (src/multigrid.py:123-162) on the slab."""
-        cfg, part = self.cheb, self.part
-        diag = self.diag[block]
+        cfg, part = self.cheb, L.part
+        diag = L.diag[block]
         ncomp = _NCOMP[mode] if mode != _lib.MODE_PHIROW else 1
-        own = self._owned(ncomp)
+        own = self._owned(part, ncomp)
         zero = torch.zeros((), dtype=torch.float64, device=self.device)
         dhalf = torch.where(own, 1.0 / torch.sqrt(torch.where(diag > 0, diag, torch.ones_like(diag))), zero)
         nglob = ncomp * part.n
-        seed = cfg.seed + 101 * self.level + blk_index
+        seed = cfg.seed + 101 * L.level + blk_index
         v_h = np.random.default_rng(seed).standard_normal(nglob)
         v_h /= np.linalg.norm(v_h)
         v = torch.from_numpy(part.scatter(v_h, self.rank, ncomp)).to(self.device) * own
@@ -139,8 +197,8 @@ class DistributedGmg:
         prev = None
         for _ in range(min(cfg.lanczos_iterations, nglob)):
             torch.mul(dhalf, v, out=tmp)
-            self.fine.apply_into(mode, tmp, w)
-            self.fine.halo.zero_ghosts(tmp, ncomp)
+            L.st.apply_into(mode, tmp, w)
+            L.st.halo.zero_ghosts(tmp, ncomp)
             w.mul_(dhalf)
             self._axpby(-beta, v_prev, 1.0, w)
             alpha = self.dot(v, w)
@@ -162,17 +220,17 @@ class DistributedGmg:
         return lo, hi
 
     # -- V-cycle -------------------------------------------------------------------
-    def _cheb(self, mode, rhs, a, b, sweeps, out):
+    def _cheb(self, L: _SlabLevel, mode, rhs, a, b, sweeps, out):
         block = "uu" if mode == _lib.MODE_UU else "phiphi"
-        inv = self.inv[block]
+        inv = L.inv[block]
         nb = rhs.numel()
-        d, cr, acc = self.w["d"][:nb], self.w["cr"][:nb], self.w["acc"][:nb]
+        d, cr, acc = L.w["d"][:nb], L.w["cr"][:nb], L.w["acc"][:nb]
         theta, delta = 0.5 * (b + a), 0.5 * (b - a)
         sigma1 = theta / delta
         st = stream_handle()
         call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0, st)
         if sweeps > 1:
-            self.fine.apply_into(mode, d, cr, rhs)
+            L.st.apply_into(mode, d, cr, rhs)
             rho_old = 1.0 / sigma1
             for k in range(1, sweeps):
                 rho = 1.0 / (2.0 * sigma1 - rho_old)
@@ -180,41 +238,57 @@ class DistributedGmg:
                      ptr(d), ptr(acc), st)
                 rho_old = rho
                 if k < sweeps - 1:
-                    self.fine.apply_into(mode, d, cr, cr)
+                    L.st.apply_into(mode, d, cr, cr)
         self._axpby(1.0, acc, 1.0, out)
 
-    def _smooth(self, z, r, first=False):
-        ln, W, c = self.fine.ln, self.w, self.cheb
+    def _smooth(self, L: _SlabLevel, z, r, first=False):
+        ln, W, c = L.st.ln, L.w, self.cheb
         if first:   # z = SELECT(r): the residual is r with constrained rows zeroed
-            call("pff_cons", self.fine.handle(), _lib.LAYOUT_FULL, _lib.CONS_EXCLUDE, ptr(r),
+            call("pff_cons", L.st.handle(), _lib.LAYOUT_FULL, _lib.CONS_EXCLUDE, ptr(r),
                  ptr(W["res"]), stream_handle())
         else:
-            self.fine.apply_into(_lib.MODE_FULL, z, W["res"], r)
-        hi = self.ranges["uu"][1]
-        self._cheb(_lib.MODE_UU, W["res"][:2 * ln], c.c * hi, c.C * hi, c.sweeps, z[:2 * ln])
-        self.fine.apply_into(_lib.MODE_PHIROW, z, W["resphi"], r[2 * ln:])
-        hi = self.ranges["phiphi"][1]
-        self._cheb(_lib.MODE_PHIPHI, W["resphi"], c.c * hi, c.C * hi, c.sweeps, z[2 * ln:])
+            L.st.apply_into(_lib.MODE_FULL, z, W["res"], r)
+        hi = L.ranges["uu"][1]
+        self._cheb(L, _lib.MODE_UU, W["res"][:2 * ln], c.c * hi, c.C * hi, c.sweeps, z[:2 * ln])
+        L.st.apply_into(_lib.MODE_PHIROW, z, W["resphi"], r[2 * ln:])
+        hi = L.ranges["phiphi"][1]
+        self._cheb(L, _lib.MODE_PHIPHI, W["resphi"], c.c * hi, c.C * hi, c.sweeps, z[2 * ln:])
+
+    def _vcycle(self, k: int, r: torch.Tensor, z: torch.Tensor):
+        L = self.lv[k]
+        st = stream_handle()
+        fh = L.st.handle()
+        call("pff_cons", fh, _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
+        self._smooth(L, z, r, first=True)
+        res = L.w["res"]
+        L.st.apply_into(_lib.MODE_FULL, z, res, r)
+        if k + 1 < len(self.lv):   # slab -> slab
+            C = self.lv[k + 1]
+            ch = C.st.handle()
+            rc, zc = C.w["r"], C.w["z"]
+            call("pff_restrict", fh, ch, ptr(res), ptr(rc), 0, st)
+            C.st.halo.reverse_add(rc, 3)
+            call("pff_cons", ch, _lib.LAYOUT_FULL, _lib.CONS_ZERO, None, ptr(rc), st)
+            self._vcycle(k + 1, rc, zc)
+            C.st.halo.exchange(zc, 3)   # the coarse ghost rows the prolongation reads
+            call("pff_prolongate", fh, ch, ptr(zc), ptr(z), 1, st)
+        else:   # slab -> agglomerated whole mesh
+            ch = self.coarse_state.bind()
+            call("pff_restrict", fh, ch, ptr(res), ptr(self.rc), 0, st)
+            self.comm.sum_(self.rc)
+            call("pff_cons", ch, _lib.LAYOUT_FULL, _lib.CONS_ZERO, None, ptr(self.rc), st)
+            r_top, z_top = self.cgmg.io_buffers()
+            r_top.copy_(self.rc)
+            self.cgmg.run_cycle()
+            call("pff_prolongate", fh, ch, ptr(z_top), ptr(z), 1, st)
+        self._smooth(L, z, r)
+        L.st.halo.zero_ghosts(z, 3)
+        return z
 
     def apply_into(self, r: torch.Tensor, z: torch.Tensor):
-        """z = V-cycle(r) on local slab vectors (src/multigrid.py:330-344)."""
-        st = stream_handle()
-        fh = self.fine.handle()
-        call("pff_cons", fh, _lib.LAYOUT_FULL, _lib.CONS_SELECT, ptr(r), ptr(z), st)
-        self._smooth(z, r, first=True)
-        res = self.w["res"]
-        self.fine.apply_into(_lib.MODE_FULL, z, res, r)
-        ch = self.coarse_state.bind()
-        call("pff_restrict", fh, ch, ptr(res), ptr(self.rc), 0, st)
-        self.comm.sum_(self.rc)
-        call("pff_cons", ch, _lib.LAYOUT_FULL, _lib.CONS_ZERO, None, ptr(self.rc), st)
-        r_top, z_top = self.cgmg.io_buffers()
-        r_top.copy_(self.rc)
-        self.cgmg.run_cycle()
-        call("pff_prolongate", fh, ch, ptr(z_top), ptr(z), 1, st)
-        self._smooth(z, r)
-        self.fine.halo.zero_ghosts(z, 3)
-        return z
+        """z = V-cycle(r) on local slab vectors of the finest level
+        (src/multigrid.py:330-344)."""
+        return self._vcycle(0, r, z)
 
     def __call__(self, r):
         z = torch.zeros_like(r)

@@ -171,18 +171,24 @@ class HaloExchange:
         return (self.part.world > 1 and vec.is_cuda
                 and dist.get_backend(self.group) != "gloo")
 
-    def start(self, vec: torch.Tensor, ncomp: int):
-        """Post the ghost-row sends/receives (NCCL); returns the work handles.
-        ``wait()`` on them orders the current stream after the transfers."""
-        ops = []
-        for c in range(ncomp):
-            for peer, a, b in self.recvs:
-                ops.append(dist.P2POp(dist.irecv, self._view(vec, c, a, b), peer, self.group))
-            for peer, a, b in self.sends:
-                ops.append(dist.P2POp(dist.isend, self._view(vec, c, a, b), peer, self.group))
-        return dist.batch_isend_irecv(ops) if ops else []
+    def start(self, vec: torch.Tensor, ncomp: int) -> "_PendingHalo":
+        """Post the ghost-row sends/receives (NCCL), one packed message per
+        neighbour and direction; ``wait()`` on the result orders the current
+        stream after the transfers and unpacks the ghost rows."""
+        ops, unpack = [], []
+        for peer, a, b in self.recvs:
+            buf = torch.empty(ncomp * (b - a) * self.np1, dtype=vec.dtype, device=vec.device)
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            unpack.append((buf, a, b))
+        for peer, a, b in self.sends:
+            buf = torch.cat([self._view(vec, c, a, b) for c in range(ncomp)])
+            ops.append(dist.P2POp(dist.isend, buf, peer, self.group))
+        return _PendingHalo(dist.batch_isend_irecv(ops) if ops else [], unpack, self, vec, ncomp)
 
     def exchange(self, vec: torch.Tensor, ncomp: int):
+        """Ghost rows <- the neighbours' owned rows.  One message per neighbour
+        and direction: the rows of all ``ncomp`` components are packed into one
+        contiguous buffer."""
         if self.part.world == 1:
             return
         if vec.is_cuda and dist.get_backend(self.group) == "gloo":
@@ -190,15 +196,63 @@ class HaloExchange:
             self.exchange(host, ncomp)
             vec.copy_(host)
             return
-        ops = []
-        for c in range(ncomp):
-            for peer, a, b in self.recvs:
-                ops.append(dist.P2POp(dist.irecv, self._view(vec, c, a, b), peer, self.group))
-            for peer, a, b in self.sends:
-                ops.append(dist.P2POp(dist.isend, self._view(vec, c, a, b).contiguous(), peer,
-                                      self.group))
+        ops, unpack = [], []
+        for peer, a, b in self.recvs:
+            buf = torch.empty(ncomp * (b - a) * self.np1, dtype=vec.dtype, device=vec.device)
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            unpack.append((buf, a, b))
+        for peer, a, b in self.sends:
+            buf = torch.cat([self._view(vec, c, a, b) for c in range(ncomp)])
+            ops.append(dist.P2POp(dist.isend, buf, peer, self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        for buf, a, b in unpack:
+            w = (b - a) * self.np1
+            for c in range(ncomp):
+                self._view(vec, c, a, b).copy_(buf[c * w:(c + 1) * w])
+
+    def reverse_add(self, vec: torch.Tensor, ncomp: int):
+        """Reverse ghost-row sum of a slab-to-slab restriction: the partial
+        sums this rank computed for its top ghost row (the next rank's bottom
+        owned row) go up and are added there, in one message per neighbour;
+        the ghost rows are zeroed afterwards."""
+        part, rank = self.part, self.rank
+        if part.world == 1:
+            return
+        if vec.is_cuda and dist.get_backend(self.group) == "gloo":
+            host = vec.cpu()
+            self.reverse_add(host, ncomp)
+            vec.copy_(host)
+            return
+        lo, hi = part.rows(rank)
+        olo, _ = part.own_rows(rank)
+        ops = []
+        recv = None
+        if rank > 0:
+            recv = torch.empty(ncomp * self.np1, dtype=vec.dtype, device=vec.device)
+            ops.append(dist.P2POp(dist.irecv, recv, rank - 1, self.group))
+        if rank < part.world - 1:
+            send = torch.cat([self._view(vec, c, hi, hi + 1) for c in range(ncomp)])
+            ops.append(dist.P2POp(dist.isend, send, rank + 1, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if recv is not None:
+            for c in range(ncomp):
+                self._view(vec, c, olo, olo + 1).add_(recv[c * self.np1:(c + 1) * self.np1])
+        self.zero_ghosts(vec, ncomp)
+
+
+class _PendingHalo:
+    def __init__(self, reqs, unpack, halo, vec, ncomp):
+        self.reqs, self.unpack, self.halo, self.vec, self.ncomp = reqs, unpack, halo, vec, ncomp
+
+    def wait(self):
+        for r in self.reqs:
+            r.wait()
+        for buf, a, b in self.unpack:
+            w = (b - a) * self.halo.np1
+            for c in range(self.ncomp):
+                self.halo._view(self.vec, c, a, b).copy_(buf[c * w:(c + 1) * w])
 
 
 class SlabState:
@@ -273,11 +327,10 @@ class SlabState:
         c0, c1 = self.part.cells(self.rank)
         if exchange and c1 - c0 >= 3 and self.halo.overlappable(src) \
                 and type(self)._local_apply is SlabState._local_apply:
-            works = self.halo.start(src, ncomp)
+            pending = self.halo.start(src, ncomp)
             h, st = self.handle(), stream_handle()
             call("pff_apply_rows", h, mode, ptr(src), ptr(dst), ptr(rhs), c0 + 1, c1 - 1, st)
-            for w in works:
-                w.wait()
+            pending.wait()
             call("pff_apply_rows", h, mode, ptr(src), ptr(dst), ptr(rhs), c0, c0 + 1, st)
             call("pff_apply_rows", h, mode, ptr(src), ptr(dst), ptr(rhs), c1 - 1, c1, st)
             return dst

@@ -58,7 +58,8 @@ def _worker(rank, world, port, level, split, q):
         out = torch.from_numpy(np.concatenate([zg, xg]))
         dist.all_reduce(out)
         if rank == 0:
-            q.put(("ok", out.numpy(), res.iterations, gmg.ranges))
+            q.put(("ok", out.numpy(), res.iterations,
+                   {L.level: L.ranges for L in gmg.lv}))
         dist.barrier()
         dist.destroy_process_group()
     except Exception:  # pragma: no cover
@@ -66,8 +67,11 @@ def _worker(rank, world, port, level, split, q):
         q.put(("err", traceback.format_exc(), None, None))
 
 
-@pytest.mark.parametrize("world,level,split", [(2, 6, "miehe"), (4, 7, "miehe"), (2, 7, "none")])
+@pytest.mark.parametrize("world,level,split", [(2, 6, "miehe"), (4, 7, "miehe"), (2, 7, "none"),
+                                                (2, 8, "miehe"), (4, 8, "none")])
 def test_distributed_newton_step_matches_single_gpu(world, level, split):
+    """Slab levels: (2, 6) the finest only; (4, 7) / (2, 7) two; (2, 8) three
+    (256^2 -> 128^2 -> 64^2 in slabs, 32^2 agglomerated); (4, 8) two."""
     import paper_2005_00331_b200 as P
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -88,8 +92,11 @@ def test_distributed_newton_step_matches_single_gpu(world, level, split):
     gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
     gmg.setup(st)
     n = st.n_scalar
-    for blk in ("uu", "phiphi"):
-        assert np.allclose(ranges[blk], gmg.ranges[level][blk], rtol=1e-10, atol=0)
+    expect_slabs = {(2, 6): 1, (4, 7): 2, (2, 7): 2, (2, 8): 3, (4, 8): 2}[(world, level)]
+    assert len(ranges) == expect_slabs
+    for l, rg in ranges.items():   # every slab level's Lanczos ranges
+        for blk in ("uu", "phiphi"):
+            assert np.allclose(rg[blk], gmg.ranges[l][blk], rtol=1e-10, atol=0), (l, blk)
     rhs = x.copy()
     rhs[st.constrained_mask()] = 0.0
     zg = out[:3 * n]

@@ -233,3 +233,88 @@ def test_overlapped_slab_decomposition_bitwise(world):
                 call("pff_apply_rows", h, 0, ptr(src), ptr(got), ptr(fused), a, b, stream_handle())
             own = torch.from_numpy(np.tile(part.owned_mask(r), 3)).cuda()
             assert torch.equal(got[own], want[own])
+
+
+def _restrict_worker(rank, world, port, p, level, q):
+    """Slab -> slab restriction on CPU: each rank restricts its OWNED fine rows
+    (the oracle's P^T with the other rows zeroed) into its coarse window, the
+    reverse ghost-row sum completes the boundary rows; then the forward
+    exchange + prolongation of the coarse window into the owned fine rows."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2005_00331_b200.parallel import HaloExchange
+        pf, pc = SlabPartition(p, level, world), SlabPartition(p, level - 1, world)
+        T = O.Transfer(p, level)
+        rng = np.random.default_rng(7)
+        y = rng.uniform(-1, 1, 3 * pf.n)
+        # restriction of the owned fine entries only
+        own_f = np.zeros(pf.n, bool)
+        own_f[pf.local_index(rank)[pf.owned_mask(rank)]] = True
+        part_glob = T.restrict(np.where(np.tile(own_f, 3), y, 0.0))
+        # the window must hold every nonzero partial: nothing outside it, zero
+        # on its bottom ghost rows
+        idx_c = pc.local_index(rank)
+        inwin = np.zeros(pc.n, bool)
+        inwin[idx_c] = True
+        assert np.all(part_glob.reshape(3, pc.n)[:, ~inwin] == 0.0)
+        loc = torch.from_numpy(pc.scatter(part_glob, rank, 3))
+        lo, _ = pc.rows(rank)
+        olo, _ = pc.own_rows(rank)
+        lnc = pc.local_n(rank)
+        for c in range(3):
+            assert torch.all(loc[c * lnc:c * lnc + (olo - lo) * pc.np1] == 0.0)
+        halo = HaloExchange(pc, rank)
+        halo.reverse_add(loc, 3)
+        rc = np.zeros(3 * pc.n)
+        pc.gather_into(rc, loc.numpy(), rank, 3)
+        t = torch.from_numpy(rc)
+        dist.all_reduce(t)
+        # prolongation from the coarse window (after the forward exchange)
+        xc = rng.uniform(-1, 1, 3 * pc.n)
+        own_c = torch.from_numpy(np.tile(pc.owned_mask(rank), 3))
+        zc = torch.where(own_c, torch.from_numpy(pc.scatter(xc, rank, 3)),
+                         torch.zeros((), dtype=torch.float64))
+        halo.exchange(zc, 3)
+        full_c = np.zeros(3 * pc.n)
+        for c in range(3):
+            full_c[c * pc.n + idx_c] = zc.numpy()[c * lnc:(c + 1) * lnc]
+        pz = T.prolongate(full_c)
+        zf = np.zeros(3 * pf.n)
+        pf.gather_into(zf, pf.scatter(pz, rank, 3), rank, 3)
+        tz = torch.from_numpy(zf)
+        dist.all_reduce(tz)
+        if rank == 0:
+            q.put(("ok", t.numpy(), tz.numpy()))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put(("err", traceback.format_exc(), None))
+
+
+@pytest.mark.parametrize("world,p,level", [(2, 2, 5), (4, 2, 5), (4, 1, 6), (2, 4, 4)])
+def test_gloo_slab_to_slab_transfers(world, p, level):
+    """The slab V-cycle's transfers (distributed.py): restriction of the owned
+    fine rows into the coarse window + reverse ghost-row sum == P^T y, and
+    prolongation from an exchanged coarse window == P x on the owned fine rows
+    (src/multigrid.py:97-120)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_restrict_worker, args=(r, world, port, p, level, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    status, rc, zf = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert status == "ok", rc
+    T = O.Transfer(p, level)
+    rng = np.random.default_rng(7)
+    y = rng.uniform(-1, 1, 3 * T.nf)
+    xc = rng.uniform(-1, 1, 3 * T.nc)
+    want = T.restrict(y)
+    assert np.max(np.abs(rc - want)) <= 1e-13 * np.max(np.abs(want))
+    wz = T.prolongate(xc)
+    assert np.max(np.abs(zf - wz)) <= 1e-14 * np.max(np.abs(wz))
