@@ -167,6 +167,24 @@ int pff_residual(const pff_level* L, double* out, int mask_dirichlet, int mask_a
  * mesh only. */
 int pff_cell_matrices(const pff_level* L, double* gk, void* stream);
 
+/* Small dense fp64 algebra of the GMG setup (the coarse solve and the level-3
+ * V-cycle as dense maps, src/multigrid.py:311-344 for a fixed setup).
+ * Row-major matrices.
+ * pff_dense_jacobian: G (3n x 3n) = the level's Jacobian assembled from its
+ *   cell matrices gk (pff_cell_matrices), identity on constrained rows and
+ *   columns (src/pff_operator.py:343-377); whole-mesh levels, 3n <= 8192.
+ * pff_dgemm: C = alpha A B + beta C (A m x k, B k x n; beta = 0 overwrites).
+ * pff_dmat_axpby: Y = a Y + b diag(s) X (s NULL: identity; a = 0 overwrites).
+ * pff_dmat_diag: Y (n x n) = diag(s) (s NULL: identity).
+ * pff_recip: y = 1/x (mode 0) or 1/sqrt(x) (mode 1). */
+int pff_dense_jacobian(const pff_level* L, const double* gk, double* G, void* stream);
+int pff_dgemm(int m, int n, int k, double alpha, const double* A, int lda, const double* B,
+              int ldb, double beta, double* C, int ldc, void* stream);
+int pff_dmat_axpby(int m, int n, double a, double* Y, int ldy, double b, const double* s,
+                   const double* X, int ldx, void* stream);
+int pff_dmat_diag(int n, const double* s, double* Y, int ldy, void* stream);
+int pff_recip(int64_t n, const double* x, double* y, int mode, void* stream);
+
 /* lumped phi mass diagonal (src/active_set_solver.py:60-69 -> src/_kernels.py:828-843):
  * row sums of the scalar mass matrix over the level's local nodes; bitwise the
  * reference's summation order.  Needs no bound state. */

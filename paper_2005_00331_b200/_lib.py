@@ -53,6 +53,11 @@ SIGNATURES = {
     "pff_diagonal": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_residual": (_i, [ctypes.c_void_p, _c_dp, _i, _i, ctypes.c_void_p]),
     "pff_cell_matrices": (_i, [ctypes.c_void_p, _c_dp, ctypes.c_void_p]),
+    "pff_dense_jacobian": (_i, [ctypes.c_void_p, _c_dp, _c_dp, ctypes.c_void_p]),
+    "pff_dgemm": (_i, [_i, _i, _i, _d, _c_dp, _i, _c_dp, _i, _d, _c_dp, _i, ctypes.c_void_p]),
+    "pff_dmat_axpby": (_i, [_i, _i, _d, _c_dp, _i, _d, _c_dp, _c_dp, _i, ctypes.c_void_p]),
+    "pff_dmat_diag": (_i, [_i, _c_dp, _c_dp, _i, ctypes.c_void_p]),
+    "pff_recip": (_i, [_i64, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_lumped_mass": (_i, [ctypes.c_void_p, _c_dp, ctypes.c_void_p]),
     "pff_active_set": (_i, [_i64, _c_dp, _c_dp, _c_dp, _c_dp, _d, _c_dp, _c_dp, _c_dp,
                             ctypes.c_void_p]),

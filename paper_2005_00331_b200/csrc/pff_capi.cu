@@ -421,6 +421,43 @@ int pff_cell_matrices(const pff_level* h, double* gk, void* stream) {
     return check(pff::launch_cell_matrices(*L, gk, S(stream)), "pff_cell_matrices");
 }
 
+int pff_dense_jacobian(const pff_level* h, const double* gk, double* G, void* stream) {
+    const Level* L = reinterpret_cast<const Level*>(h);
+    if (!bound(L)) return fail(PFF_E_UNBOUND, "%s", "pff_dense_jacobian: state not bound");
+    if (!gk || !G) return fail(PFF_E_ARG, "%s", "pff_dense_jacobian: null argument");
+    if (L->windowed() || 3 * L->mesh.n > 8192)
+        return fail(PFF_E_ARG, "%s", "pff_dense_jacobian: whole-mesh levels with 3n <= 8192 only");
+    return check(pff::launch_dense_jacobian(*L, gk, G, S(stream)), "pff_dense_jacobian");
+}
+
+int pff_dgemm(int m, int n, int k, double alpha, const double* A, int lda, const double* B, int ldb,
+              double beta, double* C, int ldc, void* stream) {
+    if (m < 0 || n < 0 || k < 0 || (m > 0 && n > 0 && (!C || (k > 0 && (!A || !B)))) ||
+        lda < k || ldb < n || ldc < n)
+        return fail(PFF_E_ARG, "%s", "pff_dgemm: bad sizes, leading dimensions or null matrix");
+    return check(pff::launch_dgemm(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, S(stream)),
+                 "pff_dgemm");
+}
+
+int pff_dmat_axpby(int m, int n, double a, double* Y, int ldy, double b, const double* s,
+                   const double* X, int ldx, void* stream) {
+    if (m < 0 || n < 0 || (m > 0 && n > 0 && (!Y || !X)) || ldy < n || ldx < n)
+        return fail(PFF_E_ARG, "%s", "pff_dmat_axpby: bad sizes or null matrix");
+    return check(pff::launch_dmat_axpby(m, n, a, Y, ldy, b, s, X, ldx, S(stream)), "pff_dmat_axpby");
+}
+
+int pff_dmat_diag(int n, const double* s, double* Y, int ldy, void* stream) {
+    if (n < 0 || (n > 0 && !Y) || ldy < n)
+        return fail(PFF_E_ARG, "%s", "pff_dmat_diag: bad size or null matrix");
+    return check(pff::launch_dmat_diag(n, s, Y, ldy, S(stream)), "pff_dmat_diag");
+}
+
+int pff_recip(int64_t n, const double* x, double* y, int mode, void* stream) {
+    if (n < 0 || (n > 0 && (!x || !y)) || (mode != 0 && mode != 1))
+        return fail(PFF_E_ARG, "%s", "pff_recip: bad size, null vector or mode");
+    return check(pff::launch_recip(n, x, y, mode, S(stream)), "pff_recip");
+}
+
 int pff_lumped_mass(const pff_level* h, double* out, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!L || !out) return fail(PFF_E_ARG, "%s", "pff_lumped_mass: null argument");

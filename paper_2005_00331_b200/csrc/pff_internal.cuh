@@ -230,6 +230,15 @@ struct ChebArgs {
     int emit_nc = 0;
 };
 
+// small dense algebra of the GMG setup (pff_dense.cu)
+cudaError_t launch_dense_jacobian(const Level& L, const double* gk, double* G, cudaStream_t s);
+cudaError_t launch_dgemm(int m, int n, int k, double alpha, const double* A, int lda, const double* B,
+                         int ldb, double beta, double* C, int ldc, cudaStream_t s);
+cudaError_t launch_dmat_axpby(int m, int n, double a, double* Y, int ldy, double b, const double* sv,
+                              const double* X, int ldx, cudaStream_t s);
+cudaError_t launch_dmat_diag(int n, const double* sv, double* Y, int ldy, cudaStream_t s);
+cudaError_t launch_recip(int64_t n, const double* x, double* y, int mode, cudaStream_t s);
+
 // options (pff_set_option)
 void set_generic_apply(bool on);
 void set_sweep_rows_per_chunk(int rows);

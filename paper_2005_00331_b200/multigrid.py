@@ -430,6 +430,13 @@ def _ritz_batched(runs):
             r.lo, r.hi = float(ev[g, 0]), float(ev[g, -1])
 
 
+def _recip(x: torch.Tensor, mode: int) -> torch.Tensor:
+    """1/x (mode 0) or 1/sqrt(x) (mode 1) by pff_recip."""
+    y = torch.empty_like(x)
+    call("pff_recip", x.numel(), ptr(x), ptr(y), mode, stream_handle())
+    return y
+
+
 class _LevelWork:
     def __init__(self, n):
         self.r = _empty(3 * n)      # level right-hand side (restricted residual)
@@ -517,7 +524,7 @@ class GmgPreconditioner:
             s = self.states[l]
             duu, dpp = op.block_diagonals(s, invert=False)
             self.diags[l] = {"uu": duu, "phiphi": dpp}
-            self._inv[l] = (1.0 / duu, 1.0 / dpp)
+            self._inv[l] = (_recip(duu, 0), _recip(dpp, 0))
             if l not in self._work or self._work[l].resphi.numel() != s.n_scalar:
                 self._work[l] = _LevelWork(s.n_scalar)
         todo = []
@@ -535,49 +542,91 @@ class GmgPreconditioner:
             logger.debug("gmg setup: levels %d..%d, ranges %s", self.coarse_level, state.level,
                          {l: (r["uu"][1], r["phiphi"][1]) for l, r in self.ranges.items()})
 
+    # -- dense maps of the coarse end of the cycle (own kernels: pff_dense.cu) ----
+    @staticmethod
+    def _gemm(C, A, B, alpha=1.0, beta=0.0):
+        """C = alpha A B + beta C on row-major (sub-)matrix views."""
+        call("pff_dgemm", C.shape[0], C.shape[1], A.shape[1], float(alpha), ptr(A), A.stride(0),
+             ptr(B), B.stride(0), float(beta), ptr(C), C.stride(0), stream_handle())
+        return C
+
+    @staticmethod
+    def _axpby(Y, a, X, b, s=None):
+        """Y = a Y + b diag(s) X."""
+        call("pff_dmat_axpby", Y.shape[0], Y.shape[1], float(a), ptr(Y), Y.stride(0), float(b),
+             ptr(s), ptr(X), X.stride(0), stream_handle())
+        return Y
+
+    @staticmethod
+    def _diagm(Y, s=None):
+        call("pff_dmat_diag", Y.shape[0], ptr(s), ptr(Y), Y.stride(0), stream_handle())
+        return Y
+
+    def _dense_jacobian(self, s):
+        """Masked dense Jacobian of a (small) level: pff_cell_matrices scattered
+        by pff_dense_jacobian (identity constrained rows and columns)."""
+        n = s.n_scalar
+        nl = 3 * s.dof_map.n_local
+        gk = torch.empty((s.mesh.n_cells, nl, nl), dtype=torch.float64, device=_dev())
+        st = stream_handle()
+        call("pff_cell_matrices", s.bind(), ptr(gk), st)
+        G = torch.empty((3 * n, 3 * n), dtype=torch.float64, device=_dev())
+        call("pff_dense_jacobian", s.bind(), ptr(gk), ptr(G), st)
+        return G
+
+    def _cheb_poly(self, A, invd, a, b, sweeps):
+        """The Jacobi-Chebyshev pass (src/multigrid.py:170-198) as a matrix
+        polynomial: the reference recurrence run on the identity."""
+        nb = A.shape[0]
+        theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+        sigma1 = theta / delta
+        d = self._diagm(torch.empty((nb, nb), dtype=torch.float64, device=A.device), invd)
+        self._axpby(d, 0.0, d, 1.0 / theta)
+        acc = self._axpby(torch.empty_like(d), 0.0, d, 1.0)
+        cr = self._diagm(torch.empty_like(d))
+        rho_old = 1.0 / sigma1
+        for _ in range(1, sweeps):
+            rho = 1.0 / (2.0 * sigma1 - rho_old)
+            self._gemm(cr, A, d, -1.0, 1.0)                            # cr -= G d
+            self._axpby(d, rho * rho_old, cr, 2.0 * rho / delta, invd)   # d = c1 d + c2 D^-1 cr
+            self._axpby(acc, 1.0, d, 1.0)                               # z += d
+            rho_old = rho
+        return acc
+
     def _build_dense_coarse(self):
         """Coarse solve (src/multigrid.py:311-328) as fixed linear maps: the
         coarse_sweeps-step Jacobi-Chebyshev pass on a block is the matrix
         polynomial obtained by running the reference recurrence (cheb_init, then
         cr -= G d, d = c1 d + c2 D^-1 cr, z += d) on the identity.  The blocks come
-        from the assembled masked Jacobian of the coarse level (identity
-        constrained rows/columns, as pff_apply's modes)."""
+        from the masked dense Jacobian of the coarse level (identity constrained
+        rows/columns, as pff_apply's modes)."""
         self._dense = None
         l = self.coarse_level
         s = self.states[l]
         n = s.n_scalar
         if not DENSE_COARSE or n > COARSE_DENSE_NMAX:
             return
-        G = op.assemble_oracle(s).device.to_dense()
+        G = self._dense_jacobian(s)
         inv_u, inv_p = self._inv[l]
         cfg = self.cheb
-
-        def poly(A, invd, a, b, sweeps):
-            nb = A.shape[0]
-            theta, delta = 0.5 * (b + a), 0.5 * (b - a)
-            sigma1 = theta / delta
-            eye = torch.eye(nb, dtype=torch.float64, device=A.device)
-            dcol = invd[:, None].contiguous()
-            d = dcol * eye / theta
-            acc = d.clone()
-            cr = eye
-            rho_old = 1.0 / sigma1
-            # in place, four launches per step (the setup is launch-bound here)
-            for _ in range(1, sweeps):
-                rho = 1.0 / (2.0 * sigma1 - rho_old)
-                cr = torch.addmm(cr, A, d, alpha=-1.0)
-                d.mul_(rho * rho_old).addcmul_(dcol, cr, value=2.0 * rho / delta)
-                acc.add_(d)
-                rho_old = rho
-            return acc.contiguous()
-
         lo, hi = self.ranges[l]["uu"]
-        Cu = poly(G[:2 * n, :2 * n], inv_u, lo, cfg.C * hi, cfg.coarse_sweeps)
+        Cu = self._cheb_poly(G[:2 * n, :2 * n], inv_u, lo, cfg.C * hi, cfg.coarse_sweeps)
         lo, hi = self.ranges[l]["phiphi"]
-        Cp = poly(G[2 * n:, 2 * n:], inv_p, lo, cfg.C * hi, cfg.coarse_sweeps)
-        Gpu = G[2 * n:, :2 * n].contiguous()
+        Cp = self._cheb_poly(G[2 * n:, 2 * n:], inv_p, lo, cfg.C * hi, cfg.coarse_sweeps)
+        Gpu = self._axpby(torch.empty((n, 2 * n), dtype=torch.float64, device=G.device), 0.0,
+                          G[2 * n:, :2 * n], 1.0)
         cmask = torch.from_numpy(s.constrained_mask().astype(np.uint8)).to(G.device)
         self._dense = (n, Cu, Gpu, Cp, cmask)
+
+    def _transfer_dense(self, L, dev):
+        """Dense scalar prolongation P (n x nc) of level L and its transpose,
+        from the structured CSR (host), cached per hierarchy."""
+        key = ("dense_P", L)
+        cache = self.__dict__.setdefault("_dense_P_cache", {})
+        if key not in cache:
+            P = self.transfers[L].P.toarray()
+            cache[key] = (torch.from_numpy(P).to(dev), torch.from_numpy(np.ascontiguousarray(P.T)).to(dev))
+        return cache[key]
 
     def _build_dense_level(self):
         """The V-cycle from level L = coarse_level + 1 down (src/multigrid.py:330-344:
@@ -596,60 +645,56 @@ class GmgPreconditioner:
         if n > DENSE_LEVEL_NMAX:
             return
         dev = self._dense[1].device
-        G = op.assemble_oracle(s).device.to_dense()
+        G = self._dense_jacobian(s)
         inv_u, inv_p = self._inv[L]
         cfg = self.cheb
-
-        def poly(A, invd, a, b, sweeps):
-            nb = A.shape[0]
-            theta, delta = 0.5 * (b + a), 0.5 * (b - a)
-            sigma1 = theta / delta
-            eye = torch.eye(nb, dtype=torch.float64, device=dev)
-            d = invd[:, None] * eye / theta
-            acc = d.clone()
-            cr = eye
-            rho_old = 1.0 / sigma1
-            for _ in range(1, sweeps):
-                rho = 1.0 / (2.0 * sigma1 - rho_old)
-                cr = cr - A @ d
-                d = (rho * rho_old) * d + (2.0 * rho / delta) * (invd[:, None] * cr)
-                acc = acc + d
-                rho_old = rho
-            return acc
-
+        N = 3 * n
         hu = self.ranges[L]["uu"][1]
         hp = self.ranges[L]["phiphi"][1]
-        Cu = poly(G[:2 * n, :2 * n], inv_u, cfg.c * hu, cfg.C * hu, cfg.sweeps)
-        Cp = poly(G[2 * n:, 2 * n:], inv_p, cfg.c * hp, cfg.C * hp, cfg.sweeps)
-        cons = torch.from_numpy(s.constrained_mask()).to(dev)
+        Cu = self._cheb_poly(G[:2 * n, :2 * n], inv_u, cfg.c * hu, cfg.C * hu, cfg.sweeps)
+        Cp = self._cheb_poly(G[2 * n:, 2 * n:], inv_p, cfg.c * hp, cfg.C * hp, cfg.sweeps)
+        cons_np = s.constrained_mask()
+        cons = torch.from_numpy(cons_np.astype(np.float64)).to(dev)
+        ncons = torch.from_numpy((~cons_np).astype(np.float64)).to(dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        T = torch.empty((N, N), **f64)
 
         def smooth(R, Z):   # _smooth: u block on r - G z, then the phi row with the new z_u
-            Z = Z.clone()
-            Z[:2 * n] += Cu @ (R[:2 * n] - G[:2 * n] @ Z)
-            Z[2 * n:] += Cp @ (R[2 * n:] - G[2 * n:] @ Z)
-            return Z
+            Tu = self._axpby(T[:2 * n], 0.0, R[:2 * n], 1.0)
+            self._gemm(Tu, G[:2 * n], Z, -1.0, 1.0)
+            self._gemm(Z[:2 * n], Cu, Tu, 1.0, 1.0)
+            Tp = self._axpby(T[2 * n:], 0.0, R[2 * n:], 1.0)
+            self._gemm(Tp, G[2 * n:], Z, -1.0, 1.0)
+            self._gemm(Z[2 * n:], Cp, Tp, 1.0, 1.0)
 
         # the coarse level: transfer (scalar P per component) and the dense solve
         nc, Cu2, Gpu2, Cp2, cmask2 = self._dense
-        P1 = torch.from_numpy(self.transfers[L].P.toarray()).to(dev)      # (n, nc)
-        cons2 = cmask2.bool()
-
-        def coarse(Rc):
-            Zc = torch.empty_like(Rc)
-            Zc[:2 * nc] = Cu2 @ Rc[:2 * nc]
-            Zc[2 * nc:] = Cp2 @ (Rc[2 * nc:] - Gpu2 @ Zc[:2 * nc])
-            Zc[cons2] = Rc[cons2]
-            return Zc
-
-        R = torch.eye(3 * n, dtype=torch.float64, device=dev)
-        Z = smooth(R, cons[:, None] * R)                     # z = select(r), first smoothing
-        res = R - G @ Z
-        Rc = torch.cat([P1.T @ res[k * n:(k + 1) * n] for k in range(3)])
-        Rc[cons2] = 0.0                                      # restriction zeroes constrained rows
-        Zc = coarse(Rc)
-        Z = Z + (~cons)[:, None] * torch.cat([P1 @ Zc[k * nc:(k + 1) * nc] for k in range(3)])
-        Z = smooth(R, Z)
-        self._dense_l = (L, 3 * n, Z.contiguous())
+        P1, P1T = self._transfer_dense(L, dev)                    # (n, nc), (nc, n)
+        cons2_np = self.states[self.coarse_level].constrained_mask()
+        c2 = torch.from_numpy(cons2_np.astype(np.float64)).to(dev)
+        nc2 = torch.from_numpy((~cons2_np).astype(np.float64)).to(dev)
+        R = self._diagm(torch.empty((N, N), **f64))
+        Z = self._diagm(torch.empty((N, N), **f64), cons)          # z = select(r)
+        smooth(R, Z)                                               # first smoothing
+        res = self._axpby(torch.empty((N, N), **f64), 0.0, R, 1.0)
+        self._gemm(res, G, Z, -1.0, 1.0)                           # res = r - G z
+        Rc = torch.empty((3 * nc, N), **f64)
+        for k in range(3):
+            self._gemm(Rc[k * nc:(k + 1) * nc], P1T, res[k * n:(k + 1) * n])
+        self._axpby(Rc, 0.0, Rc, 1.0, nc2)                         # zero constrained coarse rows
+        Zc = torch.empty((3 * nc, N), **f64)
+        self._gemm(Zc[:2 * nc], Cu2, Rc[:2 * nc])
+        Tc = self._axpby(torch.empty((nc, N), **f64), 0.0, Rc[2 * nc:], 1.0)
+        self._gemm(Tc, Gpu2, Zc[:2 * nc], -1.0, 1.0)
+        self._gemm(Zc[2 * nc:], Cp2, Tc)
+        self._axpby(Zc, 0.0, Zc, 1.0, nc2)                         # constrained: zc = rc
+        self._axpby(Zc, 1.0, Rc, 1.0, c2)
+        Pz = torch.empty((N, N), **f64)
+        for k in range(3):
+            self._gemm(Pz[k * n:(k + 1) * n], P1, Zc[k * nc:(k + 1) * nc])
+        self._axpby(Z, 1.0, Pz, 1.0, ncons)                        # masked prolongation
+        smooth(R, Z)                                               # second smoothing
+        self._dense_l = (L, N, Z)
 
     def _estimate_ranges(self, level: int):
         s = self.states[level]
@@ -726,7 +771,7 @@ class GmgPreconditioner:
                 work = torch.empty(4 * nb, dtype=torch.float64, device=diag.device)
                 work[:nb].copy_(start_vector_device(cfg.seed + 101 * l + (0 if blk == "uu" else 1),
                                                     nb, diag.device))
-                descs.append((l, blk, s.bind(), mode, nb, 1.0 / torch.sqrt(diag), work))
+                descs.append((l, blk, s.bind(), mode, nb, _recip(diag, 1), work))
         R = len(descs)
         dev = descs[0][6].device
         plen = _lib.load().pff_reduce_scratch_len()

@@ -424,6 +424,61 @@ def test_dense_matvec_matches_torch():
         assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
 
 
+def test_dense_setup_kernels_match_torch():
+    """The GMG setup's own dense kernels (pff_dense.cu) against plain torch fp64:
+    GEMM on sub-matrix views with alpha/beta, the row-scaled axpby, diag, recip."""
+    from paper_2005_00331_b200._lib import call, ptr, stream_handle
+    g = torch.Generator(device="cuda").manual_seed(4)
+    rnd = lambda *sh: torch.rand(*sh, dtype=torch.float64, device="cuda", generator=g) - 0.5  # noqa: E731
+    st = stream_handle()
+    for m, n, k in ((891, 891, 891), (85, 891, 297), (1, 3, 2), (170, 170, 170), (65, 63, 17)):
+        A, B = rnd(m + 3, k + 5), rnd(k, n + 2)
+        C0 = rnd(m, n)
+        Av, Bv = A[1:m + 1, 2:k + 2], B[:, 1:n + 1]          # strided views (lda, ldb > k, n)
+        C = C0.clone()
+        call("pff_dgemm", m, n, k, -0.75, ptr(Av), Av.stride(0), ptr(Bv), Bv.stride(0), 1.5,
+             ptr(C), C.stride(0), st)
+        ref = 1.5 * C0 - 0.75 * (Av @ Bv)
+        assert rel_l2(C.cpu().numpy(), ref.cpu().numpy()) <= 1e-14, (m, n, k)
+        C = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+        call("pff_dgemm", m, n, k, 1.0, ptr(Av), Av.stride(0), ptr(Bv), Bv.stride(0), 0.0,
+             ptr(C), C.stride(0), st)
+        assert rel_l2(C.cpu().numpy(), (Av @ Bv).cpu().numpy()) <= 1e-14
+    Y0, X, sv = rnd(40, 30), rnd(40, 30), rnd(40)
+    Y = Y0.clone()
+    call("pff_dmat_axpby", 40, 30, 0.5, ptr(Y), 30, -2.0, ptr(sv), ptr(X), 30, st)
+    assert torch.allclose(Y, 0.5 * Y0 - 2.0 * sv[:, None] * X, rtol=1e-15, atol=1e-15)
+    Y = torch.full((40, 30), float("nan"), dtype=torch.float64, device="cuda")
+    call("pff_dmat_axpby", 40, 30, 0.0, ptr(Y), 30, 3.0, None, ptr(X), 30, st)
+    assert torch.equal(Y, 3.0 * X)
+    D = torch.empty(40, 40, dtype=torch.float64, device="cuda")
+    call("pff_dmat_diag", 40, ptr(sv), ptr(D), 40, st)
+    assert torch.equal(D, torch.diag(sv))
+    x = torch.rand(1000, dtype=torch.float64, device="cuda", generator=g) + 0.1
+    y = torch.empty_like(x)
+    call("pff_recip", 1000, ptr(x), ptr(y), 1, st)
+    assert torch.allclose(y, 1.0 / torch.sqrt(x), rtol=1e-15, atol=0)
+    call("pff_recip", 1000, ptr(x), ptr(y), 0, st)
+    assert torch.allclose(y, 1.0 / x, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
+@pytest.mark.parametrize("p,level", [(2, 2), (2, 3), (1, 3)])
+def test_dense_jacobian_matches_sparse_assembly(split, p, level):
+    """pff_dense_jacobian (the setup's masked dense coarse Jacobian) against the
+    sparse assembled oracle (src/pff_operator.py:343-377)."""
+    ost, _ = O.baseline_state(p, level, split, seed=2)
+    h = P.build_hierarchy(max(level, 2), p)
+    st = P.LinearizationState(h, level, ost.params, split=split)
+    st.set_solution(ost.U); st.set_phi_tilde(ost.phi_tilde); st.set_phi_old(ost.phi_old)
+    st.set_active(ost.active); st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    gmg = P.GmgPreconditioner(h, coarse_level=2)
+    G = gmg._dense_jacobian(st).cpu().numpy()
+    ref = P.operator.assemble_oracle(st).device.to_dense().cpu().numpy()
+    assert np.max(np.abs(G - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
 @pytest.mark.parametrize("split", ["miehe", "none"])
 def test_dense_level_vcycle_matches_matrix_free(split):
     """The V-cycle with the level-3 dense map and dense coarse maps equals the
