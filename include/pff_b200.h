@@ -176,7 +176,10 @@ int pff_cell_matrices(const pff_level* L, double* gk, void* stream);
  * pff_dgemm: C = alpha A B + beta C (A m x k, B k x n; beta = 0 overwrites).
  * pff_dmat_axpby: Y = a Y + b diag(s) X (s NULL: identity; a = 0 overwrites).
  * pff_dmat_diag: Y (n x n) = diag(s) (s NULL: identity).
- * pff_recip: y = 1/x (mode 0) or 1/sqrt(x) (mode 1). */
+ * pff_recip: y = 1/x (mode 0) or 1/sqrt(x) (mode 1).
+ * pff_flags: mode 0 packs the Dirichlet / active byte masks into the level
+ *   flags (bit0 | bit1), mode 1 unpacks them (src/pff_operator.py:
+ *   constrained_mask). */
 int pff_dense_jacobian(const pff_level* L, const double* gk, double* G, void* stream);
 int pff_dgemm(int m, int n, int k, double alpha, const double* A, int lda, const double* B,
               int ldb, double beta, double* C, int ldc, void* stream);
@@ -184,6 +187,7 @@ int pff_dmat_axpby(int m, int n, double a, double* Y, int ldy, double b, const d
                    const double* X, int ldx, void* stream);
 int pff_dmat_diag(int n, const double* s, double* Y, int ldy, void* stream);
 int pff_recip(int64_t n, const double* x, double* y, int mode, void* stream);
+int pff_flags(int64_t n, uint8_t* dir, uint8_t* act, uint8_t* flags, int mode, void* stream);
 
 /* lumped phi mass diagonal (src/active_set_solver.py:60-69 -> src/_kernels.py:828-843):
  * row sums of the scalar mass matrix over the level's local nodes; bitwise the

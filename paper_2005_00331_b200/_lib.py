@@ -58,6 +58,7 @@ SIGNATURES = {
     "pff_dmat_axpby": (_i, [_i, _i, _d, _c_dp, _i, _d, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_dmat_diag": (_i, [_i, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_recip": (_i, [_i64, _c_dp, _c_dp, _i, ctypes.c_void_p]),
+    "pff_flags": (_i, [_i64, _c_dp, _c_dp, _c_dp, _i, ctypes.c_void_p]),
     "pff_lumped_mass": (_i, [ctypes.c_void_p, _c_dp, ctypes.c_void_p]),
     "pff_active_set": (_i, [_i64, _c_dp, _c_dp, _c_dp, _c_dp, _d, _c_dp, _c_dp, _c_dp,
                             ctypes.c_void_p]),

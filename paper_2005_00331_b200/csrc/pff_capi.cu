@@ -458,6 +458,12 @@ int pff_recip(int64_t n, const double* x, double* y, int mode, void* stream) {
     return check(pff::launch_recip(n, x, y, mode, S(stream)), "pff_recip");
 }
 
+int pff_flags(int64_t n, uint8_t* dir, uint8_t* act, uint8_t* flags, int mode, void* stream) {
+    if (n < 0 || (n > 0 && (!dir || !act || !flags)) || (mode != 0 && mode != 1))
+        return fail(PFF_E_ARG, "%s", "pff_flags: bad size, null mask or mode");
+    return check(pff::launch_flags(n, dir, act, flags, mode, S(stream)), "pff_flags");
+}
+
 int pff_lumped_mass(const pff_level* h, double* out, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!L || !out) return fail(PFF_E_ARG, "%s", "pff_lumped_mass: null argument");

@@ -126,6 +126,19 @@ __global__ void k_recip(int64_t n, const double* __restrict__ x, double* __restr
     y[i] = mode ? 1.0 / sqrt(x[i]) : 1.0 / x[i];
 }
 
+// constraint flags <-> masks (mode 0: flags = dir | act << 1; mode 1: unpack)
+__global__ void k_flags(int64_t n, uint8_t* dir, uint8_t* act, uint8_t* flags, int mode) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (mode == 0) {
+        flags[i] = (uint8_t)((dir[i] ? F_DIR : 0) | (act[i] ? F_ACT : 0));
+    } else {
+        const uint8_t f = flags[i];
+        dir[i] = (f & F_DIR) ? 1 : 0;
+        act[i] = (f & F_ACT) ? 1 : 0;
+    }
+}
+
 inline unsigned blocks256(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
@@ -172,6 +185,13 @@ cudaError_t launch_dmat_diag(int n, const double* sv, double* Y, int ldy, cudaSt
 cudaError_t launch_recip(int64_t n, const double* x, double* y, int mode, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     k_recip<<<blocks256(n), 256, 0, s>>>(n, x, y, mode);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flags(int64_t n, uint8_t* dir, uint8_t* act, uint8_t* flags, int mode, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_flags<<<blocks256(n), 256, 0, s>>>(n, dir, act, flags, mode);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -238,6 +238,7 @@ cudaError_t launch_dmat_axpby(int m, int n, double a, double* Y, int ldy, double
                               const double* X, int ldx, cudaStream_t s);
 cudaError_t launch_dmat_diag(int n, const double* sv, double* Y, int ldy, cudaStream_t s);
 cudaError_t launch_recip(int64_t n, const double* x, double* y, int mode, cudaStream_t s);
+cudaError_t launch_flags(int64_t n, uint8_t* dir, uint8_t* act, uint8_t* flags, int mode, cudaStream_t s);
 
 // options (pff_set_option)
 void set_generic_apply(bool on);

@@ -288,11 +288,9 @@ class LinearizationState:
         if self._flags is None or stamp != self._flags_stamp:
             d = self._dir.device()
             a = self._act.device()
-            f = d.to(torch.uint8) | (a.to(torch.uint8) << 1)
             if self._flags is None:
-                self._flags = f
-            else:
-                self._flags.copy_(f)
+                self._flags = torch.empty(d.numel(), dtype=torch.uint8, device=d.device)
+            call("pff_flags", d.numel(), ptr(d), ptr(a), ptr(self._flags), 0, stream_handle())
             self._flags_stamp = (self._dir.stamp, self._act.stamp)
         return self._flags
 
@@ -587,8 +585,11 @@ def _inject_once(fine: LinearizationState, level: int) -> LinearizationState:
     coarse.set_solution(U)
     coarse.set_phi_tilde(pt)
     coarse.set_phi_old(po)
-    coarse.set_active((fl & _lib.FLAG_ACTIVE) != 0)
-    coarse._dir.set((fl & _lib.FLAG_DIRICHLET) != 0)   # reference: no version bump
+    dmask = torch.empty(n, dtype=torch.bool, device=dev)
+    amask = torch.empty(n, dtype=torch.bool, device=dev)
+    call("pff_flags", n, ptr(dmask), ptr(amask), ptr(fl), 1, s)
+    coarse.set_active(amask)
+    coarse._dir.set(dmask)   # reference: no version bump
     return coarse
 
 
