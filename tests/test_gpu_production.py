@@ -151,6 +151,42 @@ def test_level10_vcycle_vs_reference_and_oracle(split):
     assert max(block_rel(_np(gi.apply(torch.from_numpy(x).cuda())), zo, n)) <= TOL
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("split", ["miehe", "none"])
+def test_level11_newton_step_vs_reference(split):
+    """2048^2 Q2 (50 M DoFs), the configs[3]/[4] inputs one level below
+    configs[4]: the reference itself (fixture from make_golden.py --production
+    11, an hour of serial numba GMRES) needs 43 (Miehe) GMRES(50) iterations --
+    the growth 28 (1024^2) -> 43 (2048^2) -> 82 (4096^2) is the reference's own.
+    Ranges on every level, the first V-cycle (sketch), the iteration count,
+    the residual history and the solution (sketch) against it."""
+    import os
+    from conftest import GOLDEN
+    name = f"prod_p2_l11_{split}"
+    if not os.path.exists(os.path.join(GOLDEN, name + ".npz")):
+        pytest.skip(f"{name} not generated")
+    d = load_golden(name)
+    st, x = _state(11, split)
+    n = st.n_scalar
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    _check_ranges(gmg, d, 11)
+    xd = torch.from_numpy(x).cuda()
+    want = {k[len("vcycle_"):]: d[k] for k in d if k.startswith("vcycle_") and k != "vcycle_s"}
+    assert sketch_rel(sketch(_np(gmg.apply(xd)), n), want) <= TOL
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    res = P.gmres_solve(P.JacobianOperator(st), torch.from_numpy(rhs).cuda(),
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    assert res.converged and res.iterations == int(d["gmres_iters"][0])
+    h_ref, h_got = d["gmres_hist"], np.asarray(res.residual_history)
+    assert h_got.shape == h_ref.shape
+    assert np.max(np.abs(h_got - h_ref) / h_ref[0]) <= 1e-10
+    wx = {k[len("gmres_x_"):]: d[k] for k in d if k.startswith("gmres_x_")}
+    assert sketch_rel(sketch(_np(res.solution), n), wx) <= 1e-8
+
+
 @pytest.mark.parametrize("name", ["pr1_miehe", "pr1_none"])
 def test_pr1_goldens_through_sweep_kernel(name):
     """PR1 (32^2 Q2) is below the sweep kernel's default threshold; force the

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--split", default="miehe")
     ap.add_argument("--restart", type=int, default=50)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--max-iterations", type=int, default=1000,
+                    help="stop after this many GMRES iterations (a bounded pin of the history)")
     args = ap.parse_args()
     nt = O.max_threads()
     t0 = time.perf_counter()
@@ -51,9 +53,11 @@ def main():
     rhs[ost.constrained_mask()] = 0.0
     t0 = time.perf_counter()
     res = O.gmres(lambda v: O.apply_jacobian(ost, v, nt), rhs, tol=1e-8,
-                  restart=args.restart, preconditioner=og.apply)
+                  restart=args.restart, preconditioner=og.apply,
+                  max_iterations=args.max_iterations)
     t_g = time.perf_counter() - t0
     out = {"level": args.level, "split": args.split, "restart": args.restart,
+           "max_iterations": args.max_iterations,
            "iterations": res.iterations, "converged": res.converged,
            "history": [float(v) for v in res.history],
            "ranges": {str(l): [r["uu"][0], r["uu"][1], r["phiphi"][0], r["phiphi"][1]]
