@@ -14,7 +14,7 @@ from .mesh import DofMap, MeshHierarchy, MeshLevel, build_hierarchy
 from .multigrid import (ChebyshevConfig, GmgPreconditioner, TransferOperator,
                         build_prolongation, chebyshev_apply, estimate_lambda_max,
                         estimate_lambda_range)
-from .operator import (AssemblyMemoryError, JacobianOperator, SparseOracle, assemble_oracle,
+from .operator import (AssemblyMemoryError, BlockVector, JacobianOperator, SparseOracle, assemble_oracle,
                        cell_matrices, LinearizationState, StaleCacheError,
                        apply_block_phiphi, apply_block_uu, apply_jacobian, apply_phi_row,
                        block_diagonal, block_diagonals, extrapolate_phase, residual, restrict_state_to_level)

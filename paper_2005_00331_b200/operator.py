@@ -28,6 +28,34 @@ class StaleCacheError(RuntimeError):
     """Raised when the Jacobian is applied at an outdated linearization."""
 
 
+class BlockVector:
+    """Monolithic (u_x | u_y | phi) host vector with per-component views
+    (src/pff_operator.py:32-59): ``data`` is the flat array the operator API
+    takes, the views alias it."""
+
+    __slots__ = ("data", "n_scalar")
+
+    def __init__(self, data, n_scalar: int):
+        arr = np.asarray(data, dtype=np.float64)
+        if arr.ndim != 1 or arr.size != 3 * n_scalar:
+            raise ValueError(f"a block vector of {n_scalar} scalar nodes has {3 * n_scalar} entries")
+        self.data, self.n_scalar = arr, n_scalar
+
+    @classmethod
+    def zeros(cls, n_scalar: int) -> "BlockVector":
+        return cls(np.zeros(3 * n_scalar), n_scalar)
+
+    def _part(self, k: int) -> np.ndarray:
+        return self.data[k * self.n_scalar:(k + 1) * self.n_scalar]
+
+    u_x = property(lambda self: self._part(0))
+    u_y = property(lambda self: self._part(1))
+    phi = property(lambda self: self._part(2))
+
+    def copy(self) -> "BlockVector":
+        return BlockVector(self.data.copy(), self.n_scalar)
+
+
 class AssemblyMemoryError(MemoryError):
     """Raised when the assembled (sparse) Jacobian does not fit into memory
     (src/pff_operator.py:28-29)."""
