@@ -34,6 +34,8 @@ def main():
         shutil.copyfile(path, os.path.join(VENDOR, dst))
         with open(path, "rb") as f:
             lines.append(f"{dst}  <- {src}  sha256 {hashlib.sha256(f.read()).hexdigest()}")
+    with open(os.path.join(VENDOR, "__init__.py"), "w") as f:
+        f.write("")
     with open(os.path.join(VENDOR, "PROVENANCE.txt"), "w") as f:
         f.write("fracturekit 0.1.0 (/root/reference/pkg), copied unmodified by prepare.py\n")
         f.write("\n".join(lines) + "\n")
