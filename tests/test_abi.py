@@ -2,6 +2,7 @@
 
 import ctypes
 import os
+import sys
 import re
 
 import numpy as np
@@ -175,3 +176,52 @@ def test_integration_doc_names_every_entry_point():
     doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
     missing = [s for s in header_symbols() if s not in doc]
     assert not missing, missing
+
+
+def test_bench_gpus_flag_launches_its_own_ranks(monkeypatch):
+    """bench.py --gpus N without WORLD_SIZE re-launches itself under
+    torch.distributed.run with N local ranks on 127.0.0.1; under torchrun a
+    WORLD_SIZE different from --gpus is an error."""
+    import subprocess
+    import bench
+    seen = {}
+
+    def fake_call(cmd):
+        seen["cmd"] = cmd
+        return 0
+    monkeypatch.setattr(subprocess, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "5"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert e.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "5"][-3:]
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert "WORLD_SIZE" in str(e.value.code)
+
+
+def test_scaling_model_uses_the_slab_rule():
+    """tools/scaling_model.py: the slab levels it models are the ones
+    distributed.DistributedGmg builds, and more GPUs never model slower."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import scaling_model as SM
+    from paper_2005_00331_b200 import distributed as D
+
+    class _H:
+        degree = 2
+    import torch
+    for world in (2, 4, 8):
+        g = D.DistributedGmg(_H(), 12, 0, world, coarse_level=2, device=torch.device("cpu"))
+        assert SM.slab_levels(12, world) == g.slab_levels
+    d = {"iterations": 82, "operator_s": 2.6e-3, "ortho_s": 12e-3,
+         "levels": [{"level": l, "floor_s": 95e-6, "prop_s": 0.37e-9 * (2 * 2 ** l + 1) ** 2}
+                    for l in range(4, 13)] + [{"level": 3, "floor_s": 8e-6, "prop_s": 0.0}]}
+    t = [SM.model(d, n)["gmres_s"] for n in (1, 2, 4, 8)]
+    assert t[0] > t[1] > t[2] > t[3]
+    assert SM.slab_levels(12, 8) == [12, 11, 10, 9, 8, 7]
