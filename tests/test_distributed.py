@@ -71,7 +71,7 @@ def _worker(rank, world, port, level, split, q):
                                                 (2, 8, "miehe"), (4, 8, "none")])
 def test_distributed_newton_step_matches_single_gpu(world, level, split):
     """Slab levels: (2, 6) the finest only; (4, 7) / (2, 7) two; (2, 8) three
-    (256^2 -> 128^2 -> 64^2 in slabs, 32^2 agglomerated); (4, 8) two."""
+    (256^2 -> 128^2 -> 64^2 in slabs, 32^2 agglomerated); (4, 8) three (256^2 -> 64^2 at 16 rows per rank)."""
     import paper_2005_00331_b200 as P
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -92,7 +92,7 @@ def test_distributed_newton_step_matches_single_gpu(world, level, split):
     gmg = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
     gmg.setup(st)
     n = st.n_scalar
-    expect_slabs = {(2, 6): 1, (4, 7): 2, (2, 7): 2, (2, 8): 3, (4, 8): 2}[(world, level)]
+    expect_slabs = {(2, 6): 1, (4, 7): 2, (2, 7): 2, (2, 8): 3, (4, 8): 3}[(world, level)]
     assert len(ranges) == expect_slabs
     for l, rg in ranges.items():   # every slab level's Lanczos ranges
         for blk in ("uu", "phiphi"):

@@ -187,6 +187,42 @@ def test_level11_newton_step_vs_reference(split):
     assert sketch_rel(sketch(_np(res.solution), n), wx) <= 1e-8
 
 
+@pytest.mark.slow
+def test_level12_first_iterations_vs_oracle():
+    """configs[4] (4096^2 Q2, 201 M DoFs): the C oracle's first 8 GMRES(50)
+    iterations on the box's host cores (tools/pin_newton_oracle.py
+    --max-iterations 8, fixture pin_oracle_l12_miehe_it8.json; the whole
+    82-iteration oracle solve takes about an hour) -- Lanczos ranges on every
+    level, the first V-cycle (sketch) and the residual history against the
+    device solve's."""
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "pin_oracle_l12_miehe_it8.json")) as f:
+        d = json.load(f)
+    st, x = _state(12, "miehe")
+    n = st.n_scalar
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    for l, r in d["ranges"].items():
+        got = gmg.ranges[int(l)]
+        assert np.allclose([got["uu"][0], got["uu"][1], got["phiphi"][0], got["phiphi"][1]], r,
+                           rtol=1e-10, atol=0), l
+    xd = torch.from_numpy(x).cuda()
+    want = {k: np.asarray(v) for k, v in d["vcycle_sketch"].items()}
+    assert sketch_rel(sketch(_np(gmg.apply(xd)), n), want) <= TOL
+    del xd
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    res = P.gmres_solve(P.JacobianOperator(st), torch.from_numpy(rhs).cuda(),
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50, max_iterations=8),
+                        preconditioner=gmg.apply)
+    h_ref, h_got = np.asarray(d["history"]), np.asarray(res.residual_history)
+    assert res.iterations == 8 and h_got.shape == h_ref.shape
+    # the last entry of both is the true residual of the returned iterate
+    assert np.max(np.abs(h_got - h_ref) / h_ref[0]) <= 1e-10
+
+
 @pytest.mark.parametrize("name", ["pr1_miehe", "pr1_none"])
 def test_pr1_goldens_through_sweep_kernel(name):
     """PR1 (32^2 Q2) is below the sweep kernel's default threshold; force the
