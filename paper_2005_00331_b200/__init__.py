@@ -10,7 +10,7 @@ from .active_set import (ActiveSetParams, ActiveSetSolver, SolveReport, SolverFa
                          converged, determine_active_set, lumped_mass_diagonal)
 from .basis import LANE_WIDTHS, MaterialParams, ShapeData, shape_data
 from .krylov import GmresResult, KrylovConfig, gmres_solve
-from .mesh import DofMap, MeshHierarchy, MeshLevel, build_hierarchy
+from .mesh import ConstraintSet, DofMap, MeshHierarchy, MeshLevel, build_hierarchy
 from .multigrid import (ChebyshevConfig, GmgPreconditioner, TransferOperator,
                         build_prolongation, chebyshev_apply, estimate_lambda_max,
                         estimate_lambda_range)

@@ -114,6 +114,52 @@ class DofMap:
 
 
 @dataclass
+@dataclass
+class ConstraintSet:
+    """Dirichlet dofs with prescribed values and the active phi dofs, in full
+    (3n) dof ids (src/mesh_hierarchy.py:110-153).  Duplicate Dirichlet dofs
+    must agree on their value (they are merged); active dofs must be phi dofs.
+    The device path keeps the same information as per-node flag bytes."""
+
+    dirichlet_dofs: np.ndarray
+    dirichlet_values: np.ndarray
+    active_dofs: np.ndarray
+    n_total: int
+
+    def __post_init__(self):
+        d = np.asarray(self.dirichlet_dofs, dtype=np.int64)
+        v = np.asarray(self.dirichlet_values, dtype=np.float64)
+        order = np.argsort(d, kind="stable")
+        d, v = d[order], v[order]
+        if d.size:
+            first = np.r_[True, d[1:] != d[:-1]]
+            # every repeated dof must carry exactly the value of its first occurrence
+            start = np.flatnonzero(first)
+            owner = np.repeat(start, np.diff(np.r_[start, d.size]))
+            if np.any(v != v[owner]):
+                raise ValueError("conflicting Dirichlet values for the same dof")
+            d, v = d[first], v[first]
+        self.dirichlet_dofs, self.dirichlet_values = d, v
+        a = np.asarray(self.active_dofs, dtype=np.int64)
+        n = self.n_total // 3
+        if a.size and (a.min() < 2 * n or a.max() >= self.n_total):
+            raise ValueError("active-set entries must be phi-component dofs")
+        self.active_dofs = a
+
+    def kind_of(self, dof: int) -> str:
+        if np.any(self.dirichlet_dofs == dof):
+            return "dirichlet"
+        if np.any(self.active_dofs == dof):
+            return "active"
+        return "free"
+
+    def constrained_mask(self) -> np.ndarray:
+        mask = np.zeros(self.n_total, dtype=bool)
+        mask[self.dirichlet_dofs] = True
+        mask[self.active_dofs] = True
+        return mask
+
+
 class MeshHierarchy:
     """Levels 0..max_level (src/mesh_hierarchy.py:279-338)."""
 

@@ -31,7 +31,8 @@ collect_ignore_glob = [] if _enabled() else ["_vendor/*"]
 
 def _install_shim():
     import paper_2005_00331_b200 as P
-    from paper_2005_00331_b200 import basis, krylov, mesh, multigrid, operator
+    from paper_2005_00331_b200 import active_set, basis, io, krylov, mesh, multigrid, operator
+    from paper_2005_00331_b200 import simulation
     pkg = types.ModuleType("fracturekit")
     pkg.__path__ = []
     sys.modules["fracturekit"] = pkg
@@ -53,7 +54,8 @@ def _install_shim():
     sys.modules["fracturekit.material_model"] = mm
     spec.loader.exec_module(mm)
     mods = {"pff_operator": operator, "multigrid": multigrid, "krylov": krylov,
-            "mesh_hierarchy": mesh, "tensor_basis": basis, "material_model": mm}
+            "mesh_hierarchy": mesh, "tensor_basis": basis, "material_model": mm,
+            "active_set_solver": active_set, "simulation_driver": simulation, "io": io}
     for name, mod in mods.items():
         sys.modules[f"fracturekit.{name}"] = mod
         setattr(pkg, name, mod)

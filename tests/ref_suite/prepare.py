@@ -3,7 +3,10 @@ tests/ref_suite/_vendor/ (git-ignored; run in the build container, where
 /root/reference exists; the copies travel to the GPU box with the snapshot).
 
 Provenance: fracturekit 0.1.0, /root/reference/pkg/tests/test_pff_operator.py,
-test_multigrid.py, test_krylov.py, unmodified; and its point-wise tensor algebra
+test_multigrid.py, test_krylov.py, test_mesh_hierarchy.py,
+test_active_set_solver.py, test_simulation_driver.py, unmodified
+(test_tensor_basis.py and test_material_model.py test the reference's numpy
+batch helpers and point-wise algebra, out of scope for the drop-in); and its point-wise tensor algebra
 src/fracturekit/material_model.py, which those tests use as their oracle
 (out of scope for the product, test infrastructure here).
 Nothing under _vendor/ is product code or committed; conftest.py maps the
@@ -23,6 +26,9 @@ VENDOR = os.path.join(HERE, "_vendor")
 FILES = {"tests/test_pff_operator.py": "test_pff_operator.py",
          "tests/test_multigrid.py": "test_multigrid.py",
          "tests/test_krylov.py": "test_krylov.py",
+         "tests/test_mesh_hierarchy.py": "test_mesh_hierarchy.py",
+         "tests/test_active_set_solver.py": "test_active_set_solver.py",
+         "tests/test_simulation_driver.py": "test_simulation_driver.py",
          "src/fracturekit/material_model.py": "ref_material_model.py"}
 
 
