@@ -114,7 +114,6 @@ class DofMap:
 
 
 @dataclass
-@dataclass
 class ConstraintSet:
     """Dirichlet dofs with prescribed values and the active phi dofs, in full
     (3n) dof ids (src/mesh_hierarchy.py:110-153).  Duplicate Dirichlet dofs
@@ -160,6 +159,7 @@ class ConstraintSet:
         return mask
 
 
+@dataclass
 class MeshHierarchy:
     """Levels 0..max_level (src/mesh_hierarchy.py:279-338)."""
 
