@@ -34,6 +34,65 @@ class MeshLevel:
     def n_cells(self) -> int:
         return self.cells_per_side ** 2
 
+    # -- the vertex mesh (src/mesh_hierarchy.py:36-59, 228-276): host-side
+    # geometry for topology checks and dumps; the kernels use the closed form
+    @cached_property
+    def _q1(self) -> "DofMap":
+        return DofMap(self.level_index, 1)
+
+    @cached_property
+    def vertices(self) -> np.ndarray:
+        return self._q1.coords
+
+    @cached_property
+    def cells(self) -> np.ndarray:
+        """(n_cells, 4) vertex ids, counter-clockwise from the lower-left."""
+        return np.ascontiguousarray(self._q1.conn[:, [0, 1, 3, 2]])
+
+    @cached_property
+    def boundary_edges(self) -> dict:
+        """tag -> (n_edges, 2) vertex pairs along the boundary; left-boundary
+        edges above the slit use the upper copy of the slit's end vertex."""
+        q = self._q1
+        n1, ng, im = q.nodes_per_side, q.n_grid, q.i_mid
+        k = np.arange(n1, dtype=np.int64)
+        runs = {"bottom": k, "top": (n1 - 1) * n1 + k, "left": k * n1, "right": k * n1 + n1 - 1}
+        out = {}
+        for tag in BOUNDARY_TAGS:
+            e = np.column_stack([runs[tag][:-1], runs[tag][1:]])
+            if tag == "left" and q.n_dup:
+                e[im:, 0] = np.where(e[im:, 0] == im * n1, ng, e[im:, 0])
+            out[tag] = e
+        return out
+
+    @cached_property
+    def _slit_edges(self):
+        q = self._q1
+        if not q.n_dup:
+            z = np.empty((0, 2), dtype=np.int64)
+            return z, z
+        tip = q.i_mid * q.nodes_per_side + q.i_mid
+        lo = np.append(q.slit_lower, tip)
+        up = np.append(q.slit_upper, tip)
+        return (np.column_stack([lo[:-1], lo[1:]]).astype(np.int64),
+                np.column_stack([up[:-1], up[1:]]).astype(np.int64))
+
+    @property
+    def slit_edges_lower(self) -> np.ndarray:
+        return self._slit_edges[0]
+
+    @property
+    def slit_edges_upper(self) -> np.ndarray:
+        return self._slit_edges[1]
+
+    def edge_cell_counts(self) -> dict:
+        """Undirected edge (vertex pair) -> number of cells referencing it."""
+        c = self.cells
+        e = np.stack([c, np.roll(c, -1, axis=1)], axis=2).reshape(-1, 2)
+        e.sort(axis=1)
+        keys, counts = np.unique(e, axis=0, return_counts=True)
+        return {(int(a), int(b)): int(n) for (a, b), n in zip(keys, counts)}
+
 
 @dataclass(frozen=True)
 class DofMap:
@@ -185,6 +244,24 @@ class MeshHierarchy:
         dm = self.dof_map(level)
         nodes = dm.boundary_nodes[tag]
         return np.sort(np.concatenate([nodes, dm.n_scalar + nodes]))
+
+    def slit_pairs(self, level: int) -> np.ndarray:
+        """(lower, upper) full dof ids of every duplicated slit node, per
+        component (src/mesh_hierarchy.py:304-314)."""
+        if level < 1:
+            raise ValueError("slit duplication starts at level 1")
+        dm = self.dof_map(level)
+        pairs = [np.column_stack([c * dm.n_scalar + dm.slit_lower, c * dm.n_scalar + dm.slit_upper])
+                 for c in range(3)]
+        return np.concatenate(pairs).astype(np.int64)
+
+    def dump_level(self, level: int) -> str:
+        """One record per line: header, vertices, cells (src/mesh_hierarchy.py:340-349)."""
+        mesh, dm = self.level(level), self.dof_map(level)
+        out = [f"level {level} cells {mesh.n_cells} scalar_dofs {dm.n_scalar}"]
+        out += [f"vertex {i} {x:.12g} {y:.12g}" for i, (x, y) in enumerate(mesh.vertices)]
+        out += ["cell {} {}".format(i, " ".join(str(int(v)) for v in c)) for i, c in enumerate(mesh.cells)]
+        return "\n".join(out) + "\n"
 
     def injection(self, fine_level: int) -> np.ndarray:
         """coarse = fine[injection(fine_level)] (src/mesh_hierarchy.py:316-338)."""

@@ -225,3 +225,20 @@ def test_scaling_model_uses_the_slab_rule():
     t = [SM.model(d, n)["gmres_s"] for n in (1, 2, 4, 8)]
     assert t[0] > t[1] > t[2] > t[3]
     assert SM.slab_levels(12, 8) == [12, 11, 10, 9, 8, 7]
+
+
+@pytest.mark.parametrize("level", [1, 2, 3])
+def test_vertex_mesh_topology(level):
+    """MeshLevel's vertex mesh (src/mesh_hierarchy.py:36-59): boundary and slit
+    edges belong to one cell, every other edge to two; dump_level has one
+    record per line."""
+    h = P.build_hierarchy(max(level, 2), 1)
+    mesh = h.level(level)
+    counts = mesh.edge_cell_counts()
+    single = {tuple(sorted(map(int, e))) for es in mesh.boundary_edges.values() for e in es}
+    single |= {tuple(sorted(map(int, e))) for e in mesh.slit_edges_lower}
+    single |= {tuple(sorted(map(int, e))) for e in mesh.slit_edges_upper}
+    for e, c in counts.items():
+        assert c == (1 if e in single else 2), e
+    assert len(h.dump_level(level).strip().split("\n")) == 1 + len(mesh.vertices) + mesh.n_cells
+    assert h.slit_pairs(level).shape == (3 * h.dof_map(level).n_dup, 2)
