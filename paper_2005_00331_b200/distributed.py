@@ -39,6 +39,7 @@ from .operator import LinearizationState
 from .parallel import SlabPartition, SlabState
 
 _NCOMP = {_lib.MODE_FULL: 3, _lib.MODE_UU: 2, _lib.MODE_PHIPHI: 1, _lib.MODE_PHIROW: 3}
+FUSE_CHEB = True   # slab levels run the fused Chebyshev steps (pff_apply_cheb_ex)
 
 
 class _Comm:
@@ -156,7 +157,7 @@ class DistributedGmg:
             L.inv = {k2: torch.where(self._owned(part, 2 if k2 == "uu" else 1), 1.0 / torch.where(
                 d == 0, torch.ones_like(d), d), zero) for k2, d in L.diag.items()}
             z = lambda m: torch.zeros(m * ln, dtype=torch.float64, device=self.device)  # noqa: E731
-            L.w = dict(res=z(3), resphi=z(1), d=z(2), acc=z(2), cr=z(2), r=z(3), z=z(3))
+            L.w = dict(res=z(3), resphi=z(1), d=z(2), d2=z(2), acc=z(2), cr=z(2), r=z(3), z=z(3))
             self.lv.append(L)
             L.ranges = {"uu": self._lanczos(L, _lib.MODE_UU, "uu", 0),
                         "phiphi": self._lanczos(L, _lib.MODE_PHIPHI, "phiphi", 1)}
@@ -229,7 +230,26 @@ class DistributedGmg:
         sigma1 = theta / delta
         st = stream_handle()
         call("pff_cheb_init", nb, ptr(inv), ptr(rhs), theta, ptr(d), ptr(acc), 0, st)
-        if sweeps > 1:
+        if sweeps > 1 and FUSE_CHEB:
+            # each step in ONE sweep over the slab after the direction's ghost-row
+            # exchange: cr = (rhs | cr) - G d, d' = c1 d + c2 D^-1 cr, acc += d'
+            # (pff_apply_cheb_ex: the single-GPU cycle's fused form, bitwise the
+            # unfused steps); d ping-pongs between two buffers
+            ncomp = _NCOMP[mode]
+            d_in, d_out = d, L.w["d2"][:nb]
+            src = rhs
+            rho_old = 1.0 / sigma1
+            h = L.st.handle()
+            for k in range(1, sweeps):
+                rho = 1.0 / (2.0 * sigma1 - rho_old)
+                L.st.halo.exchange(d_in, ncomp)
+                call("pff_apply_cheb_ex", h, mode, ptr(d_in), ptr(d_out), ptr(src), ptr(cr),
+                     ptr(inv), ptr(acc), rho * rho_old, 2.0 * rho / delta,
+                     _lib.CHEB_LAST if k == sweeps - 1 else 0, st)
+                rho_old = rho
+                src = cr
+                d_in, d_out = d_out, d_in
+        elif sweeps > 1:
             L.st.apply_into(mode, d, cr, rhs)
             rho_old = 1.0 / sigma1
             for k in range(1, sweeps):
@@ -336,14 +356,20 @@ def distributed_gmres(gmg: DistributedGmg, rhs: torch.Tensor, config: KrylovConf
             z = gmg.apply_into(V[j], zbuf)
             w = V[j + 1]
             fine.apply_into(_lib.MODE_FULL, z, w)
-            hcol = np.zeros(j + 2)
-            for _ in range(2):   # CGS2
+            # CGS2: both passes' coefficients and the new norm stay on the device
+            # until ONE host read per iteration (all-reduces are stream-ordered)
+            hsum = torch.zeros(j + 2, dtype=torch.float64, device=dev)
+            for _ in range(2):
                 call("pff_mdot", n, j + 1, ptr(V), n, ptr(w), ptr(parts), ptr(hbuf), st)
                 h = gmg.comm.sum_(hbuf[: j + 1].clone())
                 neg = -h
                 call("pff_combine", n, j + 1, ptr(V), n, ptr(neg), ptr(w), 1, st)
-                hcol[: j + 1] += h.cpu().numpy()
-            h_next = float(np.sqrt(gmg.dot(w, w)))
+                hsum[: j + 1] += h
+            call("pff_dot", n, ptr(w), ptr(w), ptr(gmg._scratch), ptr(gmg._dout), st)
+            hsum[j + 1] = gmg._dout[0]
+            gmg.comm.sum_(hsum[j + 1:])
+            hcol = hsum.cpu().numpy()
+            h_next = float(np.sqrt(hcol[j + 1]))
             hcol[j + 1] = h_next
             H[: j + 2, j] = hcol
             for i in range(j):
