@@ -642,8 +642,9 @@ def newton_step_distributed(args, P, torch, ws, rank, dev):
     t = torch.tensor([t_setup, t_gmres], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_setup, t_gmres = (float(v) for v in t.tolist())
-    return {"config": f"{2 ** level}^2 Q2 notch over {ws} slabs, levels 2..{level} "
-                      f"(finest in slabs, coarser agglomerated), sweeps=3, restart 50, rtol 1e-8",
+    return {"config": f"{'configs[4]: ' if level == 12 else ''}{2 ** level}^2 Q2 notch over {ws} "
+                      f"slabs, levels 2..{level} (levels {gmg.slab_levels[-1]}..{level} in slabs, "
+                      f"{gmg.agg_level}..2 agglomerated), sweeps=3, restart 50, rtol 1e-8",
             "split": args.split, "iterations": res.iterations, "converged": res.converged,
             "setup_s": round(t_setup, 4), "gmres_s": round(t_gmres, 4),
             "total_s": round(t_setup + t_gmres, 4), "orthogonalisation": "CGS2",
