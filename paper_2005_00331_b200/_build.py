@@ -9,8 +9,11 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_obj")
-LIB = os.path.join(HERE, "libpff_b200.so")
+# PFF_BUILD_TAG=debug (with PFF_NVCC_EXTRA=-DPFF_DEBUG_CHECKS) builds a side
+# library libpff_b200_debug.so for tools/debug_checks.sh; the default build is untouched
+_TAG = os.environ.get("PFF_BUILD_TAG", "")
+OBJ = os.path.join(HERE, "_obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(HERE, "libpff_b200" + (f"_{_TAG}" if _TAG else "") + ".so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-Xcompiler", "-fopenmp"] + os.environ.get("PFF_NVCC_EXTRA", "").split()   # OpenMP: host-side Ritz values

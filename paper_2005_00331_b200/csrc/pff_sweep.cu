@@ -277,11 +277,15 @@ k_sweep_q2(const SweepArgs A) {
                 if (!U::used(f)) continue;
                 const int ae = lo - ((lo + fmis[f]) & 1);
                 const int be = hi + ((hi + fmis[f]) & 1);
+                // a misaligned field base starts the copy one element early: inside the
+                // same 16-byte granule of the (aligned) allocation
+                PFF_DCHECK(be - ae <= RW && ae >= -1 && (ae >= 0 || fmis[f]));
                 bulk_g2s(W.v[slot][U::slot(f)], A.fld[f] + ae, (unsigned)(8 * (be - ae)), bar);
                 bytes += (unsigned)(8 * (be - ae));
             }
             const int ab = lo - ((lo + flmis) & 15);
             const int bb = hi + ((16 - ((hi + flmis) & 15)) & 15);
+            PFF_DCHECK(bb - ab <= FW && ab >= -15 && (ab >= 0 || flmis));
             bulk_g2s(W.f[slot], A.flags + ab, (unsigned)(bb - ab), bar);
             return bytes + (unsigned)(bb - ab);
         };
@@ -308,9 +312,15 @@ k_sweep_q2(const SweepArgs A) {
             }
         };
         auto val = [&](int b, int f, int k) -> double {
+            // (the first strip's halo lane -- cell -1, inactive, its results zeroed --
+            // reads up to 2 entries below the staged row; still inside shared memory)
+            PFF_DCHECK(vo[b][U::slot(f)] + k >= -2 && vo[b][U::slot(f)] + k < RW);
             return W.v[sb[b]][U::slot(f)][vo[b][U::slot(f)] + k];
         };
-        auto flag = [&](int b, int k) -> uint8_t { return W.f[sb[b]][fo[b] + k]; };
+        auto flag = [&](int b, int k) -> uint8_t {
+            PFF_DCHECK(fo[b] + k >= -2 && fo[b] + k < FW);
+            return W.f[sb[b]][fo[b] + k];
+        };
         // the upper cell row reads the upper slit copies of node row i_mid (b = 0)
         auto patch_slit = [&]() {
             for (int k = lane; k < SW_COLS; k += SW_LANES) {

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(32) k_sweep_q4(const Sweep4Args A) {
         const bool owner = active && c > 0;
 
         auto issue_qblock = [&](int cy) {
+            PFF_DCHECK(cy >= 0 && cy < ns);
             const double* src = A.qtile + ((int64_t)strip * ns + cy) * A.qblock + U::Q0 * QA4;
             mbar_expect_tx(&W.bar, (unsigned)(NQ * QA4 * 8));
             bulk_g2s(W.q, src, (unsigned)(NQ * QA4 * 8), &W.bar);
@@ -294,6 +295,8 @@ __global__ void __launch_bounds__(32) k_sweep_q4(const Sweep4Args A) {
                         if (U::used(k)) cp_async8(&W.st[sb][U::slot(k) * 5 + a][lane], A.fld[k] + gid);
                 }
                 const uint8_t* w0 = A.flags + (g0 & ~3);
+                // (flag buffers carry 8 bytes of padding: LinearizationState._sync_flags)
+                PFF_DCHECK((g0 & ~3) + 8 <= (int)m.n + 8 && (g4 & ~3) + 4 <= (int)m.n + 8);
                 cp_async4(&W.fw[sb][0][lane], w0);
                 cp_async4(&W.fw[sb][1][lane], w0 + 4);
                 cp_async4(&W.fw[sb][2][lane], A.flags + (g4 & ~3));
@@ -316,7 +319,10 @@ __global__ void __launch_bounds__(32) k_sweep_q4(const Sweep4Args A) {
             }
             return fl;
         };
-        auto staged = [&](int sb, int f, int a) -> double { return W.st[sb][U::slot(f) * 5 + a][lane]; };
+        auto staged = [&](int sb, int f, int a) -> double {
+            PFF_DCHECK(U::used(f) && sb >= 0 && sb < 2 && a >= 0 && a < 5);
+            return W.st[sb][U::slot(f) * 5 + a][lane];
+        };
 
         stage_row(cstart, 0);
         if (lane == 0) issue_qblock(cstart);

@@ -317,7 +317,10 @@ class LinearizationState:
             d = self._dir.device()
             a = self._act.device()
             if self._flags is None:
-                self._flags = torch.empty(d.numel(), dtype=torch.uint8, device=d.device)
+                # 8 bytes of padding: the Q4 sweep stages flag bytes as aligned 4-byte
+                # words (cp.async), whose last word may extend past the final node
+                buf = torch.zeros(d.numel() + 8, dtype=torch.uint8, device=d.device)
+                self._flags = buf[:d.numel()]
             call("pff_flags", d.numel(), ptr(d), ptr(a), ptr(self._flags), 0, stream_handle())
             self._flags_stamp = (self._dir.stamp, self._act.stamp)
         return self._flags
