@@ -102,7 +102,7 @@ int pff_level_set_window(pff_level* L, int cy_begin, int cy_end);
 int pff_level_window(const pff_level* L, int64_t* rows);
 
 /* Bind the linearisation point: U (3n), phi_tilde (n), flags (n bytes, readable
- * for 8 bytes past the end: the Q4 sweep stages them as aligned words) and a
+ * for 16 bytes past the end: the sweeps stage them in aligned units) and a
  * caller-allocated q-point cache of pff_level_qcache_len() doubles (q-point
  * state, the Q2 tangent tiles, and the element-vector scratch that the generic
  * application and the restriction INTO this level use -- so a level's

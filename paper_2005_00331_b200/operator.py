@@ -317,9 +317,10 @@ class LinearizationState:
             d = self._dir.device()
             a = self._act.device()
             if self._flags is None:
-                # 8 bytes of padding: the Q4 sweep stages flag bytes as aligned 4-byte
-                # words (cp.async), whose last word may extend past the final node
-                buf = torch.zeros(d.numel() + 8, dtype=torch.uint8, device=d.device)
+                # 16 bytes of padding: the sweeps stage flag bytes in aligned units
+                # (Q2: 16-byte TMA rows, Q4: 4-byte cp.async words) that may extend
+                # past the final node
+                buf = torch.zeros(d.numel() + 16, dtype=torch.uint8, device=d.device)
                 self._flags = buf[:d.numel()]
             call("pff_flags", d.numel(), ptr(d), ptr(a), ptr(self._flags), 0, stream_handle())
             self._flags_stamp = (self._dir.stamp, self._act.stamp)

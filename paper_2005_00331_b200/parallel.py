@@ -270,7 +270,9 @@ class SlabState:
         flags = (np.asarray(dirichlet, dtype=np.uint8) | (np.asarray(active, dtype=np.uint8) << 1))
         self.U = self._local(U, 3, np.float64)
         self.pt = self._local(phi_tilde, 1, np.float64)
-        self.flags = self._local(flags, 1, np.uint8)
+        fl = self._local(flags, 1, np.uint8)   # + 16 bytes: the sweep's 16-byte flag-row copies
+        self.flags = torch.zeros(fl.numel() + 16, dtype=torch.uint8, device=self.device)[:fl.numel()]
+        self.flags.copy_(fl)
         self._handle = None
         self._qc = None
 
