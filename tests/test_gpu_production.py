@@ -363,3 +363,36 @@ def test_q4_sweep_matches_generic_all_modes(split, level, rows, monkeypatch):
     y1 = P.apply_jacobian(st, xd)
     y2 = P.apply_jacobian(st, xd)
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("p,level,split", [(4, 6, "miehe"), (4, 6, "none"), (3, 6, "miehe"),
+                                           (1, 7, "miehe")])
+def test_other_degrees_vcycle_and_gmres_vs_oracle(p, level, split):
+    """Q4 hierarchies mix the write-once Q4 sweep (the residual and phi-row
+    applications on >= 64^2 levels) with the cooperative kernel (the fused
+    Chebyshev forms, small levels); Q3 and Q1 run the cooperative kernel
+    throughout.  V-cycle <= 1e-12 per block and GMRES(50) iterations against the
+    oracle (src/multigrid.py:201-344, src/krylov.py:37-119), notch inputs."""
+    nt = O.max_threads()
+    st, x = _state(level, split, p=p)
+    ost, _ = O.baseline_state(p, level, split, seed=0, notch=True)
+    ost.refresh_cache(nthreads=nt)
+    n = st.n_scalar
+    gmg = P.GmgPreconditioner(st.hierarchy, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
+    gmg.setup(st)
+    og = O.Gmg(p, level, coarse_level=2, cheb=O.ChebCfg(sweeps=3), nthreads=nt)
+    og.setup(ost)
+    for l in range(2, level + 1):
+        a, b = gmg.ranges[l], og.ranges[l]
+        assert np.allclose([a["uu"][0], a["uu"][1], a["phiphi"][0], a["phiphi"][1]],
+                           [b["uu"][0], b["uu"][1], b["phiphi"][0], b["phiphi"][1]], rtol=1e-10, atol=0)
+    assert max(block_rel(_np(gmg.apply(x)), og.apply(x), n)) <= TOL
+    rhs = x.copy()
+    rhs[st.constrained_mask()] = 0.0
+    res = P.gmres_solve(P.JacobianOperator(st), rhs,
+                        P.KrylovConfig(relative_tolerance=1e-8, restart=50),
+                        preconditioner=gmg.apply)
+    ores = O.gmres(lambda v: O.apply_jacobian(ost, v, nt), rhs, tol=1e-8, restart=50,
+                   preconditioner=og.apply)
+    assert abs(res.iterations - ores.iterations) <= 1
+    assert max(block_rel(_np(res.solution), ores.solution, n)) <= 1e-8
