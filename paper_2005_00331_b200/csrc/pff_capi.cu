@@ -342,8 +342,21 @@ int pff_apply_host(const pff_level* h, int mode, const double* xh, double* yh, d
     cudaEvent_t* ev_in = g_pipe.ev;            // [K]: chunk k's inputs on the device
     cudaEvent_t* ev_done = g_pipe.ev + 64;     // [K]: chunk k's sweep done
     cudaEvent_t ev_start = g_pipe.ev[192], ev_end = g_pipe.ev[193];
+    // PFF_PIPE_1D=1: one 1-D copy per component instead of one 2-D copy (measurement knob)
+    static const bool one_d = [] {
+        const char* e = std::getenv("PFF_PIPE_1D");
+        return e && e[0] == '1';
+    }();
     auto copy = [&](double* dst, const double* src, int64_t a, int64_t cnt, int nc, cudaStream_t s) {
         const size_t pitch = (size_t)n * sizeof(double);
+        if (one_d) {
+            for (int c = 0; c < nc; ++c) {
+                const cudaError_t ce = cudaMemcpyAsync(dst + a + c * n, src + a + c * n,
+                                                       (size_t)cnt * sizeof(double), cudaMemcpyDefault, s);
+                if (ce != cudaSuccess) return ce;
+            }
+            return cudaSuccess;
+        }
         return cudaMemcpy2DAsync(dst + a, pitch, src + a, pitch, (size_t)cnt * sizeof(double),
                                  (size_t)nc, cudaMemcpyDefault, s);
     };
