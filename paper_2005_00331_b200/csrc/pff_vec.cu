@@ -210,19 +210,23 @@ k_mdot_final(const double* __restrict__ part, double* out) {
 // the MGS coefficients follow exactly from h_i = r_i - sum_{k<i} (v_i.v_k) h_k
 // (the recurrence MGS evaluates with updated w), then one pass forms
 // w -= V h and |w|^2.  4 basis rows per pass, fixed grid -> deterministic.
+#ifndef LSMGS_ROWS
+#define LSMGS_ROWS 4   // basis rows per pass of the low-sync partials (A/B knob at build time)
+#endif
 __global__ void __launch_bounds__(RED_THREADS)
 k_lsmgs_partials(int64_t n, int j, const double* __restrict__ V, int64_t ldv,
                  const double* __restrict__ w, double* __restrict__ part) {
+    constexpr int RR = LSMGS_ROWS;
     const double* vj = V + (int64_t)j * ldv;
-    for (int i0 = 0; i0 <= j; i0 += MDOT_ROWS) {
-        double ar[MDOT_ROWS], at[MDOT_ROWS];
+    for (int i0 = 0; i0 <= j; i0 += RR) {
+        double ar[RR], at[RR];
 #pragma unroll
-        for (int r = 0; r < MDOT_ROWS; ++r) ar[r] = at[r] = 0.0;
+        for (int r = 0; r < RR; ++r) ar[r] = at[r] = 0.0;
         for (int64_t e = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; e < n;
              e += (int64_t)RED_BLOCKS * RED_THREADS) {
             const double we = w[e], ve = vj[e];
 #pragma unroll
-            for (int r = 0; r < MDOT_ROWS; ++r)
+            for (int r = 0; r < RR; ++r)
                 if (i0 + r <= j) {
                     const double vi = V[(int64_t)(i0 + r) * ldv + e];
                     ar[r] = fma(vi, we, ar[r]);
@@ -230,7 +234,7 @@ k_lsmgs_partials(int64_t n, int j, const double* __restrict__ V, int64_t ldv,
                 }
         }
 #pragma unroll
-        for (int r = 0; r < MDOT_ROWS; ++r) {
+        for (int r = 0; r < RR; ++r) {
             if (i0 + r > j) break;
             const double sr = block_sum(ar[r]);
             const double st = block_sum(at[r]);

@@ -426,7 +426,7 @@ def _run(state: LinearizationState, mode: int, v, n_in: int, n_out: int):
     state._check_cache()
     if (isinstance(v, torch.Tensor) and not v.is_cuda and v.is_pinned()
             and v.dtype == torch.float64 and v.is_contiguous() and v.numel() == n_in
-            and state.hierarchy.degree == 2 and state.level >= 6):
+            and state.hierarchy.degree == 2 and state.uses_sweep_kernel()):
         return _pipelined(state, mode, v.reshape(-1))
     x, was_np = as_device(v, n_in)
     out = torch.empty(n_out, dtype=torch.float64, device=x.device)
