@@ -12,6 +12,8 @@
 // into the cell's coarse nodes, in four colour passes (cx, cy parities) so
 // no two threads touch a coarse node at once -- no atomics, fixed order.
 // Injection restates src/mesh_hierarchy.py:316-338 / pff_operator.py:380-400.
+#include <cstdlib>
+
 #include "pff_internal.cuh"
 
 namespace pff {
@@ -335,6 +337,120 @@ __global__ void k_restrict_gather(Mesh mc, Win wc, const double* __restrict__ ev
     for (int k = 0; k < 3; ++k) xc[k * nloc + t] = acc[k];
 }
 
+// Q2 restriction as a direct per-coarse-node gather (whole-mesh levels): r_c =
+// P^T r_f with the tensor-product weights of the reference's P rows
+// (src/multigrid.py:44-120; first-visited-cell owners, |w| > 1e-14 kept) read
+// off the 1-D embedding table: coarse even index 2k gathers fine offsets
+// -3, -1, 0, +1, +3 (weights E[0][1][2], E[1][1][2], E[1][2][2] -- E[0][0][0]
+// at k = 0 --, E[0][1][0], E[1][1][0]), odd index 2k+1 offsets -1, 0, +1
+// (E[0][1][1], E[0][2][1], E[1][1][1]).  Every other 1-D weight of a Q2 row is
+// at most ~1e-16 and dropped by the reference's filter, so filtering the
+// product equals filtering the factors.  The slit: the coarse row i_mid's
+// lower copies (grid ids) gather the fine rows below and the fine slit row's
+// lower copies, its upper copies the fine rows above and the fine upper copies
+// (owned by the upper cell row, weight E[0][0][0]); the tip and the right half
+// gather both.  No element vectors, no scratch, write-once; the fine residual
+// was just written and is mostly L2-resident.
+// the (up to) five 1-D taps of coarse index I: fixed slots, zero weight when
+// absent (compile-time indexed: registers, no local memory)
+struct W1 {
+    int off[5];
+    double w[5];
+};
+
+__device__ __forceinline__ W1 taps_q2(const Embed& E, int I, int np1) {
+    W1 t;
+    const bool even = (I & 1) == 0;
+    const int o[5] = {-3, -1, 0, 1, 3};
+    const double we[5] = {E.E[0][1][2], E.E[1][1][2], I > 0 ? E.E[1][2][2] : E.E[0][0][0],
+                          E.E[0][1][0], E.E[1][1][0]};
+    const double wo[5] = {0.0, E.E[0][1][1], E.E[0][2][1], E.E[1][1][1], 0.0};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = 2 * I + o[k];
+        double w = even ? we[k] : wo[k];
+        if (i < 0 || i >= np1 || !(fabs(w) > 1e-14)) w = 0.0;
+        t.off[k] = (i < 0 || i >= np1) ? 0 : o[k];   // absent taps read a valid index
+        t.w[k] = w;
+    }
+    return t;
+}
+
+__global__ void __launch_bounds__(256)
+k_restrict_direct_q2(Mesh mf, Mesh mc, Embed E, const double* __restrict__ yf,
+                     double* __restrict__ xc, const uint8_t* __restrict__ flags_c, int zero_cons) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mc.n) return;
+    const int np1c = (int)mc.np1, np1f = (int)mf.np1, imc = (int)mc.i_mid, imf = (int)mf.i_mid;
+    int I, J, kind;   // kind 0: grid node, 1: lower copy (row i_mid, left), 2: upper copy
+    if (c < mc.n_grid) {
+        J = (int)(c / np1c);
+        I = (int)(c - (int64_t)J * np1c);
+        kind = (mc.level >= 1 && J == imc && I < imc) ? 1 : 0;
+    } else {
+        I = (int)(c - mc.n_grid);
+        J = imc;
+        kind = 2;
+    }
+    const W1 tx = taps_q2(E, I, np1f), ty = taps_q2(E, J, np1f);
+    const bool slit = mc.level >= 1 && J == imc;
+    double acc[3] = {0.0, 0.0, 0.0};
+    const double* y1 = yf + mf.n;
+    const double* y2 = yf + 2 * mf.n;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        const int oy = ty.off[b];
+        const double wy = ty.w[b];
+        if (wy == 0.0) continue;
+        const int j = 2 * J + oy;
+        // which copies of fine row j this coarse node sees
+        if (slit && kind == 1 && oy > 0) continue;   // lower copy: rows below + the slit row
+        if (slit && kind == 2 && oy < 0) continue;   // upper copy: rows above + the slit row
+        const bool slit_row = slit && oy == 0;
+        double rx[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            const double w = tx.w[a];
+            if (w == 0.0) continue;
+            const int i = 2 * I + tx.off[a];
+            if (slit_row && i < imf) {
+                // the fine slit row left of the tip: lower copy (grid id, owned by the
+                // lower cell: the row's weight wy) and upper copy (n_grid + i, owned by
+                // the upper cell at t = 0: weight E[0][0][0])
+                const int64_t gl = (int64_t)j * np1f + i, gu = mf.n_grid + i;
+                if (kind != 2) {
+                    rx[0] = fma(w * wy, yf[gl], rx[0]);
+                    rx[1] = fma(w * wy, y1[gl], rx[1]);
+                    rx[2] = fma(w * wy, y2[gl], rx[2]);
+                }
+                if (kind != 1) {
+                    const double wu = w * E.E[0][0][0];
+                    rx[0] = fma(wu, yf[gu], rx[0]);
+                    rx[1] = fma(wu, y1[gu], rx[1]);
+                    rx[2] = fma(wu, y2[gu], rx[2]);
+                }
+                continue;
+            }
+            const int64_t g = (int64_t)j * np1f + i;
+            const double ww = w * wy;
+            rx[0] = fma(ww, yf[g], rx[0]);
+            rx[1] = fma(ww, y1[g], rx[1]);
+            rx[2] = fma(ww, y2[g], rx[2]);
+        }
+        acc[0] += rx[0];
+        acc[1] += rx[1];
+        acc[2] += rx[2];
+    }
+    if (zero_cons) {
+        const uint8_t f = flags_c[c];
+        if (f & F_DIR) acc[0] = acc[1] = 0.0;
+        if (f & F_ACT) acc[2] = 0.0;
+    }
+    xc[c] = acc[0];
+    xc[mc.n + c] = acc[1];
+    xc[2 * mc.n + c] = acc[2];
+}
+
 // rc[cons_c] = 0 (src/multigrid.py:338)
 __global__ void k_zero_cons3(int64_t n, const uint8_t* __restrict__ flags, double* x) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -417,6 +533,16 @@ cudaError_t launch_restrict(const Level& F, const Level& C, const double* yf, do
     const int crow0 = winc ? C.q_row0() : 0;
     const int64_t nce = winc ? C.local_cells() : C.mesh.n_cells();
     if (zero_cons && !C.flags) return cudaErrorInvalidValue;
+    static const bool direct_ok = [] {
+        const char* e = getenv("PFF_RESTRICT_DIRECT");
+        return !(e && e[0] == '0');
+    }();
+    if (direct_ok && F.mesh.p == 2 && !F.windowed() && !winc && F.mesh.level >= 2) {
+        k_restrict_direct_q2<<<blocks(C.mesh.n), 256, 0, s>>>(F.mesh, C.mesh, F.embed, yf, xc,
+                                                             C.flags, zero_cons);
+        count_launches(1);
+        return cudaGetLastError();
+    }
     if (C.qcache) {   // element vectors in the coarse level's scratch + node gather
         CellColour all;
         all.c = 0;
