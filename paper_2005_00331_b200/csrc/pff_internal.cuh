@@ -90,7 +90,7 @@ struct Level {
     // generic q-point cache (layout [field][k][cell], 6 fields) over the window's cells
     int64_t generic_len() const { return 6 * (int64_t)(mesh.p + 1) * (mesh.p + 1) * local_cells(); }
     // Q2 strip-tiled q-point cache of the sweep kernel (pff_sweep.cu): per
-    // (strip of 31 cells + 1 halo, cell row) one block [array][k][lane]
+    // (strip of 31 cells + 1 halo, cell row) one block [iq][array][jq][lane]
     bool q2_struct = false;   // N[1] = (0,1,0), D[1] = (-1,0,1) at the middle Gauss point
     int min_nside = 64;       // sweep_min_nside() when the level was created (fixes its layout)
     bool sweep_ok() const {   // the sweep kernel stages with 32-bit node indices
@@ -98,7 +98,10 @@ struct Level {
                mesh.n < (int64_t(1) << 31);
     }
     int n_strips() const { return (mesh.nside + 30) / 31; }
-    int tile_nq() const { return miehe ? 10 : 5; }   // tangent (6 | 1) + coupling (3) + pc
+    // Miehe: +-g, +-gamma, cos/sin 2 theta, 2 eigen-frame coupling coefficients, pc;
+    // none: g w, coupling (3), pc
+    int tile_nq() const { return miehe ? 7 : 5; }
+    int tile4_nq() const { return miehe ? 10 : 5; }  // Q4: symmetric tangent (6 | 1) + coupling (3) + pc
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
     int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
     // element-vector scratch of the generic application and of the restriction
@@ -125,7 +128,7 @@ struct Level {
                mesh.n < (int64_t(1) << 31);
     }
     int n_strips4() const { return (mesh.nside + 4) / 5; }
-    int64_t tile4_block() const { return (int64_t)tile_nq() * 25 * 6; }
+    int64_t tile4_block() const { return (int64_t)tile4_nq() * 25 * 6; }
     int64_t tile4_len() const { return sweep4_ok() ? (int64_t)n_strips4() * mesh.nside * tile4_block() : 0; }
     int64_t qcache_len() const {
         return generic_len() + tile_len() + gtan_len() + ev_len() + tile4_len();

@@ -5,19 +5,26 @@
 // expensive, direction-independent q-point physics hoisted into refresh:
 //
 //  * refresh builds a strip-tiled tangent cache: per (strip, cell row) one
-//    contiguous block [array][q-point][lane] holding, with the quadrature
-//    weight w_jq w_iq h^2 folded in, the effective tangent of the reference's
-//    cache_tensors mode (src/_kernels.py:517-548, the solver default of
-//    src/simulation_driver.py:52) as a symmetric 3x3 form (Miehe: 6 arrays;
-//    none: the scalar g(phi~)), the coupling vector dg sigma+ (3) and pc (1).
-//    The application then needs only the direction fields: a q-point costs
-//    ~16 flops of physics instead of re-deriving the split tangent.
+//    block [Gauss column iq][array][jq][lane] holding the direction-independent
+//    part of the reference's cache_tensors mode (src/_kernels.py:517-548, the
+//    solver default of src/simulation_driver.py:52).  none: g(phi~) w, the
+//    weighted coupling vector dg sigma (3) and pc (5 arrays).  Miehe (round 2,
+//    7 arrays instead of the 10 of the symmetric 3x3 form): the split tangent
+//    in the strain eigen-frame is C - (1-g)[lam H_tr tr I + 2 mu diag(H_1, H_2,
+//    beta)], so a q-point stores g, gamma = 1 - (1-g) beta, cos/sin of twice
+//    the eigen-angle, the two eigen-frame coupling coefficients and pc; the
+//    regime (H_tr, H_1, H_2: four cases) rides in the sign bits of g and
+//    gamma.  The application rotates the direction strain into the eigen-frame
+//    and back (+12 FP64 instructions per q-point, -30 % of the tile bytes).
 //  * one warp owns a strip of 31 cell columns and sweeps upward over a chunk
 //    of cell rows; lane 0 recomputes the left neighbour cell (halo column),
 //    the first iteration recomputes the cell row below the chunk (halo row);
-//  * node rows of the direction fields are staged in a 5-row
-//    shared-memory ring and the q-point block in a 2-stage buffer, both by
-//    TMA bulk copies (cp.async.bulk + mbarrier) issued one cell row ahead;
+//  * node rows of the direction fields are staged in a 5-row shared-memory
+//    ring one cell row ahead, the tangent block in three Gauss-column slots
+//    (slot iq is refilled with the next cell row's column as soon as this
+//    row's column iq is consumed: a single-buffered block, 2/3 of a row step
+//    of prefetch distance), all by TMA bulk copies (cp.async.bulk + mbarrier);
+//    ~20-25 KB of shared memory per warp -> 8 warps per SM;
 //  * a cell's right node column goes to lane+1 by shuffle, its top node row
 //    is carried in registers; every dst entry is written exactly once
 //    (deterministic) with the identity rows and the optional fused
@@ -45,12 +52,13 @@ constexpr int RW = 68;                        // doubles per staged row (16-B al
 constexpr int FW = 112;                       // bytes per staged flag row
 constexpr int RING = 5;                       // node-row ring (3 in use + 2 in flight)
 constexpr int QK = 9;                         // q-points per Q2 cell
-constexpr int QARR = QK * SW_LANES;           // doubles per q-point array of a block
+constexpr int QCOL = 3 * SW_LANES;            // doubles per (array, Gauss column) of a block
+constexpr int NBAR = 5;                       // mbarriers: 2 node-row stages + 3 column slots
 
 enum Field { FX = 0, FY, FP, NFIELDS };
 
-// tangent-cache block: [T (NT arrays)][cw0 cw1 cw2][pc]; the modes read a
-// contiguous sub-range of it
+// tangent-cache block, per Gauss column: none [g w][cw0 cw1 cw2][pc]; Miehe
+// [+-g][+-gamma][c2][s2][q1/2][q2/2][pc]; the modes read a contiguous sub-range
 template <int MODE, bool MIEHE>
 struct Use {
     static constexpr bool ux = MODE != MODE_PHIPHI;
@@ -58,12 +66,16 @@ struct Use {
     static constexpr bool DO_UU = MODE == MODE_FULL || MODE == MODE_UU;
     static constexpr bool DO_PP = MODE != MODE_UU;
     static constexpr bool DO_COUP = MODE == MODE_FULL || MODE == MODE_PHIROW;
-    static constexpr int NT = MIEHE ? 6 : 1;            // tangent arrays
-    static constexpr int NQT = NT + 4;                  // arrays of a block
-    static constexpr int Q0 = MODE == MODE_PHIROW ? NT : MODE == MODE_PHIPHI ? NT + 3 : 0;
+    static constexpr int NT = MIEHE ? 4 : 1;            // tangent arrays
+    static constexpr int NCW = MIEHE ? 2 : 3;           // coupling arrays
+    static constexpr int NQT = NT + NCW + 1;            // arrays of a block (7 | 5)
+    // the Miehe phi row needs the eigen-angle too: it starts at c2
+    static constexpr int Q0 = MODE == MODE_PHIROW ? (MIEHE ? 2 : NT)
+                              : MODE == MODE_PHIPHI ? NQT - 1 : 0;
     static constexpr int NQ = MODE == MODE_FULL ? NQT : MODE == MODE_UU ? NT
-                              : MODE == MODE_PHIROW ? 4 : 1;
-    static constexpr int QCW = DO_UU ? NT : 0;          // local index of cw0
+                              : MODE == MODE_PHIROW ? NQT - Q0 : 1;
+    static constexpr int QC2 = 2 - Q0;                  // local index of c2 (Miehe, not PHIPHI)
+    static constexpr int QCW = NT - Q0;                 // local index of the first coupling array
     static constexpr int QPC = NQ - 1;                  // local index of pc
     static constexpr bool used(int f) { return (f == FX || f == FY) ? ux : ph; }
     static constexpr int slot(int f) {
@@ -75,12 +87,15 @@ struct Use {
 };
 
 // (the fused forms keep rhs / D^-1 / acc in registers: nothing else is staged)
-template <int NF, int NQ>
+// CR (column ring): the tangent block single-buffered in three Gauss-column
+// slots, each refilled as soon as it is consumed; otherwise two whole-row
+// stages that ride on the node rows' mbarriers (one wait per row step)
+template <int NF, int NQ, bool CR>
 struct __align__(16) WarpSmem {
-    double q[2][NQ * QARR];                  // tangent-cache blocks, two stages
+    double q[CR ? 3 : 6][NQ * QCOL];         // tangent-cache block(s): [stage][Gauss column]
     alignas(16) double v[RING][NF][RW];      // node-row ring (TMA destinations: 16-B aligned)
     alignas(16) uint8_t f[RING][FW];         // flag rows
-    unsigned long long bar[2];
+    unsigned long long bar[NBAR];            // [0,1] node-row stages, [2+iq] column slots
 };
 
 // Q2 constants of one application, prepared on the host (exact rescalings)
@@ -89,6 +104,9 @@ struct SweepConst {
     double Dh[3][3];   // shape derivatives / h (row 1 is (-1,0,1)/h)
     double ih;         // 1/h
     double cgw[9];     // gc eps w_jq w_iq h^2
+    double wlh[9];     // lam w_jq w_iq h^2 / 2   (Miehe eigen-frame form)
+    double wmh[9];     // mu w_jq w_iq h^2 / 2
+    double wm[9];      // mu w_jq w_iq h^2
     double lam, mu2;
 };
 
@@ -133,8 +151,11 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
     const int strip = (int)(blk / q_rows), cy = q_row0 + (int)(blk % q_rows);
     const int cx = strip * SW_OWN - 1 + lane;
     double* out = qt + blk * qblock + lane;
-    constexpr int NT = MIEHE ? 6 : 1, NQT = NT + 4;
-    auto put = [&](int arr, int k, double x) { out[(arr * QK + k) * SW_LANES] = x; };
+    constexpr int NT = MIEHE ? 4 : 1, NCW = MIEHE ? 2 : 3, NQT = NT + NCW + 1;
+    // block layout [iq][array][jq][lane]: one Gauss column is one contiguous run
+    auto put = [&](int arr, int k, double x) {
+        out[(((k % 3) * NQT + arr) * 3 + k / 3) * SW_LANES] = x;
+    };
     if (cx < 0 || cx >= m.nside) {
         for (int a = 0; a < NQT; ++a)
             for (int k = 0; k < QK; ++k) put(a, k, 0.0);
@@ -180,45 +201,45 @@ __global__ void k_refresh_tiled(Mesh m, Shape S, Material M, const double* __res
             const double tre = e11 + e22;
             const double g = (1.0 - M.kappa) * pt[jq][iq] * pt[jq][iq] + M.kappa;
             const double dg = gdd * p0[jq][iq];
-            double esp, q11, q22, q12;
+            double esp;
             if (MIEHE) {
-                // the reference's tangent columns for unit directions (src/_kernels.py:519-523)
-                // stored as the symmetric form y = (ds11, ds22, 2 ds12) = T (d11, d22, d12)
-                const double mm = 0.5 * (e11 + e22);
-                const double dh = 0.5 * (e11 - e22);
-                const double r = sqrt(dh * dh + e12 * e12);
+                // split tangent of src/_kernels.py:50-74,102-123 in the strain eigen-frame
+                // (n1 = (c, s)): s' = C d' - (1-g) [lam H_tr tr d I + 2 mu (H_1 d'11, H_2 d'22,
+                // beta d'12)], beta = (<ev1>+ - <ev2>+) / (ev1 - ev2) (0 below the gap
+                // threshold of _dpos2s).  ev1 >= ev2 and tr e = ev1 + ev2 leave four
+                // regimes: sign(g) carries H_tr, sign(gamma) carries H_tr ? H_2 : H_1.
                 const Eig e = eig2(e11, e22, e12);
                 const bool gap_ok = (e.ev1 - e.ev2) > 1e-12 * scale2(e11, e22, e12);
-                const MieheQ q = miehe_q(mm, gap_ok ? r : -r, e.c, e.s);
-                double Mc[3][3], sp;
-                miehe_dsig(M, g, q, 1.0, 0.0, 0.0, Mc[0][0], Mc[1][0], Mc[2][0], sp);
-                miehe_dsig(M, g, q, 0.0, 1.0, 0.0, Mc[0][1], Mc[1][1], Mc[2][1], sp);
-                miehe_dsig(M, g, q, 0.0, 0.0, 1.0, Mc[0][2], Mc[1][2], Mc[2][2], sp);
-                put(0, k, wv * Mc[0][0]);
-                put(1, k, wv * 0.5 * (Mc[0][1] + Mc[1][0]));
-                put(2, k, wv * 0.5 * (Mc[0][2] + 2.0 * Mc[2][0]));
-                put(3, k, wv * Mc[1][1]);
-                put(4, k, wv * 0.5 * (Mc[1][2] + 2.0 * Mc[2][1]));
-                put(5, k, wv * 2.0 * Mc[2][2]);
-                sigplus2(lam, mu, tre, e, q11, q22, q12);
+                const double l1p = posp(e.ev1), l2p = posp(e.ev2), trp = posp(tre);
+                const double beta = gap_ok ? (l1p - l2p) / (e.ev1 - e.ev2) : 0.0;
+                const double gam = fma(g, beta, 1.0 - beta);
+                const bool htr = !(tre < 0.0), h1 = e.ev1 >= 0.0, h2 = e.ev2 >= 0.0;
+                const bool bb = htr ? h2 : h1;
+                put(0, k, htr ? g : -g);
+                put(1, k, bb ? gam : -gam);
+                put(2, k, e.c * e.c - e.s * e.s);
+                put(3, k, 2.0 * e.c * e.s);
+                // coupling dg sigma+ : de = q1 d'11 + q2 d'22 (src/_kernels.py:633-635), halved
+                put(4, k, 0.5 * wv * dg * (lam * trp + 2.0 * mu * l1p));
+                put(5, k, 0.5 * wv * dg * (lam * trp + 2.0 * mu * l2p));
                 esp = esplus2(lam, mu, tre, e);
             } else {
                 put(0, k, wv * g);
-                q11 = lam * tre + 2.0 * mu * e11;
-                q22 = lam * tre + 2.0 * mu * e22;
-                q12 = 2.0 * mu * e12;
+                const double q11 = lam * tre + 2.0 * mu * e11;
+                const double q22 = lam * tre + 2.0 * mu * e22;
+                const double q12 = 2.0 * mu * e12;
                 esp = 0.5 * lam * tre * tre + mu * (e11 * e11 + e22 * e22 + 2.0 * e12 * e12);
+                // coupling dg sigma : de (src/_kernels.py:645-653), weighted
+                put(NT + 0, k, wv * dg * q11);
+                put(NT + 1, k, wv * dg * q22);
+                put(NT + 2, k, wv * dg * 2.0 * q12);
             }
-            // coupling dg sigma+ : de (src/_kernels.py:633-635) and pc, weighted
-            put(NT + 0, k, wv * dg * q11);
-            put(NT + 1, k, wv * dg * q22);
-            put(NT + 2, k, wv * dg * 2.0 * q12);
-            put(NT + 3, k, wv * (gdd * esp + gce));
+            put(NQT - 1, k, wv * (gdd * esp + gce));
         }
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false>
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false, bool CR = false>
 __global__ void __launch_bounds__(SW_LANES)
 k_sweep_q2(const SweepArgs A) {
     using U = Use<MODE, MIEHE>;
@@ -227,7 +248,7 @@ k_sweep_q2(const SweepArgs A) {
     // the fused forms prefetch rhs (and D^-1, acc) of the lane's output nodes
     // into registers at the top of the row step: no staging buffer in shared
     // memory, so they run at the plain kernel's CTAs per SM
-    using Smem = WarpSmem<NF, NQ>;
+    using Smem = WarpSmem<NF, NQ, CR>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& W = *reinterpret_cast<Smem*>(smem_raw);
     const int lane = threadIdx.x;
@@ -238,8 +259,7 @@ k_sweep_q2(const SweepArgs A) {
     const int half = ns >> 1;
 
     if (lane == 0) {
-        mbar_init(&W.bar[0]);
-        mbar_init(&W.bar[1]);
+        for (int b = 0; b < NBAR; ++b) mbar_init(&W.bar[b]);
         fence_mbar_init();
     }
     __syncwarp();
@@ -289,11 +309,16 @@ k_sweep_q2(const SweepArgs A) {
             bulk_g2s(W.f[slot], A.flags + ab, (unsigned)(bb - ab), bar);
             return bytes + (unsigned)(bb - ab);
         };
-        auto issue_qblock = [&](int cy, int stage) -> unsigned {
-            const double* src =
-                A.qtile + ((int64_t)strip * A.q_rows + (cy - A.q_row0)) * A.qblock + U::Q0 * QARR;
-            bulk_g2s(W.q[stage], src, (unsigned)(NQ * QARR * 8), &W.bar[stage]);
-            return (unsigned)(NQ * QARR * 8);
+        // lane 0: Gauss column iq of cell row cy's tangent block (the mode's arrays)
+        // into slot iq (column ring, its own mbarrier) or into row stage `st`
+        auto issue_qcol = [&](int cy, int iq, int st) -> unsigned {
+            const double* src = A.qtile +
+                                ((int64_t)strip * A.q_rows + (cy - A.q_row0)) * A.qblock +
+                                (iq * U::NQT + U::Q0) * QCOL;
+            unsigned long long* bar = CR ? &W.bar[2 + iq] : &W.bar[st];
+            bulk_g2s(W.q[CR ? iq : st * 3 + iq], src, (unsigned)(NQ * QCOL * 8), bar);
+            if (CR) mbar_expect_tx(bar, (unsigned)(NQ * QCOL * 8));
+            return (unsigned)(NQ * QCOL * 8);
         };
         // reads of the staged rows b = 0, 1, 2 of the current cell row: ring slot
         // sb[b], element offset of staged column 0 vo[b][field slot] / fo[b] -- the
@@ -360,8 +385,9 @@ k_sweep_q2(const SweepArgs A) {
             }
         };
 
-        // iteration cy issues the TMA stage of cy+1; the virtual iteration
-        // cy = cstart-1 issues the first window (3 rows) -- one staging call site
+        // iteration cy issues the node rows of cy+1, and column iq of cy+1's tangent
+        // block once its own column iq is consumed; the virtual iteration
+        // cy = cstart-1 issues the first window (3 rows, 3 columns)
         int stage = 1;
         double carry[3][3] = {};
         for (int cy = cstart - 1; cy < c1; ++cy) {
@@ -375,8 +401,20 @@ k_sweep_q2(const SweepArgs A) {
                 unsigned bytes = 0;
 #pragma unroll 1
                 for (int t = 0; t < (first ? 3 : 2); ++t) bytes += issue_row(j0 + t, &W.bar[nstage]);
-                bytes += issue_qblock(cy + 1, nstage);
+                if (!CR && NQ == U::NQT) {
+                    // every array of the block: its three columns are one contiguous run
+                    const double* src = A.qtile + ((int64_t)strip * A.q_rows + (cy + 1 - A.q_row0)) * A.qblock;
+                    bulk_g2s(W.q[nstage * 3], src, (unsigned)(3 * NQ * QCOL * 8), &W.bar[nstage]);
+                    bytes += (unsigned)(3 * NQ * QCOL * 8);
+                } else if (!CR) {
+#pragma unroll 1
+                    for (int iq = 0; iq < 3; ++iq) bytes += issue_qcol(cy + 1, iq, nstage);
+                }
                 mbar_expect_tx(&W.bar[nstage], bytes);
+                if (CR && first) {
+#pragma unroll 1
+                    for (int iq = 0; iq < 3; ++iq) issue_qcol(cy + 1, iq, 0);
+                }
             }
             if (cy < cstart) {   // the virtual iteration only stages the first window
                 stage = nstage;
@@ -434,8 +472,6 @@ k_sweep_q2(const SweepArgs A) {
                 if (f == FP) return (mact & bit) ? 0.0 : x;
                 return x;
             };
-            const double* qb = W.q[stage];
-            auto qv = [&](int arr, int k) -> double { return qb[arr * QARR + k * SW_LANES + lane]; };
 
             // ---- cell computation (one cell per lane), Q2-specialised -----------------
             // Middle Gauss point: N[1] = (0,1,0), D[1] = (-1,0,1) (checked on the host);
@@ -454,6 +490,13 @@ k_sweep_q2(const SweepArgs A) {
                 const int side = SIDEC;
                 const int iq = MID ? 1 : 2 * side;
                 const int ic = MID ? 1 : 0;        // coefficient / weight column
+                // this column's slot of the tangent block
+                if (CR) {
+                    mbar_wait(&W.bar[2 + iq], (phase >> (2 + iq)) & 1u);
+                    phase ^= 1u << (2 + iq);
+                }
+                const double* qb = W.q[CR ? iq : stage * 3 + iq] + lane;
+                auto qv = [&](int arr, int jq) -> double { return qb[arr * QCOL + jq * SW_LANES]; };
                 const double sD = (!MID && side) ? -1.0 : 1.0;
                 auto g = [&](int f, int b, int a) -> double {
                     return MID ? get(f, b, a) : get(f, b, side ? 2 - a : a);
@@ -488,38 +531,57 @@ k_sweep_q2(const SweepArgs A) {
                         if (jq == 1) return K.ih * (X[2] - X[0]);
                         return fma(K.Dh[jq][2], X[2], fma(K.Dh[jq][1], X[1], K.Dh[jq][0] * X[0]));
                     };
-                    const int k = jq * 3 + iq;
+                    const int kc = jq * 3 + ic;   // weight index (w[2] = w[0])
                     // weighted stress increment s = C de (cache_tensors form,
                     // src/_kernels.py:624-635) and phi-row terms
-                    double s11 = 0.0, s22 = 0.0, s12 = 0.0, d11 = 0.0, d22 = 0.0, d12 = 0.0;
-                    if (U::ux) {
-                        d11 = yN(XxD);
-                        d22 = yD(XyN);
-                        d12 = 0.5 * (yD(XxN) + yN(XyD));
-                    }
-                    if (U::DO_UU) {
-                        if (MIEHE) {
-                            const double t00 = qv(0, k), t01 = qv(1, k), t02 = qv(2, k);
-                            const double t11 = qv(3, k), t12 = qv(4, k), t22 = qv(5, k);
-                            s11 = fma(t00, d11, fma(t01, d22, t02 * d12));
-                            s22 = fma(t01, d11, fma(t11, d22, t12 * d12));
-                            s12 = 0.5 * fma(t02, d11, fma(t12, d22, t22 * d12));
-                        } else {
-                            const double gw = qv(0, k);
+                    double s11 = 0.0, s22 = 0.0, s12 = 0.0, fv = 0.0, fgx = 0.0, fgy = 0.0;
+                    if (U::DO_PP) fv = qv(U::QPC, jq) * yN(XpN);
+                    if (MIEHE && U::ux) {
+                        // direction strain in the state's eigen-frame (twice the values):
+                        // 2 d'11 = e1, 2 d'22 = e2, 2 d'12 = v2
+                        const double d11 = yN(XxD), d22 = yD(XyN);
+                        const double D12 = yD(XxN) + yN(XyD);
+                        const double c2 = qv(U::QC2, jq), s2 = qv(U::QC2 + 1, jq);
+                        const double pd = d11 + d22, qd = d11 - d22;
+                        const double u2 = fma(c2, qd, s2 * D12);
+                        const double e1 = pd + u2, e2 = pd - u2;
+                        if (U::DO_COUP)
+                            fv = fma(qv(U::QCW, jq), e1, fma(qv(U::QCW + 1, jq), e2, fv));
+                        if (U::DO_UU) {
+                            const double v2 = fma(c2, D12, -(s2 * qd));
+                            const double gs = qv(0, jq), ms = qv(1, jq);
+                            const bool ha = __double2hiint(gs) >= 0, hb = __double2hiint(ms) >= 0;
+                            const double g = fabs(gs), gam = fabs(ms);
+                            const double ca = ha ? g : 1.0;            // H_tr
+                            const double c1 = (ha || hb) ? g : 1.0;    // H_1
+                            const double cb = (ha && hb) ? g : 1.0;    // H_2
+                            const double at = (K.wlh[kc] * ca) * pd;
+                            const double hs1 = fma(K.wmh[kc] * c1, e1, at);   // s'11 / 2
+                            const double hs2 = fma(K.wmh[kc] * cb, e2, at);   // s'22 / 2
+                            const double s3 = (K.wm[kc] * gam) * v2;          // s'12
+                            const double hp = hs1 + hs2, hd = hs1 - hs2;
+                            const double t = fma(c2, hd, -(s2 * s3));
+                            s11 = hp + t;
+                            s22 = hp - t;
+                            s12 = fma(s2, hd, c2 * s3);
+                        }
+                    } else if (U::ux) {
+                        const double d11 = yN(XxD), d22 = yD(XyN);
+                        const double d12 = 0.5 * (yD(XxN) + yN(XyD));
+                        if (U::DO_UU) {
+                            const double gw = qv(0, jq);
                             const double lt = K.lam * (d11 + d22);
                             s11 = gw * fma(K.mu2, d11, lt);
                             s22 = gw * fma(K.mu2, d22, lt);
                             s12 = (gw * K.mu2) * d12;
                         }
-                    }
-                    double fv = 0.0, fgx = 0.0, fgy = 0.0;
-                    if (U::DO_PP) {
-                        fv = qv(U::QPC, k) * yN(XpN);
                         if (U::DO_COUP)
-                            fv = fma(qv(U::QCW, k), d11,
-                                     fma(qv(U::QCW + 1, k), d22, fma(qv(U::QCW + 2, k), d12, fv)));
-                        fgx = K.cgw[jq * 3 + ic] * yN(XpD);
-                        fgy = K.cgw[jq * 3 + ic] * yD(XpN);
+                            fv = fma(qv(U::QCW, jq), d11,
+                                     fma(qv(U::QCW + 1, jq), d22, fma(qv(U::QCW + 2, jq), d12, fv)));
+                    }
+                    if (U::DO_PP) {
+                        fgx = K.cgw[kc] * yN(XpD);
+                        fgy = K.cgw[kc] * yD(XpN);
                     }
                     // backward y-pass: T[b] += M[jq][b] f
                     if (jq == 1) {
@@ -584,6 +646,12 @@ k_sweep_q2(const SweepArgs A) {
                         }
                         if (U::DO_PP) acc(r[2][b], Tp2[b], Tp1[b]);
                     }
+                }
+                // slot iq is consumed: refill it with the next cell row's column
+                if (CR && more) {
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) issue_qcol(cy + 1, iq, 0);
                 }
             };
             using I0 = std::integral_constant<int, 0>;
@@ -697,12 +765,25 @@ struct LaunchCfg {
     int blocks_per_sm = 0;
 };
 
-template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false>
-cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
+// tangent-block staging per (mode, split): PFF_SWEEP_COLRING = 0 / 1 forces the row
+// stages / the column ring everywhere; default: the measured choice
+template <int MODE, bool MIEHE>
+bool use_colring() {
+    static int env = -2;
+    if (env == -2) {
+        const char* e = getenv("PFF_SWEEP_COLRING");
+        env = e ? atoi(e) : -1;
+    }
+    if (env >= 0) return env != 0;
+    return MIEHE && (MODE == MODE_FULL || MODE == MODE_UU);
+}
+
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB, bool EMIT, bool CR>
+cudaError_t launch_mode_cr(SweepArgs& a, cudaStream_t s, int rows_override) {
     using U = Use<MODE, MIEHE>;
     // must match k_sweep_q2's Smem (the fused forms keep rhs / D^-1 / acc in registers)
-    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ>);
-    auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB, EMIT>;
+    const size_t shm = sizeof(WarpSmem<U::NF, U::NQ, CR>);
+    auto k = k_sweep_q2<MODE, MIEHE, FUSED, CHEB, EMIT, CR>;
     static LaunchCfg cfg;
     static int n_sm = 0;
     if (!cfg.init) {
@@ -735,6 +816,13 @@ cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
     k<<<grid, SW_LANES, shm, s>>>(a);
     count_launches(1);
     return cudaGetLastError();
+}
+
+template <int MODE, bool MIEHE, bool FUSED, bool CHEB = false, bool EMIT = false>
+cudaError_t launch_mode(SweepArgs& a, cudaStream_t s, int rows_override) {
+    return use_colring<MODE, MIEHE>()
+               ? launch_mode_cr<MODE, MIEHE, FUSED, CHEB, EMIT, true>(a, s, rows_override)
+               : launch_mode_cr<MODE, MIEHE, FUSED, CHEB, EMIT, false>(a, s, rows_override);
 }
 
 template <bool MIEHE, bool FUSED>
@@ -846,6 +934,9 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
             for (int iq = 0; iq < 3; ++iq) {
                 const double wq = L.shape.w[jq] * L.shape.w[iq];
                 K.cgw[jq * 3 + iq] = L.mat.gc * L.mat.eps * (wq * h * h);
+                K.wlh[jq * 3 + iq] = 0.5 * (L.mat.lam * (wq * h * h));
+                K.wmh[jq * 3 + iq] = 0.5 * (L.mat.mu * (wq * h * h));
+                K.wm[jq * 3 + iq] = L.mat.mu * (wq * h * h);
             }
         K.lam = L.mat.lam;
         K.mu2 = 2.0 * L.mat.mu;

@@ -41,9 +41,9 @@ def test_abi_version_and_host_only_calls():
     assert rc == 0
     assert L.pff_level_n_scalar(h) == 4_199_425
     assert L.pff_level_n_cells(h) == 1024 * 1024
-    # generic cache + strip-tiled Q2 tangent cache (34 strips x 1024 rows x 10 arrays x 9 q x 32
-    # lanes) + element-vector scratch (3 components x 9 nodes per cell)
-    assert L.pff_level_qcache_len(h) == (6 * 9 * 1024 * 1024 + 34 * 1024 * 10 * 9 * 32
+    # generic cache + strip-tiled Q2 tangent cache (34 strips x 1024 rows x 7 Miehe arrays x 9 q
+    # x 32 lanes) + element-vector scratch (3 components x 9 nodes per cell)
+    assert L.pff_level_qcache_len(h) == (6 * 9 * 1024 * 1024 + 34 * 1024 * 7 * 9 * 32
                                          + 3 * 9 * 1024 * 1024)
     rows = (ctypes.c_int64 * 6)()
     assert L.pff_level_set_window(h, 256, 512) == 0

@@ -311,6 +311,54 @@ def test_sweep_matches_generic_all_modes(generic_apply, split, level, rows):
         assert torch.equal(y1, y2)
 
 
+REGIMES = {
+    # affine displacement fields u = (a x + b y, c x + d y): one strain regime on every q-point
+    "zero": (0.0, 0.0, 0.0, 0.0),                   # e = 0: degenerate gap, tr e = 0
+    "near_biaxial_tension": (1e-3, 0.0, 0.0, 1e-3 * (1 + 1e-6)),    # gap 1e-9: resolved
+    "biaxial_compression": (-1e-3, 0.0, 0.0, -1e-3),  # ev1 = ev2 < 0: sigma+ = 0 in any frame
+    "uniaxial_tension": (1e-3, 0.0, 0.0, -3e-4),    # mixed signs, tr e > 0
+    "uniaxial_compression": (3e-4, 0.0, 0.0, -1e-3),  # mixed signs, tr e < 0
+    "shear_tr_pos": (1e-5, 1e-3, 1e-3, 0.0),        # ev ~ +-|e12|, tr e > 0
+    "shear_tr_neg": (0.0, 1e-3, 0.0, -1e-5),        # simple shear, tr e < 0
+    "tension_tension": (1e-3, 2e-4, -1e-4, 4e-4),   # both eigenvalues > 0, distinct
+    "compression_compression": (-1e-3, 2e-4, -1e-4, -4e-4),
+}
+
+
+@pytest.mark.parametrize("regime", sorted(REGIMES))
+def test_sweep_miehe_regimes_vs_oracle(regime):
+    """The Q2 sweep kernel's eigen-frame Miehe tile (regime in the sign bits of g and gamma)
+    against the C oracle on states that hold ONE strain regime everywhere, including the
+    zero state and equal compressive eigenvalues (src/_kernels.py:50-74,102-123).  Not
+    here: states where the reference's own branches are decided by round-off -- tr e = 0
+    up to rounding (pure shear: `tre < 0` flips) or ev1 = ev2 > 0 up to rounding (the
+    eigen-frame of _dpos2s is noise and its off-diagonal term is dropped below the gap
+    threshold, so the result depends on that frame); the oracle and any device kernel
+    (the round-1 symmetric-tangent form included) differ there by O(1)."""
+    level = 6
+    ost, x = O.baseline_state(2, level, "miehe", seed=3)
+    a, b, c, d = REGIMES[regime]
+    xy = ost.lv.coords()
+    n = ost.n
+    ost.U[:n] = a * xy[:, 0] + b * xy[:, 1]
+    ost.U[n:2 * n] = c * xy[:, 0] + d * xy[:, 1]
+    ost.refresh_cache(nthreads=O.max_threads())
+    h = P.build_hierarchy(level, 2)
+    st = P.LinearizationState(h, level, ost.params, split="miehe")
+    st.set_solution(ost.U)
+    st.set_phi_tilde(ost.phi_tilde)
+    st.set_phi_old(ost.phi_old)
+    st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    assert st.uses_sweep_kernel()
+    nt = O.max_threads()
+    assert max(block_rel(P.apply_jacobian(st, x), O.apply_jacobian(ost, x, nthreads=nt), n)) <= TOL
+    assert max(block_rel(P.apply_block_uu(st, x[:2 * n]),
+                         O.apply_block_uu(ost, x[:2 * n], nthreads=nt), n)) <= TOL
+    assert rel_l2(P.apply_phi_row(st, x), O.apply_phi_row(ost, x, nthreads=nt)) <= TOL
+
+
 @pytest.mark.parametrize("split", ["miehe", "none"])
 @pytest.mark.parametrize("level", [6, 9])
 def test_pipelined_host_path_matches_device_path(split, level):
