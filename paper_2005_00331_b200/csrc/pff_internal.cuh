@@ -101,7 +101,7 @@ struct Level {
     // Miehe: +-g, +-gamma, cos/sin 2 theta, 2 eigen-frame coupling coefficients, pc;
     // none: g w, coupling (3), pc
     int tile_nq() const { return miehe ? 7 : 5; }
-    int tile4_nq() const { return miehe ? 10 : 5; }  // Q4: symmetric tangent (6 | 1) + coupling (3) + pc
+    int tile4_nq() const { return miehe ? 7 : 5; }   // Q4: the same arrays
     int64_t tile_block() const { return (int64_t)tile_nq() * 9 * 32; }
     int64_t tile_len() const { return sweep_ok() ? (int64_t)n_strips() * q_rows() * tile_block() : 0; }
     // element-vector scratch of the generic application and of the restriction

@@ -53,12 +53,17 @@ struct Use4 {
     static constexpr bool DO_UU = MODE == MODE_FULL || MODE == MODE_UU;
     static constexpr bool DO_PP = MODE != MODE_UU;
     static constexpr bool DO_COUP = MODE == MODE_FULL || MODE == MODE_PHIROW;
-    static constexpr int NT = MIEHE ? 6 : 1;
-    static constexpr int NQT = NT + 4;
-    static constexpr int Q0 = MODE == MODE_PHIROW ? NT : MODE == MODE_PHIPHI ? NT + 3 : 0;
+    // tangent block arrays: none [g w][cw0 cw1 cw2][pc]; Miehe the eigen-frame form
+    // of the Q2 sweep (pff_sweep.cu): [+-g w][+-gamma w][c2][s2][q1/2][q2/2][pc]
+    static constexpr int NT = MIEHE ? 4 : 1;
+    static constexpr int NCW = MIEHE ? 2 : 3;
+    static constexpr int NQT = NT + NCW + 1;
+    static constexpr int Q0 = MODE == MODE_PHIROW ? (MIEHE ? 2 : NT)
+                              : MODE == MODE_PHIPHI ? NQT - 1 : 0;
     static constexpr int NQ = MODE == MODE_FULL ? NQT : MODE == MODE_UU ? NT
-                              : MODE == MODE_PHIROW ? 4 : 1;
-    static constexpr int QCW = DO_UU ? NT : 0;
+                              : MODE == MODE_PHIROW ? NQT - Q0 : 1;
+    static constexpr int QC2 = 2 - Q0;     // local index of c2 (Miehe, not PHIPHI)
+    static constexpr int QCW = NT - Q0;
     static constexpr int QPC = NQ - 1;
     static constexpr bool used(int f) { return (f == GX || f == GY) ? ux : ph; }
     static constexpr int slot(int f) {
@@ -100,7 +105,9 @@ struct EO4 {
     double N2E[2], N22, D2O[2];  // (N[2][a] + N[2][4-a]) / 2, N[2][2], (Dh[2][a] - Dh[2][4-a]) / 2
     double w[5];                 // Gauss weights
     double cg;                   // gc eps h^2
+    double h2;                   // h^2 (the Miehe eigen-frame form weights its constants)
     double lam, mu2;
+    double lamh, muh, mu;        // lam / 2, mu / 2, mu
 };
 
 // v[q] = sum_a N[q][a] u[a], d[q] = sum_a Dh[q][a] u[a], q = 0..4
@@ -192,7 +199,7 @@ __global__ void k_refresh_tile4(Mesh m, Shape S, Material M, const double* __res
     const int jq = within / 30, r = within - 30 * jq, c = r / 5, iq = r - 5 * c;
     const int cx = strip * OWN4 - 1 + c;
     double* o = qt + blk * qblock + within;
-    constexpr int NQT = MIEHE ? 10 : 5;
+    constexpr int NQT = MIEHE ? 7 : 5;
     if (cx < 0 || cx >= ns) {
 #pragma unroll
         for (int a = 0; a < NQT; ++a) o[a * QA4] = 0.0;
@@ -212,27 +219,22 @@ __global__ void k_refresh_tile4(Mesh m, Shape S, Material M, const double* __res
         o[4 * QA4] = wv * q[5 * fs];
         return;
     }
-    const double mm = 0.5 * (e11 + e22), dh = 0.5 * (e11 - e22);
-    const double rr = sqrt(dh * dh + e12 * e12);
+    // the eigen-frame split tangent of k_refresh_tiled (pff_sweep.cu), with the weight
+    // folded into g and gamma (the kernel rebuilds w_jq w_iq h^2 for the undegraded terms)
     const Eig e = eig2(e11, e22, e12);
     const bool gap_ok = (e.ev1 - e.ev2) > 1e-12 * scale2(e11, e22, e12);
-    const MieheQ mq = miehe_q(mm, gap_ok ? rr : -rr, e.c, e.s);
-    double Mc[3][3], sp;
-    miehe_dsig(M, g, mq, 1.0, 0.0, 0.0, Mc[0][0], Mc[1][0], Mc[2][0], sp);
-    miehe_dsig(M, g, mq, 0.0, 1.0, 0.0, Mc[0][1], Mc[1][1], Mc[2][1], sp);
-    miehe_dsig(M, g, mq, 0.0, 0.0, 1.0, Mc[0][2], Mc[1][2], Mc[2][2], sp);
-    double q11, q22, q12;
-    sigplus2(M.lam, M.mu, tre, e, q11, q22, q12);
-    o[0] = wv * Mc[0][0];
-    o[QA4] = wv * 0.5 * (Mc[0][1] + Mc[1][0]);
-    o[2 * QA4] = wv * 0.5 * (Mc[0][2] + 2.0 * Mc[2][0]);
-    o[3 * QA4] = wv * Mc[1][1];
-    o[4 * QA4] = wv * 0.5 * (Mc[1][2] + 2.0 * Mc[2][1]);
-    o[5 * QA4] = wv * 2.0 * Mc[2][2];
-    o[6 * QA4] = wv * dg * q11;
-    o[7 * QA4] = wv * dg * q22;
-    o[8 * QA4] = wv * dg * 2.0 * q12;
-    o[9 * QA4] = wv * q[5 * fs];
+    const double l1p = posp(e.ev1), l2p = posp(e.ev2), trp = posp(tre);
+    const double beta = gap_ok ? (l1p - l2p) / (e.ev1 - e.ev2) : 0.0;
+    const double gam = fma(g, beta, 1.0 - beta);
+    const bool htr = !(tre < 0.0), h1 = e.ev1 >= 0.0, h2 = e.ev2 >= 0.0;
+    const bool bb = htr ? h2 : h1;
+    o[0] = htr ? wv * g : -(wv * g);
+    o[QA4] = bb ? wv * gam : -(wv * gam);
+    o[2 * QA4] = e.c * e.c - e.s * e.s;
+    o[3 * QA4] = 2.0 * e.c * e.s;
+    o[4 * QA4] = 0.5 * wv * dg * (M.lam * trp + 2.0 * M.mu * l1p);
+    o[5 * QA4] = 0.5 * wv * dg * (M.lam * trp + 2.0 * M.mu * l2p);
+    o[6 * QA4] = wv * q[5 * fs];
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -256,6 +258,7 @@ __global__ void __launch_bounds__(32) k_sweep_q4(const Sweep4Args A) {
     // this lane's Gauss weight (iq = t) times gc eps h^2
     const double wt = t == 0 ? K.w[0] : t == 1 ? K.w[1] : t == 2 ? K.w[2] : t == 3 ? K.w[3] : K.w[4];
     const double cgl = K.cg * wt;
+    const double wth2 = wt * K.h2;   // w_iq h^2
 
     if (lane == 0) {
         mbar_init(&W.bar);
@@ -384,8 +387,10 @@ __global__ void __launch_bounds__(32) k_sweep_q4(const Sweep4Args A) {
                     fwd5<false, true>(K, X, tmp, d12);
                     col(3, X);                         // D_x v  -> N_y
                     fwd5<true, false>(K, X, pv, tmp);
+                    // d12 = (u_y + v_x) / 2; the Miehe form takes twice that
 #pragma unroll
-                    for (int q = 0; q < 5; ++q) d12[q] = 0.5 * (d12[q] + pv[q]);
+                    for (int q = 0; q < 5; ++q)
+                        d12[q] = MIEHE ? d12[q] + pv[q] : 0.5 * (d12[q] + pv[q]);
                 }
                 if (U::ph) {
                     col(4, X);                         // N_x phi -> value, D_y
@@ -398,31 +403,51 @@ __global__ void __launch_bounds__(32) k_sweep_q4(const Sweep4Args A) {
                 double S11[5], S12[5], S22[5], FV[5], FGX[5], FGY[5];
 #pragma unroll
                 for (int jq = 0; jq < 5; ++jq) {
-                    double s11 = 0.0, s22 = 0.0, s12 = 0.0;
-                    if (U::DO_UU) {
-                        if (MIEHE) {
-                            const double t00 = qv(0, jq), t01 = qv(1, jq), t02 = qv(2, jq);
-                            const double t11 = qv(3, jq), t12 = qv(4, jq), t22 = qv(5, jq);
-                            s11 = fma(t00, d11[jq], fma(t01, d22[jq], t02 * d12[jq]));
-                            s22 = fma(t01, d11[jq], fma(t11, d22[jq], t12 * d12[jq]));
-                            s12 = 0.5 * fma(t02, d11[jq], fma(t12, d22[jq], t22 * d12[jq]));
-                        } else {
+                    double s11 = 0.0, s22 = 0.0, s12 = 0.0, fv = 0.0, fgx = 0.0, fgy = 0.0;
+                    if (U::DO_PP) fv = qv(U::QPC, jq) * pv[jq];
+                    if (MIEHE && U::ux) {
+                        // eigen-frame form (pff_sweep.cu): d12[] holds 2 d12 here
+                        const double c2 = qv(U::QC2, jq), s2 = qv(U::QC2 + 1, jq);
+                        const double pd = d11[jq] + d22[jq], qd = d11[jq] - d22[jq];
+                        const double u2 = fma(c2, qd, s2 * d12[jq]);
+                        const double e1 = pd + u2, e2 = pd - u2;
+                        if (U::DO_COUP)
+                            fv = fma(qv(U::QCW, jq), e1, fma(qv(U::QCW + 1, jq), e2, fv));
+                        if (U::DO_UU) {
+                            const double v2 = fma(c2, d12[jq], -(s2 * qd));
+                            const double gs = qv(0, jq), ms = qv(1, jq);
+                            const bool ha = __double2hiint(gs) >= 0, hb = __double2hiint(ms) >= 0;
+                            const double wq = K.w[jq] * wth2;           // w_jq w_iq h^2
+                            const double gw = fabs(gs), gamw = fabs(ms);
+                            const double ca = ha ? gw : wq;             // H_tr
+                            const double c1 = (ha || hb) ? gw : wq;     // H_1
+                            const double cb = (ha && hb) ? gw : wq;     // H_2
+                            const double at = (K.lamh * ca) * pd;
+                            const double hs1 = fma(K.muh * c1, e1, at);
+                            const double hs2 = fma(K.muh * cb, e2, at);
+                            const double s3 = (K.mu * gamw) * v2;
+                            const double hp = hs1 + hs2, hd = hs1 - hs2;
+                            const double tt = fma(c2, hd, -(s2 * s3));
+                            s11 = hp + tt;
+                            s22 = hp - tt;
+                            s12 = fma(s2, hd, c2 * s3);
+                        }
+                    } else if (U::ux) {
+                        if (U::DO_UU) {
                             const double gw = qv(0, jq);
                             const double lt = K.lam * (d11[jq] + d22[jq]);
                             s11 = gw * fma(K.mu2, d11[jq], lt);
                             s22 = gw * fma(K.mu2, d22[jq], lt);
                             s12 = (gw * K.mu2) * d12[jq];
                         }
+                        if (U::DO_COUP)
+                            fv = fma(qv(U::QCW, jq), d11[jq],
+                                     fma(qv(U::QCW + 1, jq), d22[jq], fma(qv(U::QCW + 2, jq), d12[jq], fv)));
                     }
                     S11[jq] = s11;
                     S12[jq] = s12;
                     S22[jq] = s22;
-                    double fv = 0.0, fgx = 0.0, fgy = 0.0;
                     if (U::DO_PP) {
-                        fv = qv(U::QPC, jq) * pv[jq];
-                        if (U::DO_COUP)
-                            fv = fma(qv(U::QCW, jq), d11[jq],
-                                     fma(qv(U::QCW + 1, jq), d22[jq], fma(qv(U::QCW + 2, jq), d12[jq], fv)));
                         const double cw = cgl * K.w[jq];
                         fgx = cw * pgx[jq];
                         fgy = cw * pgy[jq];
@@ -646,6 +671,10 @@ cudaError_t launch_sweep4_apply(const Level& L, int mode, const double* src, dou
         K.cg = L.mat.gc * L.mat.eps * (m.h * m.h);
         K.lam = L.mat.lam;
         K.mu2 = 2.0 * L.mat.mu;
+        K.h2 = m.h * m.h;
+        K.lamh = 0.5 * L.mat.lam;
+        K.muh = 0.5 * L.mat.mu;
+        K.mu = L.mat.mu;
     }
     for (int f = 0; f < NF4; ++f) a.fld[f] = nullptr;
     switch (mode) {
