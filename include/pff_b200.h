@@ -298,9 +298,12 @@ int pff_apply_cheb_ex(const pff_level* L, int mode, const double* d, double* d_o
                       const double* rhs, double* cr, const double* invd, double* acc, double c1,
                       double c2, int flags, void* stream);
 
-/* Fused residual dst = rhs - G src (mode FULL or PHIROW) that also emits the
- * next smoothing block's Chebyshev start d0 = invd * dst / theta (FULL: the
- * two u components, invd/d0 of length 2n; PHIROW: the phi output, length n)
+/* Fused residual dst = rhs - G src (mode FULL, UU or PHIROW) that also emits the
+ * next smoothing block's Chebyshev start d0 = invd * dst / theta (FULL / UU: the
+ * two u components, invd/d0 of length 2n; PHIROW: the phi output, length n).
+ * UU: the u rows of the FULL residual alone -- bitwise the same values, the
+ * Jacobian has no u-phi block (src/_kernels.py:611-669) -- for the smoother's
+ * u-block residual, whose phi rows nothing reads (src/multigrid.py:262-276)
  * -- pff_cheb_init folded into the residual's store. */
 int pff_apply_emit(const pff_level* L, int mode, const double* src, double* dst,
                    const double* rhs, const double* invd, double* d0, double theta,

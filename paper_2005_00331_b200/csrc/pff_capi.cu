@@ -227,12 +227,12 @@ int pff_apply_emit(const pff_level* h, int mode, const double* src, double* dst,
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
         return fail(PFF_E_UNBOUND, "%s", "pff_apply_emit: state not bound");
-    if ((mode != 0 && mode != 3) || !src || !dst || !rhs || !invd || !d0 || !(theta != 0.0))
-        return fail(PFF_E_ARG, "%s", "pff_apply_emit: mode must be FULL or PHIROW, fused, theta != 0");
+    if ((mode != 0 && mode != 1 && mode != 3) || !src || !dst || !rhs || !invd || !d0 || !(theta != 0.0))
+        return fail(PFF_E_ARG, "%s", "pff_apply_emit: mode must be FULL, UU or PHIROW, fused, theta != 0");
     pff::ChebArgs cb{invd, nullptr, nullptr, 0.0, 0.0};
     cb.emit = d0;
     cb.theta = theta;
-    cb.emit_nc = mode == 0 ? 2 : 1;
+    cb.emit_nc = mode == 3 ? 1 : 2;
     return check(pff::launch_apply(*L, mode, src, dst, rhs, S(stream), &cb), "pff_apply_emit");
 }
 

@@ -767,8 +767,8 @@ cudaError_t launch_apply(const Level& L, int mode, const double* src, double* ds
     if (cheb && cheb->dout && (!rhs || (mode != MODE_UU && mode != MODE_PHIPHI) || cheb->dout == src))
         return cudaErrorInvalidValue;
     if (cheb && !cheb->dout &&
-        (!rhs || !cheb->emit || !cheb->invd || (mode != MODE_FULL && mode != MODE_PHIROW) ||
-         cheb->emit_nc != (mode == MODE_FULL ? 2 : 1)))
+        (!rhs || !cheb->emit || !cheb->invd || mode == MODE_PHIPHI ||
+         cheb->emit_nc != (mode == MODE_PHIROW ? 1 : 2)))
         return cudaErrorInvalidValue;
     if (L.windowed()) {   // slabs run the write-once sweep kernel only
         cudaError_t e = launch_sweep_apply(L, mode, src, dst, rhs, s, &handled, cheb);

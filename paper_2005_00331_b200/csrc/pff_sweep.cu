@@ -840,6 +840,7 @@ template <bool MIEHE>
 cudaError_t launch_emit(int mode, SweepArgs& a, cudaStream_t s, int rows) {
     switch (mode) {
         case MODE_FULL: return launch_mode<MODE_FULL, MIEHE, true, false, true>(a, s, rows);
+        case MODE_UU: return launch_mode<MODE_UU, MIEHE, true, false, true>(a, s, rows);
         case MODE_PHIROW: return launch_mode<MODE_PHIROW, MIEHE, true, false, true>(a, s, rows);
     }
     return cudaErrorInvalidValue;
@@ -977,9 +978,9 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
     a.emit_nc = 0;
     const bool emit = cheb && !cheb->dout;
     if (emit) {   // residual producer emitting the next block's Chebyshev d0
-        if (!rhs || !cheb->emit || !cheb->invd || (mode != MODE_FULL && mode != MODE_PHIROW))
+        if (!rhs || !cheb->emit || !cheb->invd || mode == MODE_PHIPHI)
             return cudaErrorInvalidValue;
-        a.emit_nc = mode == MODE_FULL ? 2 : 1;
+        a.emit_nc = mode == MODE_PHIROW ? 1 : 2;
         for (int c = 0; c < a.emit_nc; ++c) {
             a.invd[c] = cheb->invd + c * n - sh;
             a.emit[c] = cheb->emit + c * n - sh;

@@ -266,8 +266,8 @@ class DistributedGmg:
         if first:   # z = SELECT(r): the residual is r with constrained rows zeroed
             call("pff_cons", L.st.handle(), _lib.LAYOUT_FULL, _lib.CONS_EXCLUDE, ptr(r),
                  ptr(W["res"]), stream_handle())
-        else:
-            L.st.apply_into(_lib.MODE_FULL, z, W["res"], r)
+        else:   # the u rows of r - G z alone (no u-phi block): 2 components exchanged, not 3
+            L.st.apply_into(_lib.MODE_UU, z[:2 * ln], W["res"][:2 * ln], r[:2 * ln])
         hi = L.ranges["uu"][1]
         self._cheb(L, _lib.MODE_UU, W["res"][:2 * ln], c.c * hi, c.C * hi, c.sweeps, z[:2 * ln])
         L.st.apply_into(_lib.MODE_PHIROW, z, W["resphi"], r[2 * ln:])

@@ -38,10 +38,16 @@ FUSE_CHEB = True   # Chebyshev steps fused into the block applications (pff_appl
 # levels of at most COARSE_DENSE_NMAX scalar nodes (Q2 level 2: 85)
 # pff_cheb_init folded into the residual producers (pff_apply_emit, pff_smooth_init)
 FUSE_INIT = os.environ.get("PFF_FUSE_INIT", "1") != "0"
-# the FULL residual emitting the u block's d0 measured slower (+4.5 ms per Newton
-# solve at 1024^2) than the separate pff_cheb_init pass it replaces: off
-EMIT_FULL = os.environ.get("PFF_EMIT_FULL", "0") != "0"
 EMIT_PHIROW = os.environ.get("PFF_EMIT_PHIROW", "1") != "0"
+# the later smoothings' u-block residual as the UU application on (z_u, r_u): its phi
+# rows are never read and G has no u-phi block, so the u rows are bitwise those of the
+# FULL residual at 4 tile arrays and 2 fields instead of 7 and 3 (Newton solve at
+# 1024^2: 97.5 -> 95.2 ms of device time)
+POST_UU = os.environ.get("PFF_POST_UU", "1") != "0"
+# that residual emitting the u block's d0 (pff_apply_emit): as the FULL application it
+# measured slower (+4.5 ms per solve) than the separate pff_cheb_init pass it replaces;
+# as the UU application it is faster (95.2 -> 94.0 ms) -- on with POST_UU
+EMIT_FULL = os.environ.get("PFF_EMIT_FULL", "1" if POST_UU else "0") != "0"
 DENSE_COARSE = os.environ.get("PFF_DENSE_COARSE", "1") != "0"
 COARSE_DENSE_NMAX = 256
 # the whole V-cycle from the level above the coarse one as one dense map
@@ -942,8 +948,10 @@ class GmgPreconditioner:
             if first:
                 call("pff_smooth_init", h, ptr(r), ptr(z), ptr(W.res), ptr(inv_u), ptr(W.d), th_u, st)
             elif EMIT_FULL:
-                call("pff_apply_emit", h, _lib.MODE_FULL, ptr(z), ptr(W.res), ptr(r), ptr(inv_u),
-                     ptr(W.d), th_u, st)
+                call("pff_apply_emit", h, _lib.MODE_UU if POST_UU else _lib.MODE_FULL, ptr(z),
+                     ptr(W.res), ptr(r), ptr(inv_u), ptr(W.d), th_u, st)
+            elif POST_UU:
+                s.apply_into(_lib.MODE_UU, z[:2 * n], W.res[:2 * n], r[:2 * n])
             else:
                 s.apply_into(_lib.MODE_FULL, z, W.res, r)
             self._cheb(l, _lib.MODE_UU, W.res[:2 * n], c * hu, C * hu, self.cheb.sweeps, z[:2 * n],
@@ -961,6 +969,8 @@ class GmgPreconditioner:
             # (identity rows/columns), so no operator application is needed
             call("pff_cons", s.bind(), _lib.LAYOUT_FULL, _lib.CONS_EXCLUDE, ptr(r), ptr(W.res),
                  stream_handle())
+        elif POST_UU:
+            s.apply_into(_lib.MODE_UU, z[:2 * n], W.res[:2 * n], r[:2 * n])
         else:
             s.apply_into(_lib.MODE_FULL, z, W.res, r)
         hi = self.ranges[l]["uu"][1]
