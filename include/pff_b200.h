@@ -293,7 +293,11 @@ int pff_apply_cheb_first(const pff_level* L, int mode, const double* d, double* 
 /* pff_apply_cheb with options: PFF_CHEB_FIRST = pff_apply_cheb_first's
  * acc += d + d'; PFF_CHEB_LAST = the last step of a pass: only acc is
  * written (cr and d_out are not stored; nothing reads them afterwards). */
-enum { PFF_CHEB_FIRST = 1, PFF_CHEB_LAST = 2 };
+/* PFF_CHEB_NOACC: the step leaves acc alone; the NEXT step then runs with
+ * PFF_CHEB_FIRST and adds this step's d' (its own d) and its d' in the same
+ * order, (acc + d) + d' -- bitwise the two separate updates, one acc read and
+ * write fewer. */
+enum { PFF_CHEB_FIRST = 1, PFF_CHEB_LAST = 2, PFF_CHEB_NOACC = 4 };
 int pff_apply_cheb_ex(const pff_level* L, int mode, const double* d, double* d_out,
                       const double* rhs, double* cr, const double* invd, double* acc, double c1,
                       double c2, int flags, void* stream);
@@ -314,6 +318,12 @@ int pff_apply_emit(const pff_level* L, int mode, const double* src, double* dst,
  * (pff_cons SELECT + EXCLUDE + pff_cheb_init in one pass). */
 int pff_smooth_init(const pff_level* L, const double* r, double* z, double* res_u,
                     const double* invd_u, double* d_u, double theta, void* stream);
+/* flags & PFF_SMOOTH_ADD_D0: z[:2n] also takes the Chebyshev start, z_u = d_u on
+ * unconstrained rows (exactly 0 + d_u; d_u is 0 on constrained rows) -- the
+ * `z += d` of src/multigrid.py:185, so the first fused step needs no PFF_CHEB_FIRST */
+enum { PFF_SMOOTH_ADD_D0 = 1 };
+int pff_smooth_init_ex(const pff_level* L, const double* r, double* z, double* res_u,
+                       const double* invd_u, double* d_u, double theta, int flags, void* stream);
 
 /* y = M x for a row-major dense device matrix M (rows x cols); x != y.  The
  * V-cycle below a small level as one precomputed linear map. */

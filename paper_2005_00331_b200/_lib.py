@@ -46,6 +46,8 @@ SIGNATURES = {
                             ctypes.c_void_p]),
     "pff_smooth_init": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _d,
                              ctypes.c_void_p]),
+    "pff_smooth_init_ex": (_i, [ctypes.c_void_p, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _d, _i,
+                                ctypes.c_void_p]),
     "pff_dense_matvec": (_i, [_i64, _i64, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_coarse_dense": (_i, [_i64, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, ctypes.c_void_p]),
     "pff_apply_rows": (_i, [ctypes.c_void_p, _i, _c_dp, _c_dp, _c_dp, _i, _i, ctypes.c_void_p]),
@@ -90,7 +92,8 @@ FLAG_DIRICHLET, FLAG_ACTIVE = 1, 2
 LAYOUT_FULL, LAYOUT_UU, LAYOUT_PHI = 0, 1, 2
 CONS_SELECT, CONS_ZERO, CONS_COPY, CONS_EXCLUDE = 0, 1, 2, 3
 OPT_GENERIC_APPLY, OPT_SWEEP_ROWS, OPT_SWEEP_MIN_NSIDE = 1, 2, 3
-CHEB_FIRST, CHEB_LAST = 1, 2
+CHEB_FIRST, CHEB_LAST, CHEB_NOACC = 1, 2, 4
+SMOOTH_ADD_D0 = 1
 
 
 def set_option(key: int, value: int):

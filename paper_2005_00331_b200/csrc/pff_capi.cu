@@ -207,11 +207,13 @@ int pff_apply_cheb_ex(const pff_level* h, int mode, const double* d, double* d_o
     if (!bound(L) && !(L && L->windowed() && L->U && L->phi_tilde && L->flags && L->qcache))
         return fail(PFF_E_UNBOUND, "%s", "pff_apply_cheb_ex: state not bound");
     if ((mode != 1 && mode != 2) || !d || !d_out || !rhs || !cr || !invd || !acc || d_out == d ||
-        (flags & ~(PFF_CHEB_FIRST | PFF_CHEB_LAST)))
-        return fail(PFF_E_ARG, "%s", "pff_apply_cheb_ex: mode must be UU or PHIPHI, d_out != d, known flags");
+        (flags & ~(PFF_CHEB_FIRST | PFF_CHEB_LAST | PFF_CHEB_NOACC)) ||
+        ((flags & PFF_CHEB_NOACC) && (flags & (PFF_CHEB_FIRST | PFF_CHEB_LAST))))
+        return fail(PFF_E_ARG, "%s", "pff_apply_cheb_ex: mode must be UU or PHIPHI, d_out != d, known flags (NOACC alone)");
     pff::ChebArgs cb{invd, d_out, acc, c1, c2};
     cb.acc_src = (flags & PFF_CHEB_FIRST) ? 1 : 0;
     cb.last = (flags & PFF_CHEB_LAST) ? 1 : 0;
+    cb.noacc = (flags & PFF_CHEB_NOACC) ? 1 : 0;
     return check(pff::launch_apply(*L, mode, d, cr, rhs, S(stream), &cb), "pff_apply_cheb_ex");
 }
 
@@ -238,11 +240,17 @@ int pff_apply_emit(const pff_level* h, int mode, const double* src, double* dst,
 
 int pff_smooth_init(const pff_level* h, const double* r, double* z, double* res_u,
                     const double* invd_u, double* d_u, double theta, void* stream) {
+    return pff_smooth_init_ex(h, r, z, res_u, invd_u, d_u, theta, 0, stream);
+}
+
+int pff_smooth_init_ex(const pff_level* h, const double* r, double* z, double* res_u,
+                       const double* invd_u, double* d_u, double theta, int flags, void* stream) {
     const Level* L = reinterpret_cast<const Level*>(h);
     if (!L || !L->flags) return fail(PFF_E_UNBOUND, "%s", "pff_smooth_init: flags not bound");
-    if (!r || !z || !res_u || !invd_u || !d_u || !(theta != 0.0))
+    if (!r || !z || !res_u || !invd_u || !d_u || !(theta != 0.0) || (flags & ~PFF_SMOOTH_ADD_D0))
         return fail(PFF_E_ARG, "%s", "pff_smooth_init: bad argument");
-    return check(pff::launch_smooth_init(*L, r, z, res_u, invd_u, d_u, theta, S(stream)),
+    return check(pff::launch_smooth_init(*L, r, z, res_u, invd_u, d_u, theta,
+                                         (flags & PFF_SMOOTH_ADD_D0) != 0, S(stream)),
                  "pff_smooth_init");
 }
 

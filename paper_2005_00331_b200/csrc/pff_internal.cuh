@@ -226,6 +226,8 @@ struct ChebArgs {
     // last: the final step of a pass -- only acc is consumed, so the residual
     // (dst) and d' (dout) stores are skipped
     int last = 0;
+    // noacc: the step leaves acc alone (the next step adds both, acc_src)
+    int noacc = 0;
     // residual producers (fused form, no dout): d0 = invd * dst / theta on the
     // first emit_nc output components (pff_cheb_init's d, same rounding)
     double* emit = nullptr;
@@ -304,7 +306,8 @@ constexpr int RED_THREADS = 256;
 cudaError_t launch_cons(const Level& L, int layout, int op, const double* r, double* z,
                         cudaStream_t s);
 cudaError_t launch_smooth_init(const Level& L, const double* r, double* z, double* res_u,
-                               const double* invd_u, double* d_u, double theta, cudaStream_t s);
+                               const double* invd_u, double* d_u, double theta, bool add_d0,
+                               cudaStream_t s);
 cudaError_t launch_cheb_init(int64_t n, const double* invd, const double* rhs, double theta,
                              double* d, double* acc, int acc_mode, cudaStream_t s);
 cudaError_t launch_cheb_step(int64_t n, const double* invd, const double* r, double c1,

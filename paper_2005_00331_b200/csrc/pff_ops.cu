@@ -223,8 +223,10 @@ __global__ void k_apply_gather(Mesh m, const uint8_t* __restrict__ flags,
         if (cheb.dout) {   // fused Chebyshev step on the residual just formed
             const double dn = cheb_update(cheb.c1, sv, cheb.c2, cheb.invd[c * n + i], x);
             if (!cheb.last) cheb.dout[c * n + i] = dn;
-            const double av = cheb.acc[c * n + i];
-            cheb.acc[c * n + i] = (cheb.acc_src ? av + sv : av) + dn;
+            if (!cheb.noacc) {
+                const double av = cheb.acc[c * n + i];
+                cheb.acc[c * n + i] = (cheb.acc_src ? av + sv : av) + dn;
+            }
         } else if (c < cheb.emit_nc) {   // the next block's Chebyshev d0
             cheb.emit[c * n + i] = cheb.invd[c * n + i] * x / cheb.theta;
         }

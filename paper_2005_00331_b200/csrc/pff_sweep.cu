@@ -127,6 +127,7 @@ struct SweepArgs {
     double c1, c2;
     int acc_src;                  // first Chebyshev step: acc += d + d'
     int last;                     // last Chebyshev step: only acc is stored
+    int noacc;                    // this step leaves acc alone (the next one adds both)
     // EMIT: d0 = invd * dst / theta on the first emit_nc components (reuses invd)
     double* emit[2];
     double theta;
@@ -380,7 +381,7 @@ k_sweep_q2(const SweepArgs A) {
                     const double av = rh[2][c];
                     const double dn = cheb_update(A.c1, sv, A.c2, iv, x);
                     if (!A.last) A.dout[c][gid] = dn;
-                    A.acc[c][gid] = (A.acc_src ? av + sv : av) + dn;
+                    if (!A.noacc) A.acc[c][gid] = (A.acc_src ? av + sv : av) + dn;
                 }
             }
         };
@@ -436,7 +437,7 @@ k_sweep_q2(const SweepArgs A) {
                             const int64_t gi = (jb + b) * np1 + 2 * (int64_t)cx + a;
                             rr[b][a][c] = A.rhs[c][gi];
                             if (CHEB || (EMIT && c < A.emit_nc)) ri[b][a][c] = A.invd[c][gi];
-                            if (CHEB) ra[b][a][c] = A.acc[c][gi];
+                            if (CHEB && !A.noacc) ra[b][a][c] = A.acc[c][gi];
                         }
                     }
             }
@@ -685,7 +686,7 @@ k_sweep_q2(const SweepArgs A) {
                     if (rbi < 0) {
                         rh[0][c] = A.rhs[c][gid];
                         if (wi) rh[1][c] = A.invd[c][gid];
-                        if (CHEB) rh[2][c] = A.acc[c][gid];
+                        if (CHEB && !A.noacc) rh[2][c] = A.acc[c][gid];
                     } else {
                         rh[0][c] = rr[rbi / 3][rbi % 3][c];
                         if (wi) rh[1][c] = ri[rbi / 3][rbi % 3][c];
@@ -973,6 +974,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
     a.c1 = a.c2 = 0.0;
     a.acc_src = 0;
     a.last = 0;
+    a.noacc = 0;
     a.emit[0] = a.emit[1] = nullptr;
     a.theta = 1.0;
     a.emit_nc = 0;
@@ -998,6 +1000,7 @@ cudaError_t launch_sweep_apply_rows(const Level& L, int mode, const double* src,
         a.c2 = cheb->c2;
         a.acc_src = cheb->acc_src;
         a.last = cheb->last;
+        a.noacc = cheb->noacc;
     }
     a.n_strips = L.n_strips();
     int rows = g_rows_override;

@@ -46,7 +46,7 @@ __global__ void k_cons(int64_t n, const uint8_t* __restrict__ flags, int layout,
 __global__ void k_smooth_init(int64_t n, const uint8_t* __restrict__ flags,
                               const double* __restrict__ r, double* __restrict__ z,
                               double* __restrict__ res_u, const double* __restrict__ invd_u,
-                              double* __restrict__ d_u, double theta) {
+                              double* __restrict__ d_u, double theta, bool add_d0) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint8_t f = flags[i];
@@ -55,12 +55,15 @@ __global__ void k_smooth_init(int64_t n, const uint8_t* __restrict__ flags,
         const int64_t k = c * n + i;
         const bool cons = is_cons(f, 0, c);
         const double rv = r[k];
-        z[k] = cons ? rv : 0.0;
+        double zv = cons ? rv : 0.0;
         if (c < 2) {
             const double rr = cons ? 0.0 : rv;
             res_u[k] = rr;
-            d_u[k] = invd_u[k] * rr / theta;
+            const double d0 = invd_u[k] * rr / theta;
+            d_u[k] = d0;
+            if (add_d0) zv += d0;   // exact: one of the two terms is zero
         }
+        z[k] = zv;
     }
 }
 
@@ -351,9 +354,10 @@ cudaError_t launch_cons(const Level& L, int layout, int op, const double* r, dou
 }
 
 cudaError_t launch_smooth_init(const Level& L, const double* r, double* z, double* res_u,
-                               const double* invd_u, double* d_u, double theta, cudaStream_t s) {
+                               const double* invd_u, double* d_u, double theta, bool add_d0,
+                               cudaStream_t s) {
     const int64_t n = L.local_n();
-    k_smooth_init<<<blocks(n), 256, 0, s>>>(n, L.flags, r, z, res_u, invd_u, d_u, theta);
+    k_smooth_init<<<blocks(n), 256, 0, s>>>(n, L.flags, r, z, res_u, invd_u, d_u, theta, add_d0);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -44,6 +44,11 @@ EMIT_PHIROW = os.environ.get("PFF_EMIT_PHIROW", "1") != "0"
 # FULL residual at 4 tile arrays and 2 fields instead of 7 and 3 (Newton solve at
 # 1024^2: 97.5 -> 95.2 ms of device time)
 POST_UU = os.environ.get("PFF_POST_UU", "1") != "0"
+# first smoothing: pff_smooth_init adds the u block's Chebyshev start to z itself and the
+# fused steps touch z only every second step ((z + d_k) + d_k+1 in one update,
+# PFF_CHEB_NOACC / PFF_CHEB_FIRST: bitwise the step-by-step sums, one read and write
+# of z fewer per skipped step)
+DEFER_ACC = os.environ.get("PFF_DEFER_ACC", "1") != "0"
 # that residual emitting the u block's d0 (pff_apply_emit): as the FULL application it
 # measured slower (+4.5 ms per solve) than the separate pff_cheb_init pass it replaces;
 # as the UU application it is faster (95.2 -> 94.0 ms) -- on with POST_UU
@@ -869,7 +874,7 @@ class GmgPreconditioner:
                            (tr - tc) * 1e3, (time.perf_counter() - tr) * 1e3)
 
     # -- device V-cycle (src/multigrid.py:295-344) ---------------------------------
-    def _cheb(self, l, mode, rhs, a, b, sweeps, out, assign, pre_d=False):
+    def _cheb(self, l, mode, rhs, a, b, sweeps, out, assign, pre_d=False, d0_in_acc=False):
         s = self.states[l]
         W = self._work[l]
         nb = rhs.numel()
@@ -889,9 +894,19 @@ class GmgPreconditioner:
             d_in, d_out = d, W.d2[:nb]
             src = rhs
             rho_old = 1.0 / sigma1
+            skipped = False   # the previous step left acc alone
             for k in range(1, sweeps):
                 rho = 1.0 / (2.0 * sigma1 - rho_old)
-                fl = (_lib.CHEB_FIRST if k == 1 else 0) | (_lib.CHEB_LAST if k == sweeps - 1 else 0)
+                if d0_in_acc:
+                    # acc already holds d0: steps pair up from the end -- a step with an odd
+                    # number of steps after it skips acc, the next adds both
+                    if (sweeps - 1 - k) % 2 == 1:
+                        fl, skipped = _lib.CHEB_NOACC, True
+                    else:
+                        fl, skipped = (_lib.CHEB_FIRST if skipped else 0), False
+                else:
+                    fl = _lib.CHEB_FIRST if k == 1 else 0
+                fl |= _lib.CHEB_LAST if k == sweeps - 1 else 0
                 call("pff_apply_cheb_ex", h, mode, ptr(d_in), ptr(d_out), ptr(src), ptr(cr),
                      ptr(inv), ptr(acc), rho * rho_old, 2.0 * rho / delta, fl, st)
                 rho_old = rho
@@ -945,8 +960,10 @@ class GmgPreconditioner:
             inv_u, inv_p = self._inv[l]
             st = stream_handle()
             h = s.bind()
+            defer = first and DEFER_ACC
             if first:
-                call("pff_smooth_init", h, ptr(r), ptr(z), ptr(W.res), ptr(inv_u), ptr(W.d), th_u, st)
+                call("pff_smooth_init_ex", h, ptr(r), ptr(z), ptr(W.res), ptr(inv_u), ptr(W.d), th_u,
+                     _lib.SMOOTH_ADD_D0 if defer else 0, st)
             elif EMIT_FULL:
                 call("pff_apply_emit", h, _lib.MODE_UU if POST_UU else _lib.MODE_FULL, ptr(z),
                      ptr(W.res), ptr(r), ptr(inv_u), ptr(W.d), th_u, st)
@@ -955,7 +972,7 @@ class GmgPreconditioner:
             else:
                 s.apply_into(_lib.MODE_FULL, z, W.res, r)
             self._cheb(l, _lib.MODE_UU, W.res[:2 * n], c * hu, C * hu, self.cheb.sweeps, z[:2 * n],
-                       False, pre_d=first or EMIT_FULL)
+                       False, pre_d=first or EMIT_FULL, d0_in_acc=defer)
             if EMIT_PHIROW:
                 call("pff_apply_emit", h, _lib.MODE_PHIROW, ptr(z), ptr(W.resphi), ptr(r[2 * n:]),
                      ptr(inv_p), ptr(W.d), th_p, st)

@@ -445,21 +445,48 @@ def test_vcycle_fused_chebyshev_start_bitwise(split):
     st.set_dirichlet_nodes(dirn)
     st.refresh_cache()
     out = []
-    saved = (MG.FUSE_INIT, MG.EMIT_FULL, MG.POST_UU)
+    saved = (MG.FUSE_INIT, MG.EMIT_FULL, MG.POST_UU, MG.DEFER_ACC)
     try:
         # (.., post_uu): the later smoothings' u-block residual as the UU application
-        # instead of the FULL one (its phi rows are never read)
-        for fuse, emit, post_uu in ((False, False, False), (False, False, True),
-                                    (True, False, False), (True, False, True),
-                                    (True, True, False), (True, True, True)):
-            MG.FUSE_INIT, MG.EMIT_FULL, MG.POST_UU = fuse, emit, post_uu
+        # instead of the FULL one (its phi rows are never read); (.., defer): the first
+        # smoothing's z updated every second fused step (PFF_CHEB_NOACC)
+        for fuse, emit, post_uu, defer in ((False, False, False, False), (False, False, True, False),
+                                           (True, False, False, False), (True, False, True, True),
+                                           (True, True, False, True), (True, True, True, False),
+                                           (True, True, True, True)):
+            MG.FUSE_INIT, MG.EMIT_FULL, MG.POST_UU, MG.DEFER_ACC = fuse, emit, post_uu, defer
             g = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=3))
             g.setup(st)
             out.append(g.apply(x))
     finally:
-        MG.FUSE_INIT, MG.EMIT_FULL, MG.POST_UU = saved
+        MG.FUSE_INIT, MG.EMIT_FULL, MG.POST_UU, MG.DEFER_ACC = saved
     for o in out[1:]:
         assert np.array_equal(out[0], o)
+
+
+@pytest.mark.parametrize("sweeps", [2, 4, 5])
+def test_vcycle_deferred_acc_other_sweep_counts(sweeps):
+    """The NOACC / FIRST pairing of the fused Chebyshev steps for sweep counts other than
+    the default 3 (odd and even numbers of fused steps), bitwise against the step-by-step z."""
+    import bench
+    from paper_2005_00331_b200 import multigrid as MG
+    level = 6
+    h, params, U, pt, act, dirn, x = bench.baseline_inputs(2, level, "miehe", seed=2, notch=True)
+    st = P.LinearizationState(h, level, params, split="miehe")
+    st.set_solution(U); st.set_phi_tilde(pt); st.set_phi_old(pt); st.set_active(act)
+    st.set_dirichlet_nodes(dirn)
+    st.refresh_cache()
+    out = []
+    saved = MG.DEFER_ACC
+    try:
+        for defer in (False, True):
+            MG.DEFER_ACC = defer
+            g = P.GmgPreconditioner(h, coarse_level=2, cheb=P.ChebyshevConfig(sweeps=sweeps))
+            g.setup(st)
+            out.append(g.apply(x))
+    finally:
+        MG.DEFER_ACC = saved
+    assert np.array_equal(out[0], out[1])
 
 
 def test_dense_matvec_matches_torch():
