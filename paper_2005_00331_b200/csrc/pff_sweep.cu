@@ -466,13 +466,24 @@ k_sweep_q2(const SweepArgs A) {
                     mdir |= (fl & F_DIR) ? 1u << (3 * b + a) : 0u;
                     mact |= (fl & F_ACT) ? 1u << (3 * b + a) : 0u;
                 }
-            auto get = [&](int f, int b, int a) -> double {
-                const double x = rowp[b][U::slot(f)][a];
-                const unsigned bit = 1u << (3 * b + a);
-                if (f == FX || f == FY) return (mdir & bit) ? 0.0 : x;
-                if (f == FP) return (mact & bit) ? 0.0 : x;
-                return x;
-            };
+            // the cell's masked node values, loaded and masked ONCE into registers: the
+            // column ring's mbarrier waits are compiler memory barriers, so values read
+            // through `rowp` inside the three column passes would be re-loaded and
+            // re-masked per pass (3 x 27 LDS + 54 FSEL; the row-stage kernels were
+            // already hoisted by the compiler)
+            double nv[NF][3][3];
+#pragma unroll
+            for (int q = 0; q < NF; ++q)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const double x = rowp[b][q][a];
+                        const unsigned bit = 1u << (3 * b + a);
+                        const bool isphi = U::ph && q == U::slot(FP);
+                        nv[q][b][a] = ((isphi ? mact : mdir) & bit) ? 0.0 : x;
+                    }
+            auto get = [&](int f, int b, int a) -> double { return nv[U::slot(f)][b][a]; };
 
             // ---- cell computation (one cell per lane), Q2-specialised -----------------
             // Middle Gauss point: N[1] = (0,1,0), D[1] = (-1,0,1) (checked on the host);
@@ -776,7 +787,9 @@ bool use_colring() {
         env = e ? atoi(e) : -1;
     }
     if (env >= 0) return env != 0;
-    return MIEHE && (MODE == MODE_FULL || MODE == MODE_UU);
+    // measured (tools/ab_apply.py, 1024^2): the ring wins for FULL (both splits) and the
+    // Miehe UU block; the phi modes and the one-array `none` UU block keep the row stages
+    return MODE == MODE_FULL || (MIEHE && MODE == MODE_UU);
 }
 
 template <int MODE, bool MIEHE, bool FUSED, bool CHEB, bool EMIT, bool CR>
