@@ -461,12 +461,21 @@ k_diag_cells(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc, 
             const double* q = qc + (int64_t)(jq * N1 + iq) * nc + cell;
             const double e11 = q[0], e22 = q[fs], e12 = q[2 * fs], g_t = q[3 * fs],
                          pc = q[5 * fs];
-            Eig e;
-            double scale = 1.0, tre = 0.0;
+            // Miehe: the split tangent is linear in the direction strain, so its three unit
+            // columns (one dsig_split_pre each, per q-point) replace the two evaluations
+            // per (node, q-point) of src/_kernels.py:700-746: t[i][k] = s_i for unit
+            // direction k, (s11, s22, s12) over (d11, d22, d12)
+            double t[3][3] = {};
             if (MIEHE) {
-                e = eig2(e11, e22, e12);
-                scale = scale2(e11, e22, e12);
-                tre = e11 + e22;
+                const Eig e = eig2(e11, e22, e12);
+                const double scale = scale2(e11, e22, e12), tre = e11 + e22;
+                double unused;
+                dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, 1.0, 0.0, 0.0, t[0][0], t[1][0],
+                               t[2][0], unused);
+                dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, 0.0, 1.0, 0.0, t[0][1], t[1][1],
+                               t[2][1], unused);
+                dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, 0.0, 0.0, 1.0, t[0][2], t[1][2],
+                               t[2][2], unused);
             }
 #pragma unroll
             for (int b = 0; b < N1; ++b)
@@ -475,12 +484,13 @@ k_diag_cells(Mesh m, Win w, Shape S, Material M, const double* __restrict__ qc, 
                     double gx = S.D[iq][a] * S.N[jq][b] * inv_h;
                     double gy = S.N[iq][a] * S.D[jq][b] * inv_h;
                     double val = S.N[iq][a] * S.N[jq][b];
-                    double x11, x12, y12, y22, unused0, unused1;
+                    double x11, x12, y12, y22;
                     if (MIEHE) {
-                        dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, gx, 0.0, 0.5 * gy, x11,
-                                       unused0, x12, unused1);
-                        dsig_split_pre(M.lam, M.mu, g_t, e, scale, tre, 0.0, gy, 0.5 * gx,
-                                       unused0, y22, y12, unused1);
+                        // u_x direction (gx, 0, gy/2), u_y direction (0, gy, gx/2)
+                        x11 = fma(t[0][2], 0.5 * gy, t[0][0] * gx);
+                        x12 = fma(t[2][2], 0.5 * gy, t[2][0] * gx);
+                        y22 = fma(t[1][2], 0.5 * gx, t[1][1] * gy);
+                        y12 = fma(t[2][2], 0.5 * gx, t[2][1] * gy);
                     } else {
                         x11 = g_t * (M.lam + 2.0 * M.mu) * gx;
                         x12 = g_t * M.mu * gy;
