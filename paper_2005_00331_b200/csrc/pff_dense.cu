@@ -48,18 +48,24 @@ __global__ void k_dense_jacobian(Mesh m, const double* __restrict__ gk,
     G[t] = acc;
 }
 
-// C = alpha A B + beta C (row-major; A m x k, B k x n): 64 x 64 tiles per
-// 256-thread block, 4 x 4 outputs per thread, k in steps of 16 through shared
-// memory.  beta == 0 ignores C's previous contents.
-constexpr int GT = 64, GK = 16;
+// C = alpha A B + beta C (row-major; A m x k, B k x n): GT x GT tiles per
+// 256-thread block, k in steps of 16 through shared memory.  beta == 0 ignores
+// C's previous contents.
+// Tile GT x GT (64: 4 x 4 outputs per thread; 32: 2 x 2 -- the small matrices of
+// the coarse maps, where 64-wide tiles leave a handful of blocks with long
+// serial chains).  Every output sums over k in increasing order: the tile size
+// does not change a bit of the result.
+constexpr int GK = 16;
+template <int GT>
 __global__ void __launch_bounds__(256)
 k_dgemm(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
         const double* __restrict__ B, int ldb, double beta, double* __restrict__ C, int ldc) {
+    constexpr int TO = GT / 16;   // outputs per thread and dimension
     __shared__ double As[GK][GT + 1];
     __shared__ double Bs[GK][GT + 1];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int row0 = blockIdx.y * GT, col0 = blockIdx.x * GT;
-    double acc[4][4] = {};
+    double acc[TO][TO] = {};
     for (int k0 = 0; k0 < k; k0 += GK) {
         for (int e = threadIdx.x; e < GT * GK; e += 256) {
             const int i = e / GK, kk = e - i * GK;          // A tile: rows i, cols kk
@@ -72,26 +78,26 @@ k_dgemm(int m, int n, int k, double alpha, const double* __restrict__ A, int lda
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < GK; ++kk) {
-            double a[4], b[4];
+            double a[TO], b[TO];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                a[u] = As[kk][ty * 4 + u];
-                b[u] = Bs[kk][tx * 4 + u];
+            for (int u = 0; u < TO; ++u) {
+                a[u] = As[kk][ty * TO + u];
+                b[u] = Bs[kk][tx * TO + u];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < TO; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+                for (int v = 0; v < TO; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int gi = row0 + ty * 4 + u;
+    for (int u = 0; u < TO; ++u) {
+        const int gi = row0 + ty * TO + u;
         if (gi >= m) continue;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int gj = col0 + tx * 4 + v;
+        for (int v = 0; v < TO; ++v) {
+            const int gj = col0 + tx * TO + v;
             if (gj >= n) continue;
             double* cp = C + (int64_t)gi * ldc + gj;
             *cp = beta == 0.0 ? alpha * acc[u][v] : fma(alpha, acc[u][v], beta * *cp);
@@ -161,8 +167,14 @@ cudaError_t launch_dense_jacobian(const Level& L, const double* gk, double* G, c
 cudaError_t launch_dgemm(int m, int n, int k, double alpha, const double* A, int lda, const double* B,
                          int ldb, double beta, double* C, int ldc, cudaStream_t s) {
     if (m <= 0 || n <= 0) return cudaSuccess;
-    dim3 grid((n + GT - 1) / GT, (m + GT - 1) / GT);
-    k_dgemm<<<grid, 256, 0, s>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    // fewer than half a wave of 64-wide tiles: the 32-wide form (four times the blocks)
+    if ((int64_t)((n + 63) / 64) * ((m + 63) / 64) < 64) {
+        dim3 grid((n + 31) / 32, (m + 31) / 32);
+        k_dgemm<32><<<grid, 256, 0, s>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    } else {
+        dim3 grid((n + 63) / 64, (m + 63) / 64);
+        k_dgemm<64><<<grid, 256, 0, s>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    }
     count_launches(1);
     return cudaGetLastError();
 }
