@@ -184,8 +184,11 @@ struct Sweep4Args {
 
 // ------------------------------------------------------------- tiled refresh
 // Per (strip, cell row) block [array][jq][cell c][iq] from the generic q-point
-// cache (k_refresh): the same quantities as k_refresh_gtan (the reference's
-// cache_tensors form, src/_kernels.py:517-548, weight w_jq w_iq h^2 folded in).
+// cache (k_refresh): the direction-independent part of the reference's
+// cache_tensors form (src/_kernels.py:517-548), weight w_jq w_iq h^2 folded in --
+// none: g w, the coupling vector (3), pc; Miehe: the 7-array eigen-frame form of
+// the Q2 sweep (pff_sweep.cu: +-g w, +-gamma w, cos / sin of twice the
+// eigen-angle, two eigen-frame coupling coefficients, pc).
 template <bool MIEHE>
 __global__ void k_refresh_tile4(Mesh m, Shape S, Material M, const double* __restrict__ qc,
                                 double* __restrict__ qt, int n_strips, int64_t qblock) {
