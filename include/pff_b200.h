@@ -69,7 +69,11 @@ int64_t pff_launch_counter(void);
  *   PFF_OPT_SWEEP_MIN_NSIDE: smallest Q2 mesh (cells per side) on the sweep
  *     kernel for levels created AFTER the call (a level keeps the layout it was
  *     created with); 0 = PFF_SWEEP_MIN_NSIDE or the default 64, minimum 4 */
-enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2, PFF_OPT_SWEEP_MIN_NSIDE = 3 };
+/*   PFF_OPT_SWEEP_COLRING: staging of the Q2 sweep's tangent block: 1 = the
+ *     single-buffered Gauss-column ring, 0 = two whole-row stages, -1 = the
+ *     measured per-mode default (the results are bitwise the same either way) */
+enum { PFF_OPT_GENERIC_APPLY = 1, PFF_OPT_SWEEP_ROWS = 2, PFF_OPT_SWEEP_MIN_NSIDE = 3,
+       PFF_OPT_SWEEP_COLRING = 4 };
 int pff_set_option(int key, int value);
 
 /* One mesh level (replaces DofMap + LinearizationState's static data,

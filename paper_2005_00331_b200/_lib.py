@@ -91,7 +91,7 @@ MODE_FULL, MODE_UU, MODE_PHIPHI, MODE_PHIROW = 0, 1, 2, 3
 FLAG_DIRICHLET, FLAG_ACTIVE = 1, 2
 LAYOUT_FULL, LAYOUT_UU, LAYOUT_PHI = 0, 1, 2
 CONS_SELECT, CONS_ZERO, CONS_COPY, CONS_EXCLUDE = 0, 1, 2, 3
-OPT_GENERIC_APPLY, OPT_SWEEP_ROWS, OPT_SWEEP_MIN_NSIDE = 1, 2, 3
+OPT_GENERIC_APPLY, OPT_SWEEP_ROWS, OPT_SWEEP_MIN_NSIDE, OPT_SWEEP_COLRING = 1, 2, 3, 4
 CHEB_FIRST, CHEB_LAST, CHEB_NOACC = 1, 2, 4
 SMOOTH_ADD_D0 = 1
 

@@ -53,6 +53,7 @@ int pff_set_option(int key, int value) {
         case PFF_OPT_GENERIC_APPLY: pff::set_generic_apply(value != 0); return 0;
         case PFF_OPT_SWEEP_ROWS: pff::set_sweep_rows_per_chunk(value); return 0;
         case PFF_OPT_SWEEP_MIN_NSIDE: pff::set_sweep_min_nside(value); return 0;
+        case PFF_OPT_SWEEP_COLRING: pff::set_sweep_colring(value); return 0;
     }
     return fail(PFF_E_ARG, "%s", "pff_set_option: unknown key");
 }

@@ -248,6 +248,7 @@ cudaError_t launch_flags(int64_t n, uint8_t* dir, uint8_t* act, uint8_t* flags, 
 // options (pff_set_option)
 void set_generic_apply(bool on);
 void set_sweep_rows_per_chunk(int rows);
+void set_sweep_colring(int mode);   // -1 auto (env / measured default), 0 row stages, 1 column ring
 
 // Q2 sweep kernel (pff_sweep.cu)
 cudaError_t launch_refresh_tiled(const Level& L, cudaStream_t s);

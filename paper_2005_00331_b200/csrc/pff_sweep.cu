@@ -779,8 +779,11 @@ struct LaunchCfg {
 
 // tangent-block staging per (mode, split): PFF_SWEEP_COLRING = 0 / 1 forces the row
 // stages / the column ring everywhere; default: the measured choice
+int g_colring = -1;   // pff_set_option(PFF_OPT_SWEEP_COLRING): -1 = env / default
+
 template <int MODE, bool MIEHE>
 bool use_colring() {
+    if (g_colring >= 0) return g_colring != 0;
     static int env = -2;
     if (env == -2) {
         const char* e = getenv("PFF_SWEEP_COLRING");
@@ -875,6 +878,7 @@ int g_rows_override = 0;
 }  // namespace
 
 void set_sweep_rows_per_chunk(int r) { g_rows_override = r; }
+void set_sweep_colring(int mode) { g_colring = mode < 0 ? -1 : (mode != 0); }
 
 static int g_min_nside = -1;   // -1: PFF_SWEEP_MIN_NSIDE or the default
 

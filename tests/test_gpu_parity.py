@@ -360,6 +360,56 @@ def test_sweep_miehe_regimes_vs_oracle(regime):
 
 
 @pytest.mark.parametrize("split", ["miehe", "none"])
+@pytest.mark.parametrize("level,rows", [(6, 0), (7, 5), (8, 0), (9, 64)])
+def test_sweep_column_ring_matches_row_stages_bitwise(split, level, rows):
+    """Both stagings of the tangent block (the single-buffered Gauss-column ring and the two
+    whole-row stages) run the same arithmetic: every mode, plain, fused and the fused
+    Chebyshev step, bit for bit."""
+    from paper_2005_00331_b200 import _lib
+    ost, x = O.baseline_state(2, level, split, seed=level + 1)
+    h = P.build_hierarchy(level, 2)
+    st = P.LinearizationState(h, level, ost.params, split=split)
+    st.set_solution(ost.U); st.set_phi_tilde(ost.phi_tilde); st.set_phi_old(ost.phi_old)
+    st.set_active(ost.active)
+    st.set_dirichlet_nodes(np.flatnonzero(ost.dirichlet))
+    st.refresh_cache()
+    assert st.uses_sweep_kernel()
+    n = st.n_scalar
+    xd = torch.from_numpy(x).cuda()
+    g = torch.Generator(device="cuda").manual_seed(level)
+    rhs = torch.rand(3 * n, dtype=torch.float64, device="cuda", generator=g)
+    invd = torch.rand(2 * n, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    acc0 = torch.rand(2 * n, dtype=torch.float64, device="cuda", generator=g)
+    outs = []
+    try:
+        _lib.set_option(_lib.OPT_SWEEP_ROWS, rows)
+        for ring in (0, 1):
+            _lib.set_option(_lib.OPT_SWEEP_COLRING, ring)
+            res = []
+            for mode, src, nout in ((0, xd, 3 * n), (1, xd[:2 * n], 2 * n), (2, xd[2 * n:], n),
+                                    (3, xd, n)):
+                y = torch.empty(nout, dtype=torch.float64, device="cuda")
+                st.apply_into(mode, src, y)
+                yf = torch.empty(nout, dtype=torch.float64, device="cuda")
+                st.apply_into(mode, src, yf, rhs[:nout])
+                res += [y, yf]
+            # one fused Chebyshev step on the u block (cr, d', acc)
+            cr = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+            dn = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+            acc = acc0.clone()
+            _lib.call("pff_apply_cheb_ex", st.bind(), _lib.MODE_UU, _lib.ptr(xd[:2 * n].contiguous()),
+                      _lib.ptr(dn), _lib.ptr(rhs[:2 * n].contiguous()), _lib.ptr(cr), _lib.ptr(invd),
+                      _lib.ptr(acc), 0.3, 0.7, _lib.CHEB_FIRST, _lib.stream_handle())
+            res += [cr, dn, acc]
+            outs.append([t.clone() for t in res])
+    finally:
+        _lib.set_option(_lib.OPT_SWEEP_COLRING, -1)
+        _lib.set_option(_lib.OPT_SWEEP_ROWS, 0)
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("split", ["miehe", "none"])
 @pytest.mark.parametrize("level", [6, 9])
 def test_pipelined_host_path_matches_device_path(split, level):
     """apply_* with a pinned host tensor runs the chunked H2D/compute/D2H
